@@ -1,0 +1,338 @@
+#!/usr/bin/env python
+"""Benchmark: RNN-T / W-RNNT loss + logits-gradient throughput on B200 (utterances/s).
+
+One step = one pass of the whole hot path over one batch: K1 (log-softmax normalizer + Populate gather),
+K2 (alpha/beta wavefront), K3 (fused gradient), the device loss sum and, for N > 1, the NCCL all-reduce of
+that sum.  Default workload: c3 = BASELINE.json configs[2] (B=32 per GPU, T=500, U=100, V=1024, fp32,
+plain RNN-T), weak scaling (32 utterances per GPU, global ids rank*32 + i).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--variant rnnt|force_final|allow_ignore]
+  python bench.py --impl reference ...   # the CPU oracle on the host cores (bounded sample)
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import dataclasses
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import workloads  # noqa: E402
+
+METRIC = "utterances/s loss+grad (B=32,T=500,U=100,V=1024 fp32); HBM GB/s vs peak"
+UNIT = "utt/s"
+FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback, used only if MEASURED_PEAKS.json is absent
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--variant", default=None)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-threads", type=int, default=16)
+    return ap.parse_args()
+
+
+def workload_desc(cfg, variant):
+    return (f"{cfg.name}: B={cfg.B}/GPU, Tmax={cfg.Tmax}, Umax={cfg.Umax}, V={cfg.V}, fp32 logits, "
+            f"{'RNN-T' if variant == 'rnnt' else 'W-RNNT ' + variant}"
+            f"{', variable lengths' if cfg.variable_lengths else ', full lengths'}")
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy bandwidth)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md; MEASURED_PEAKS.json absent)"
+
+
+def ncu_traffic(kernel: str, cfg_name: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu --set full capture."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        d = json.load(f)
+    ent = d.get(cfg_name, {}).get(kernel)
+    return None if ent is None else float(ent["dram_bytes_per_launch"])
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 50 ms while the timed region runs."""
+    Q = ("clocks.sm,clocks.max.sm,utilization.gpu,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "50",
+                 "-i", str(self.index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+            time.sleep(0.4)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        loaded = [r for r in self.rows if (num(r[2]) or 0) >= 50] or self.rows
+        sm = [num(r[0]) for r in loaded if num(r[0]) is not None]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in loaded for i in range(4) if r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": num(loaded[0][1]),
+                "reasons": reasons, "samples": len(self.rows), "samples_under_load": len(loaded)}
+
+
+# ------------------------------------------------------------------------------------------ CPU oracle
+def oracle_inputs(cfg, b_ids):
+    return workloads.problem(cfg, b_ids=b_ids)
+
+
+def oracle_sample(cfg, variant, nthreads, b_ids, pb=None):
+    """Time the CPU oracle (as it stands) on utterances b_ids of the workload, nthreads OpenMP threads."""
+    import oracle
+    pb = oracle_inputs(cfg, b_ids) if pb is None else pb
+    z = pb["logits"].numpy()
+    t0 = time.perf_counter()
+    oracle.batch(z, pb["targets"], pb["logit_lens"], pb["target_lens"], cfg.blank, variant, grad=True,
+                 nthreads=nthreads)
+    return time.perf_counter() - t0
+
+
+def host_cores():
+    return len(os.sched_getaffinity(0))
+
+
+def run_reference(args):
+    """--impl reference: the oracle on the host cores; each step = one utterance per thread."""
+    rank = int(os.environ.get("RANK", 0))
+    if rank != 0:
+        return
+    cfg = workloads.CONFIGS[args.config]
+    variant = args.variant or cfg.variant
+    threads = max(1, min(host_cores(), args.cpu_threads))
+    import oracle
+    oracle.build()
+    b_ids = [i % cfg.B for i in range(threads)]
+    pb = oracle_inputs(cfg, b_ids)                      # generated once, untimed
+    for _ in range(min(args.warmup, 1)):               # the oracle has no warm-up state: one step pages it in
+        oracle_sample(cfg, variant, threads, b_ids, pb)
+    times = [oracle_sample(cfg, variant, threads, b_ids, pb) for _ in range(args.steps)]
+    total = sum(times)
+    value = len(b_ids) * args.steps / total
+    sample = (f"{len(b_ids)} of the {cfg.B} utterances of {cfg.name} per step (one per thread), full "
+              f"loss+grad per utterance, {args.steps} steps")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": workload_desc(cfg, variant), "variant": variant},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------ GPU arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import paper_2303_10384_b200 as rb
+    from paper_2303_10384_b200 import dist as rdist
+
+    rank, world, local = rdist.init("nccl")
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    base = workloads.CONFIGS[args.config]
+    variant = args.variant or base.variant
+    gcfg = dataclasses.replace(base, B=base.B * world)           # weak scaling: B per GPU fixed
+    b_ids = rdist.contiguous_shard(gcfg.B, rank, world)
+    pb = workloads.problem(gcfg, b_ids=b_ids, device=dev)
+    z = pb["logits"]
+    B, Tmax, Up1, V = z.shape
+    Umax = Up1 - 1
+    targets = torch.from_numpy(pb["targets"]).to(dev)
+    T_b = torch.from_numpy(pb["logit_lens"]).to(dev)
+    U_b = torch.from_numpy(pb["target_lens"]).to(dev)
+    grads = torch.empty_like(z)                                  # out of place: logits stay fixed across steps
+    losses = torch.empty(B, dtype=torch.float32, device=dev)
+    loss_sum = torch.empty((), dtype=torch.float64, device=dev)
+    workspace = torch.empty(rb.rnnt_workspace_bytes(B, Tmax, Umax), dtype=torch.uint8, device=dev)
+
+    K, W = args.steps, args.warmup
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+    for row in evs:
+        for e in row:
+            e.record()  # create the CUDA handles
+    torch.cuda.synchronize()
+
+    def step(events=None):
+        rb.rnnt_loss_timed(z, targets, T_b, U_b, gcfg.blank, variant, events=events, grads=grads,
+                           losses=losses, workspace=workspace)
+        rb.rnnt_loss_sum(losses, out=loss_sum)
+        rdist.allreduce_loss_sum(loss_sum)
+
+    for _ in range(W):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        start.record()
+        for i in range(K):
+            step(evs[i])
+        end.record()
+        torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    ms_local = start.elapsed_time(end)
+    ms_total = rdist.max_over_ranks(ms_local, dev)
+    ms_step = ms_total / K
+    value = B * world / (ms_step / 1e3)
+
+    # per-kernel device durations inside the timed region
+    k_ms = {name: statistics.mean(evs[i][j].elapsed_time(evs[i][j + 1]) for i in range(K))
+            for j, name in enumerate(("k1_lse_gather", "k2_alpha_beta", "k3_grad"))}
+    T_np, U_np = pb["logit_lens"], pb["target_lens"]
+    valid_elems = int(sum(int(t) * (int(u) + 1) for t, u in zip(T_np, U_np))) * V
+    all_elems = B * Tmax * Up1 * V
+    k3_bytes = 8 * valid_elems + 4 * (all_elems - valid_elems)   # read + write valid, zero-write padding
+    k1_bytes = 4 * valid_elems
+    peak, peak_src = measured_peaks()
+    k3_gbs = k3_bytes / (k_ms["k3_grad"] / 1e3) / 1e9
+    k1_gbs = k1_bytes / (k_ms["k1_lse_gather"] / 1e3) / 1e9
+
+    # sanity: finite losses and the all-reduced sum
+    loss_total = float(loss_sum.item())
+
+    line = None
+    if rank == 0:
+        clk = clocks.summary()
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": workload_desc(base, variant), "variant": variant, "B_per_gpu": B,
+                       "global_batch": B * world, "parallelism": f"dp{world} (batch shards, NCCL all-reduce of "
+                       f"the fp64 loss sum)", "l2": f"inputs {z.numel() * 4 / 1e9:.2f} GB/GPU > 126 MB L2: no flush",
+                       "grads": "out of place"},
+            "roofline": {"bound": "hbm", "kernel": "k3_grad", "achieved": k3_gbs, "peak": peak, "unit": "GB/s",
+                         "frac": k3_gbs / peak, "traffic": ncu_traffic("k3_grad", args.config),
+                         "algorithmic_bytes_per_launch": k3_bytes, "peak_source": peak_src},
+            "kernels_ms": k_ms,
+            "kernel_gbs": {"k1_lse_gather": k1_gbs, "k3_grad": k3_gbs},
+            "kernel_frac_of_peak": {"k1_lse_gather": k1_gbs / peak, "k3_grad": k3_gbs / peak},
+            "step_frac_of_12B_roofline": (12 * valid_elems / (ms_step / 1e3) / 1e9) / peak,
+            "clocks": clk,
+            "gpu_launches": 4 * K,
+            "loss_sum_last_step": loss_total,
+        }
+
+    # ---- end to end through the host-buffer C-ABI entry point (pinned host in/out, copies in the timed region)
+    e2e = None
+    if not args.no_e2e:
+        zh = z.cpu().pin_memory()
+        gh = torch.empty_like(zh).pin_memory()
+        th = torch.from_numpy(pb["targets"]).contiguous().pin_memory()
+        Th = torch.from_numpy(pb["logit_lens"]).pin_memory()
+        Uh = torch.from_numpy(pb["target_lens"]).pin_memory()
+        lh = torch.empty(B, dtype=torch.float32).pin_memory()
+        del grads
+        torch.cuda.empty_cache()
+        dbuf = torch.empty(rb.rnnt_host_buffer_bytes(B, Tmax, Umax, V), dtype=torch.uint8, device=dev)
+        for _ in range(1):
+            rb.rnnt_loss_host(zh, th, Th, Uh, gcfg.blank, variant, losses_host=lh, grads_host=gh, device_buffer=dbuf)
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e_start.record()
+        for _ in range(args.e2e_steps):
+            rb.rnnt_loss_host(zh, th, Th, Uh, gcfg.blank, variant, losses_host=lh, grads_host=gh, device_buffer=dbuf)
+        e_end.record()
+        torch.cuda.synchronize()
+        e_ms = rdist.max_over_ranks(e_start.elapsed_time(e_end), dev) / args.e2e_steps
+        h2d = zh.numel() * 4 + th.numel() * 4 + Th.numel() * 4 + Uh.numel() * 4
+        d2h = gh.numel() * 4 + lh.numel() * 4
+        e2e = {"value": B * world / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": e_ms, "steps": args.e2e_steps,
+               "api": "rnnt_loss_host (pinned host buffers; chunked H2D / compute / D2H overlap)"}
+        del dbuf
+    if rank == 0:
+        line["e2e"] = e2e
+
+    # ---- CPU baseline: the oracle as it stands, on the host cores, rank 0 at N=1 only
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = max(1, min(host_cores(), args.cpu_threads))
+        ids = [i % base.B for i in range(threads)]
+        secs = oracle_sample(base, variant, threads, ids)
+        line["cpu_baseline"] = {"value": len(ids) / secs, "unit": UNIT, "cores": threads, "kind": "oracle",
+                                "sample": f"{len(ids)} utterances of {base.name} (one per OpenMP thread), full "
+                                          f"double-precision loss+grad, {secs:.1f} s wall",
+                                "host_cores_available": host_cores()}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

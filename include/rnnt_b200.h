@@ -1,0 +1,118 @@
+/*
+ * rnnt_b200.h -- C ABI of the B200 (sm_100a) RNN-T / W-RNNT loss + logits-gradient library.
+ *
+ * What is computed (PAPER.md = /root/reference/PAPER.md, cited P:<line>):
+ *   loss_b = -Fwd(L_b) = -log sum over complete alignment paths pi of the lattice L_b of
+ *            prod_{arcs a in pi} w(a)                              Eq.(1), P:54-56 ("negative forward scores")
+ *   L_b    = the Grid-Transducer lattice: a T_b x (U_b+1) grid whose horizontal (time) arcs emit <blank>
+ *            and whose vertical (unit) arcs emit y_{u+1}; a terminating <blank> arc leaves (T_b-1, U_b)
+ *                                                                   §2.3
+ *   w(a)   = softmax(logits[b,t,u,:])[label(a)]: the lattice is populated by indexed selection from the
+ *            log-probabilities tensor X = log_softmax(logits)       §2.1, §2.2 P:88 ("Populate")
+ *   W-RNNT adds weight-1 <eps> skip-frame arcs:                       §3.2, §4.3
+ *            initial skips (0,0) -> (t,0), 1 <= t <= T_b-1           ("from the initial state to any state
+ *                                                                      before non-<blank> emissions")
+ *            force-final:  (t,U_b) -> (T_b-1,U_b), 0 <= t <= T_b-2   ("point to the previous-to-final state")
+ *            allow-ignore: (t,U_b) -> final,       0 <= t <= T_b-2   ("point to the final state"),
+ *                          the ordinary terminating blank is kept.
+ *   grads  = d loss_b / d logits[b,t,u,v] (chain rule through the log-softmax; reading R8).
+ *
+ * Conventions shared by every entry point:
+ *   - All tensor pointers are DEVICE pointers owned by the caller unless the name ends in _host.  The
+ *     library allocates no device memory and keeps no state between calls; every call is asynchronous on
+ *     `stream` (a cudaStream_t passed as void*; NULL = the legacy default stream).
+ *   - logits  fp32 [B][Tmax][Umax+1][V], contiguous, V innermost.  Cells with t >= T_b or u > U_b are
+ *             padding: never read.
+ *   - targets int32 [B][Umax] (may be NULL when Umax == 0); targets[b][u], u < U_b, is unit u+1 of
+ *             utterance b and must lie in [0,V) and differ from `blank`.  Entries u >= U_b are never read.
+ *   - logit_lens / target_lens int32 [B]: 1 <= T_b <= Tmax, 0 <= U_b <= Umax.
+ *   - losses  fp32 [B] out: per-utterance -log P_b (no reduction; reading R10).
+ *   - grads   fp32 [B][Tmax][Umax+1][V] out, or NULL (loss only: the gradient pass is skipped).  grads
+ *             MAY EQUAL logits (in place: each element is read before it is overwritten) but must not
+ *             otherwise overlap it.  Padding cells receive exact zeros.
+ *   - grad_scale fp32 [B] or NULL (= 1): grads[b] are multiplied by grad_scale[b] (e.g. 1/B for a mean
+ *             reduction) inside the gradient pass, at no extra memory traffic.
+ *   - Data-dependent errors are NOT reported synchronously (that would need a device sync): an utterance
+ *     whose lengths or targets are out of range gets loss = NaN and all-zero grads.  An utterance whose
+ *     lattice has no path of non-zero probability (e.g. -inf logits) gets loss = +inf and zero grads.
+ *   - Argument errors detectable on the host (sizes, null pointers, workspace size, overlap) are returned
+ *     as a status before anything is launched.
+ *   - Limits: Umax + 1 <= 1024 (one CTA per utterance and direction in the alpha/beta wavefront);
+ *     element offsets are 64-bit (a single call may exceed 2^31 elements).
+ */
+#ifndef RNNT_B200_H
+#define RNNT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    RNNT_OK = 0,
+    RNNT_ERR_INVALID_ARG = 1,          /* bad size, null pointer, blank out of range, partial overlap */
+    RNNT_ERR_WORKSPACE_TOO_SMALL = 2,  /* workspace_bytes < rnnt_workspace_bytes(B, Tmax, Umax) */
+    RNNT_ERR_UNSUPPORTED = 3,          /* Umax + 1 > 1024 */
+    RNNT_ERR_CUDA = 4                  /* a CUDA launch / copy failed (cudaGetLastError) */
+} rnnt_status;
+
+typedef enum {
+    WRNNT_FORCE_FINAL = 0,   /* final skips land on (T_b-1, U_b): the last blank is still emitted */
+    WRNNT_ALLOW_IGNORE = 1   /* final skips land on the final state */
+} wrnnt_variant;
+
+/* Device workspace (bytes) one call needs for these padded sizes; 0 if the sizes are invalid.
+ * Holds, per (b,t,u) cell: log-softmax normalizer (fp32), blank/label log-probs (fp32 x2, anti-diagonal
+ * major), alpha and beta (fp64); per utterance: log P (fp64). About 28 B per cell. */
+size_t rnnt_workspace_bytes(int B, int Tmax, int Umax);
+
+/* Plain RNN-T loss (Eq.(1) over the §2.3 grid) and, if grads != NULL, its logits-gradient. */
+rnnt_status rnnt_loss(const float* logits, const int32_t* targets, const int32_t* logit_lens,
+                      const int32_t* target_lens, int B, int Tmax, int Umax, int V, int blank,
+                      float* losses, float* grads, const float* grad_scale,
+                      void* workspace, size_t workspace_bytes, void* stream);
+
+/* W-Transducer loss (§3.2 + §4.3) in the given variant; same arguments and conventions as rnnt_loss. */
+rnnt_status wrnnt_loss(const float* logits, const int32_t* targets, const int32_t* logit_lens,
+                       const int32_t* target_lens, int B, int Tmax, int Umax, int V, int blank,
+                       float* losses, float* grads, const float* grad_scale,
+                       void* workspace, size_t workspace_bytes, void* stream, wrnnt_variant variant);
+
+/* rnnt_loss / wrnnt_loss with per-kernel timing (the profiling hook bench.py uses).  variant: -1 = plain
+ * RNN-T, else a wrnnt_variant.  If events != NULL, events[0..3] are cudaEvent_t handles recorded on
+ * `stream` before K1 (log-softmax + gather), before K2 (alpha/beta wavefront), before K3 (gradient) and
+ * after K3, so cudaEventElapsedTime between consecutive events is each kernel's device duration. */
+rnnt_status rnnt_loss_timed(const float* logits, const int32_t* targets, const int32_t* logit_lens,
+                            const int32_t* target_lens, int B, int Tmax, int Umax, int V, int blank,
+                            float* losses, float* grads, const float* grad_scale,
+                            void* workspace, size_t workspace_bytes, void* stream, int variant,
+                            void* const* events);
+
+/* Deterministic fp64 sum of losses[0..B) into *loss_sum (device), fixed summation order for a given B.
+ * This is the per-rank operand of the cross-GPU all-reduce of the loss sum (BASELINE.json north_star (5)). */
+rnnt_status rnnt_loss_sum(const float* losses, int B, double* loss_sum, void* stream);
+
+/* Host-buffer entry point (the end-to-end path): logits_host / targets_host / lens_host / losses_host /
+ * grads_host are HOST pointers (pinned memory recommended; pageable works but serialises the copies).
+ * device_buffer must hold rnnt_host_buffer_bytes(...) bytes of device memory: it receives staged logits
+ * (and grads, in place) plus the workspace.  variant: -1 = plain RNN-T, else a wrnnt_variant.  Copies and
+ * compute are pipelined over chunks of utterances on `stream` and internal events; the call returns after
+ * enqueueing -- synchronize `stream` before reading the host outputs.  grads_host may be NULL (loss only). */
+size_t rnnt_host_buffer_bytes(int B, int Tmax, int Umax, int V);
+rnnt_status rnnt_loss_host(const float* logits_host, const int32_t* targets_host,
+                           const int32_t* logit_lens_host, const int32_t* target_lens_host,
+                           int B, int Tmax, int Umax, int V, int blank, int variant,
+                           float* losses_host, float* grads_host,
+                           void* device_buffer, size_t device_buffer_bytes, void* stream);
+
+const char* rnnt_status_string(rnnt_status status);
+
+/* Library version, e.g. "rnnt_b200 0.1 sm_100a". */
+const char* rnnt_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RNNT_B200_H */

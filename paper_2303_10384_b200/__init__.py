@@ -1,0 +1,193 @@
+"""B200-native RNN-T / W-RNNT loss + logits-gradient (arXiv 2303.10384 Grid-Transducer hot path).
+
+Thin ctypes binding over the C ABI in ``include/rnnt_b200.h`` (``lib/librnnt_b200.so``): argument
+marshalling only -- every step of the path runs in the sm_100a kernels.  PyTorch supplies device memory
+and the current CUDA stream.  There is no CPU fallback: importing this package without the built library
+raises, and the compute entry points require CUDA tensors.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+from ._build import LIB_PATH
+
+__all__ = ["rnnt_loss", "wrnnt_loss", "rnnt_loss_sum", "rnnt_loss_host", "rnnt_workspace_bytes",
+           "rnnt_host_buffer_bytes", "RnntError", "library", "LIB_PATH", "EXPORTS"]
+
+RNNT_OK = 0
+VARIANTS = {"rnnt": -1, "force_final": 0, "allow_ignore": 1}
+
+# Every symbol include/rnnt_b200.h declares.
+EXPORTS = ("rnnt_workspace_bytes", "rnnt_loss", "wrnnt_loss", "rnnt_loss_timed", "rnnt_loss_sum", "rnnt_host_buffer_bytes",
+           "rnnt_loss_host", "rnnt_status_string", "rnnt_version")
+
+
+class RnntError(RuntimeError):
+    pass
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+                          f"g.build()'` (nvcc, sm_100a). There is no CPU fallback.")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, I, S = ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t
+    lib.rnnt_workspace_bytes.argtypes = [I, I, I]
+    lib.rnnt_workspace_bytes.restype = S
+    common = [P, P, P, P, I, I, I, I, I, P, P, P, P, S, P]
+    lib.rnnt_loss.argtypes = common
+    lib.rnnt_loss.restype = I
+    lib.wrnnt_loss.argtypes = common + [I]
+    lib.wrnnt_loss.restype = I
+    lib.rnnt_loss_timed.argtypes = common + [I, P]
+    lib.rnnt_loss_timed.restype = I
+    lib.rnnt_loss_sum.argtypes = [P, I, P, P]
+    lib.rnnt_loss_sum.restype = I
+    lib.rnnt_host_buffer_bytes.argtypes = [I, I, I, I]
+    lib.rnnt_host_buffer_bytes.restype = S
+    lib.rnnt_loss_host.argtypes = [P, P, P, P, I, I, I, I, I, I, P, P, P, S, P]
+    lib.rnnt_loss_host.restype = I
+    lib.rnnt_status_string.argtypes = [I]
+    lib.rnnt_status_string.restype = ctypes.c_char_p
+    lib.rnnt_version.argtypes = []
+    lib.rnnt_version.restype = ctypes.c_char_p
+    return lib
+
+
+library = _load()
+
+
+def _check(status: int):
+    if status != RNNT_OK:
+        raise RnntError(library.rnnt_status_string(status).decode())
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def rnnt_workspace_bytes(B: int, Tmax: int, Umax: int) -> int:
+    return int(library.rnnt_workspace_bytes(B, Tmax, Umax))
+
+
+def rnnt_host_buffer_bytes(B: int, Tmax: int, Umax: int, V: int) -> int:
+    return int(library.rnnt_host_buffer_bytes(B, Tmax, Umax, V))
+
+
+def _as_i32(x, device):
+    if not isinstance(x, torch.Tensor):
+        x = torch.as_tensor(x)
+    return x.to(device=device, dtype=torch.int32).contiguous()
+
+
+def _call(fn_variant, logits, targets, logit_lens, target_lens, blank, grads, grad_scale, losses, workspace,
+          stream, events=None):
+    if not (isinstance(logits, torch.Tensor) and logits.is_cuda and logits.dtype == torch.float32):
+        raise TypeError("logits must be a CUDA float32 tensor [B, Tmax, Umax+1, V] (no CPU fallback)")
+    if not logits.is_contiguous():
+        raise ValueError("logits must be contiguous")
+    B, Tmax, Up1, V = logits.shape
+    Umax = Up1 - 1
+    dev = logits.device
+    targets = _as_i32(targets, dev).reshape(B, Umax) if Umax > 0 else None
+    logit_lens = _as_i32(logit_lens, dev)
+    target_lens = _as_i32(target_lens, dev)
+    if losses is None:
+        losses = torch.empty(B, dtype=torch.float32, device=dev)
+    if isinstance(grads, str) and grads == "inplace":
+        grads = logits
+    elif grads is True:
+        grads = torch.empty_like(logits)
+    elif grads is False:
+        grads = None
+    if grads is not None and (grads.shape != logits.shape or not grads.is_contiguous()):
+        raise ValueError("grads must be contiguous and shaped like logits")
+    if grad_scale is not None:
+        grad_scale = grad_scale.to(device=dev, dtype=torch.float32).contiguous()
+    need = rnnt_workspace_bytes(B, Tmax, Umax)
+    if workspace is None:
+        workspace = torch.empty(max(need, 1), dtype=torch.uint8, device=dev)
+    args = [_ptr(logits), _ptr(targets), _ptr(logit_lens), _ptr(target_lens), B, Tmax, Umax, V, int(blank),
+            _ptr(losses), _ptr(grads), _ptr(grad_scale), _ptr(workspace), workspace.numel(), _stream(stream)]
+    if events is not None:
+        handles = [e.cuda_event for e in events]
+        if len(handles) != 4 or not all(handles):
+            raise ValueError("need 4 recorded torch.cuda.Events")
+        arr = (ctypes.c_void_p * 4)(*handles)
+        _check(library.rnnt_loss_timed(*args, fn_variant, ctypes.cast(arr, ctypes.c_void_p)))
+    elif fn_variant < 0:
+        _check(library.rnnt_loss(*args))
+    else:
+        _check(library.wrnnt_loss(*args, fn_variant))
+    return losses, grads
+
+
+def rnnt_loss(logits, targets, logit_lens, target_lens, blank=0, grads=True, grad_scale=None, losses=None,
+              workspace=None, stream=None):
+    """Per-utterance RNN-T losses and d loss_b / d logits (Eq.(1), §2.3 Grid-Transducer).
+
+    grads: True (new tensor), "inplace" (overwrite logits), False (loss only) or a preallocated tensor.
+    Returns (losses fp32 [B], grads or None).  Asynchronous on the current CUDA stream.
+    """
+    return _call(-1, logits, targets, logit_lens, target_lens, blank, grads, grad_scale, losses, workspace,
+                 stream)
+
+
+def wrnnt_loss(logits, targets, logit_lens, target_lens, blank=0, variant="force_final", grads=True,
+               grad_scale=None, losses=None, workspace=None, stream=None):
+    """W-Transducer losses (§3.2; variant "force_final" P:116 or "allow_ignore" P:167)."""
+    return _call(VARIANTS[variant], logits, targets, logit_lens, target_lens, blank, grads, grad_scale, losses,
+                 workspace, stream)
+
+
+def loss(logits, targets, logit_lens, target_lens, blank=0, variant="rnnt", **kw):
+    """Dispatch on variant name: "rnnt" | "force_final" | "allow_ignore"."""
+    if variant == "rnnt":
+        return rnnt_loss(logits, targets, logit_lens, target_lens, blank, **kw)
+    return wrnnt_loss(logits, targets, logit_lens, target_lens, blank, variant, **kw)
+
+
+def rnnt_loss_timed(logits, targets, logit_lens, target_lens, blank=0, variant="rnnt", events=None, grads=True,
+                    grad_scale=None, losses=None, workspace=None, stream=None):
+    """rnnt_loss / wrnnt_loss recording 4 torch.cuda.Events around K1, K2, K3 (events must be recorded once
+    beforehand so that their CUDA handles exist)."""
+    return _call(VARIANTS[variant], logits, targets, logit_lens, target_lens, blank, grads, grad_scale, losses,
+                 workspace, stream, events)
+
+
+def rnnt_loss_sum(losses, out=None, stream=None):
+    """Deterministic fp64 device sum of the per-utterance losses (operand of the cross-rank all-reduce)."""
+    if out is None:
+        out = torch.empty((), dtype=torch.float64, device=losses.device)
+    _check(library.rnnt_loss_sum(_ptr(losses), losses.numel(), _ptr(out), _stream(stream)))
+    return out
+
+
+def rnnt_loss_host(logits_host, targets_host, logit_lens_host, target_lens_host, blank=0, variant="rnnt",
+                   losses_host=None, grads_host=None, device_buffer=None, stream=None):
+    """Host-buffer entry point: host (ideally pinned) CPU tensors in and out; copies overlap compute.
+
+    Returns (losses_host, grads_host).  Synchronize the stream before reading them.
+    """
+    B, Tmax, Up1, V = logits_host.shape
+    Umax = Up1 - 1
+    if losses_host is None:
+        losses_host = torch.empty(B, dtype=torch.float32, pin_memory=True)
+    need = rnnt_host_buffer_bytes(B, Tmax, Umax, V)
+    if device_buffer is None:
+        device_buffer = torch.empty(need, dtype=torch.uint8, device="cuda")
+    tg = targets_host if Umax > 0 else None
+    _check(library.rnnt_loss_host(_ptr(logits_host), _ptr(tg), _ptr(logit_lens_host), _ptr(target_lens_host),
+                                  B, Tmax, Umax, V, int(blank), VARIANTS[variant], _ptr(losses_host),
+                                  _ptr(grads_host), _ptr(device_buffer), device_buffer.numel(),
+                                  _stream(stream)))
+    return losses_host, grads_host

@@ -1,0 +1,243 @@
+// rnnt_api.cu -- the C ABI (include/rnnt_b200.h): host-side argument checks, workspace carve-up, and the
+// K1 -> K2 -> K3 launch sequence on the caller's stream; plus the chunk-pipelined host-buffer path.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "rnnt_b200.h"
+
+using rnnt::Problem;
+using rnnt::Workspace;
+
+namespace {
+
+bool ranges_overlap(const void* a, size_t na, const void* b, size_t nb) {
+    const uintptr_t pa = reinterpret_cast<uintptr_t>(a), pb = reinterpret_cast<uintptr_t>(b);
+    return pa < pb + nb && pb < pa + na;
+}
+
+rnnt_status check_sizes(int B, int Tmax, int Umax, int V, int blank) {
+    if (B < 0 || Tmax < 1 || Umax < 0 || V < 2 || blank < 0 || blank >= V) return RNNT_ERR_INVALID_ARG;
+    if (Umax + 1 > rnnt::kMaxUp1) return RNNT_ERR_UNSUPPORTED;
+    return RNNT_OK;
+}
+
+rnnt_status run(const float* logits, const int32_t* targets, const int32_t* logit_lens,
+                const int32_t* target_lens, int B, int Tmax, int Umax, int V, int blank, float* losses,
+                float* grads, const float* grad_scale, void* workspace, size_t workspace_bytes, void* stream,
+                int variant, void* const* events = nullptr) {
+    rnnt_status st = check_sizes(B, Tmax, Umax, V, blank);
+    if (st != RNNT_OK) return st;
+    if (variant < rnnt::kRnnt || variant > rnnt::kAllowIgnore) return RNNT_ERR_INVALID_ARG;
+    if (B == 0) return RNNT_OK;  // empty batch: nothing to do
+    if (!logits || !logit_lens || !target_lens || !losses || !workspace) return RNNT_ERR_INVALID_ARG;
+    if (Umax > 0 && !targets) return RNNT_ERR_INVALID_ARG;
+    if (workspace_bytes < rnnt::workspace_bytes(B, Tmax, Umax)) return RNNT_ERR_WORKSPACE_TOO_SMALL;
+    const size_t tensor_bytes = sizeof(float) * static_cast<size_t>(B) * Tmax * (Umax + 1) * V;
+    if (grads && grads != logits && ranges_overlap(grads, tensor_bytes, logits, tensor_bytes))
+        return RNNT_ERR_INVALID_ARG;
+
+    Problem p{logits, targets, logit_lens, target_lens, B, Tmax, Umax, V, blank, variant, losses, grads,
+              grad_scale};
+    const Workspace w = rnnt::carve(workspace, B, Tmax, Umax);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    auto mark = [&](int i) {
+        return !events || cudaEventRecord(static_cast<cudaEvent_t>(events[i]), s) == cudaSuccess;
+    };
+    if (!mark(0) || rnnt::launch_k1_lse_gather(p, w, s) != cudaSuccess) return RNNT_ERR_CUDA;
+    if (!mark(1) || rnnt::launch_k2_alpha_beta(p, w, s) != cudaSuccess) return RNNT_ERR_CUDA;
+    if (!mark(2) || (grads && rnnt::launch_k3_grad(p, w, s) != cudaSuccess)) return RNNT_ERR_CUDA;
+    if (!mark(3)) return RNNT_ERR_CUDA;
+    return RNNT_OK;
+}
+
+// Chunk size of the host path: enough chunks to overlap H2D(c+1) / compute(c) / D2H(c-1).
+int host_chunk(int B) { return std::max(1, (B + 7) / 8); }
+
+}  // namespace
+
+extern "C" {
+
+size_t rnnt_workspace_bytes(int B, int Tmax, int Umax) {
+    if (B < 0 || Tmax < 1 || Umax < 0) return 0;
+    return rnnt::workspace_bytes(B, Tmax, Umax);
+}
+
+rnnt_status rnnt_loss(const float* logits, const int32_t* targets, const int32_t* logit_lens,
+                      const int32_t* target_lens, int B, int Tmax, int Umax, int V, int blank, float* losses,
+                      float* grads, const float* grad_scale, void* workspace, size_t workspace_bytes,
+                      void* stream) {
+    return run(logits, targets, logit_lens, target_lens, B, Tmax, Umax, V, blank, losses, grads, grad_scale,
+               workspace, workspace_bytes, stream, rnnt::kRnnt);
+}
+
+rnnt_status wrnnt_loss(const float* logits, const int32_t* targets, const int32_t* logit_lens,
+                       const int32_t* target_lens, int B, int Tmax, int Umax, int V, int blank, float* losses,
+                       float* grads, const float* grad_scale, void* workspace, size_t workspace_bytes,
+                       void* stream, wrnnt_variant variant) {
+    int v;
+    if (variant == WRNNT_FORCE_FINAL)
+        v = rnnt::kForceFinal;
+    else if (variant == WRNNT_ALLOW_IGNORE)
+        v = rnnt::kAllowIgnore;
+    else
+        return RNNT_ERR_INVALID_ARG;
+    return run(logits, targets, logit_lens, target_lens, B, Tmax, Umax, V, blank, losses, grads, grad_scale,
+               workspace, workspace_bytes, stream, v);
+}
+
+rnnt_status rnnt_loss_timed(const float* logits, const int32_t* targets, const int32_t* logit_lens,
+                            const int32_t* target_lens, int B, int Tmax, int Umax, int V, int blank,
+                            float* losses, float* grads, const float* grad_scale, void* workspace,
+                            size_t workspace_bytes, void* stream, int variant, void* const* events) {
+    if (variant < -1 || variant > 1) return RNNT_ERR_INVALID_ARG;
+    const int kind = (variant < 0) ? rnnt::kRnnt : (variant == 0 ? rnnt::kForceFinal : rnnt::kAllowIgnore);
+    return run(logits, targets, logit_lens, target_lens, B, Tmax, Umax, V, blank, losses, grads, grad_scale,
+               workspace, workspace_bytes, stream, kind, events);
+}
+
+rnnt_status rnnt_loss_sum(const float* losses, int B, double* loss_sum, void* stream) {
+    if (B < 0 || !loss_sum || (B > 0 && !losses)) return RNNT_ERR_INVALID_ARG;
+    if (rnnt::launch_loss_sum(losses, B, loss_sum, static_cast<cudaStream_t>(stream)) != cudaSuccess)
+        return RNNT_ERR_CUDA;
+    return RNNT_OK;
+}
+
+// Device buffer of the host path: [logits/grads staging B*cells*V fp32][targets][T_b][U_b][losses]
+// [workspace for one chunk per chunk slot].  All 256-byte aligned.
+size_t rnnt_host_buffer_bytes(int B, int Tmax, int Umax, int V) {
+    if (check_sizes(B, Tmax, Umax, V, 0) != RNNT_OK) return 0;
+    const int64_t cells = static_cast<int64_t>(Tmax) * (Umax + 1);
+    const int C = host_chunk(B);
+    const int nchunks = (B + C - 1) / C;
+    size_t s = 0;
+    s += rnnt::align256(sizeof(float) * B * cells * V);
+    s += rnnt::align256(sizeof(int32_t) * B * std::max(Umax, 1));
+    s += 2 * rnnt::align256(sizeof(int32_t) * B);
+    s += rnnt::align256(sizeof(float) * B);
+    s += static_cast<size_t>(nchunks) * rnnt::workspace_bytes(C, Tmax, Umax);
+    return s;
+}
+
+rnnt_status rnnt_loss_host(const float* logits_host, const int32_t* targets_host, const int32_t* logit_lens_host,
+                           const int32_t* target_lens_host, int B, int Tmax, int Umax, int V, int blank,
+                           int variant, float* losses_host, float* grads_host, void* device_buffer,
+                           size_t device_buffer_bytes, void* stream) {
+    rnnt_status st = check_sizes(B, Tmax, Umax, V, blank);
+    if (st != RNNT_OK) return st;
+    if (variant < -1 || variant > 1) return RNNT_ERR_INVALID_ARG;
+    if (B == 0) return RNNT_OK;
+    if (!logits_host || !logit_lens_host || !target_lens_host || !losses_host || !device_buffer)
+        return RNNT_ERR_INVALID_ARG;
+    if (Umax > 0 && !targets_host) return RNNT_ERR_INVALID_ARG;
+    if (device_buffer_bytes < rnnt_host_buffer_bytes(B, Tmax, Umax, V)) return RNNT_ERR_WORKSPACE_TOO_SMALL;
+    const int kind = (variant < 0) ? rnnt::kRnnt : (variant == 0 ? rnnt::kForceFinal : rnnt::kAllowIgnore);
+
+    const int64_t cells = static_cast<int64_t>(Tmax) * (Umax + 1);
+    const int64_t utt_elems = cells * V;
+    char* p = static_cast<char*>(device_buffer);
+    float* d_logits = reinterpret_cast<float*>(p);
+    p += rnnt::align256(sizeof(float) * B * utt_elems);
+    int32_t* d_targets = reinterpret_cast<int32_t*>(p);
+    p += rnnt::align256(sizeof(int32_t) * B * std::max(Umax, 1));
+    int32_t* d_T = reinterpret_cast<int32_t*>(p);
+    p += rnnt::align256(sizeof(int32_t) * B);
+    int32_t* d_U = reinterpret_cast<int32_t*>(p);
+    p += rnnt::align256(sizeof(int32_t) * B);
+    float* d_losses = reinterpret_cast<float*>(p);
+    p += rnnt::align256(sizeof(float) * B);
+    const int C = host_chunk(B);
+    const int nchunks = (B + C - 1) / C;
+    const size_t ws_chunk = rnnt::workspace_bytes(C, Tmax, Umax);
+
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t ev_start = nullptr, ev_done = nullptr;
+    cudaEvent_t* ev_in = new cudaEvent_t[nchunks]();
+    cudaEvent_t* ev_out = new cudaEvent_t[nchunks]();
+    rnnt_status ret = RNNT_OK;
+    auto ok = [&](cudaError_t e) {
+        if (e != cudaSuccess && ret == RNNT_OK) ret = RNNT_ERR_CUDA;
+        return e == cudaSuccess;
+    };
+    do {
+        if (!ok(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking))) break;
+        if (!ok(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking))) break;
+        if (!ok(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming))) break;
+        if (!ok(cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming))) break;
+        bool good = true;
+        for (int c = 0; c < nchunks && good; ++c)
+            good = ok(cudaEventCreateWithFlags(&ev_in[c], cudaEventDisableTiming)) &&
+                   ok(cudaEventCreateWithFlags(&ev_out[c], cudaEventDisableTiming));
+        if (!good) break;
+        // Small inputs first, on the caller's stream; the copy streams start after prior work on it.
+        if (!ok(cudaEventRecord(ev_start, s))) break;
+        if (!ok(cudaStreamWaitEvent(h2d, ev_start, 0))) break;
+        if (!ok(cudaStreamWaitEvent(d2h, ev_start, 0))) break;
+        if (Umax > 0 && !ok(cudaMemcpyAsync(d_targets, targets_host, sizeof(int32_t) * B * Umax,
+                                            cudaMemcpyHostToDevice, s)))
+            break;
+        if (!ok(cudaMemcpyAsync(d_T, logit_lens_host, sizeof(int32_t) * B, cudaMemcpyHostToDevice, s))) break;
+        if (!ok(cudaMemcpyAsync(d_U, target_lens_host, sizeof(int32_t) * B, cudaMemcpyHostToDevice, s))) break;
+        // H2D(c) on h2d  ->  K1..K3(c) on s  ->  D2H(c) on d2h; chunks own disjoint staging, so no WAR hazards.
+        for (int c = 0; c < nchunks && good; ++c) {
+            const int b0 = c * C, nb = std::min(C, B - b0);
+            const size_t bytes = sizeof(float) * nb * utt_elems;
+            good = ok(cudaMemcpyAsync(d_logits + b0 * utt_elems, logits_host + b0 * utt_elems, bytes,
+                                      cudaMemcpyHostToDevice, h2d)) &&
+                   ok(cudaEventRecord(ev_in[c], h2d));
+        }
+        for (int c = 0; c < nchunks && good; ++c) {
+            const int b0 = c * C, nb = std::min(C, B - b0);
+            good = ok(cudaStreamWaitEvent(s, ev_in[c], 0));
+            if (!good) break;
+            void* ws = p + static_cast<size_t>(c) * ws_chunk;
+            float* zc = d_logits + b0 * utt_elems;
+            rnnt_status r = run(zc, d_targets + static_cast<int64_t>(b0) * Umax, d_T + b0, d_U + b0, nb, Tmax,
+                                Umax, V, blank, d_losses + b0, grads_host ? zc : nullptr, nullptr, ws, ws_chunk,
+                                s, kind);
+            if (r != RNNT_OK) {
+                ret = r;
+                good = false;
+                break;
+            }
+            good = ok(cudaEventRecord(ev_out[c], s)) && ok(cudaStreamWaitEvent(d2h, ev_out[c], 0));
+            if (good && grads_host)
+                good = ok(cudaMemcpyAsync(grads_host + b0 * utt_elems, zc, sizeof(float) * nb * utt_elems,
+                                          cudaMemcpyDeviceToHost, d2h));
+        }
+        if (!good) break;
+        if (!ok(cudaMemcpyAsync(losses_host, d_losses, sizeof(float) * B, cudaMemcpyDeviceToHost, s))) break;
+        if (!ok(cudaEventRecord(ev_done, d2h))) break;
+        ok(cudaStreamWaitEvent(s, ev_done, 0));
+    } while (false);
+    // Destroying streams/events with pending work is legal: resources are released on completion.
+    for (int c = 0; c < nchunks; ++c) {
+        if (ev_in[c]) cudaEventDestroy(ev_in[c]);
+        if (ev_out[c]) cudaEventDestroy(ev_out[c]);
+    }
+    delete[] ev_in;
+    delete[] ev_out;
+    if (ev_start) cudaEventDestroy(ev_start);
+    if (ev_done) cudaEventDestroy(ev_done);
+    if (h2d) cudaStreamDestroy(h2d);
+    if (d2h) cudaStreamDestroy(d2h);
+    return ret;
+}
+
+const char* rnnt_status_string(rnnt_status status) {
+    switch (status) {
+        case RNNT_OK: return "RNNT_OK";
+        case RNNT_ERR_INVALID_ARG: return "RNNT_ERR_INVALID_ARG: invalid argument";
+        case RNNT_ERR_WORKSPACE_TOO_SMALL: return "RNNT_ERR_WORKSPACE_TOO_SMALL: workspace too small";
+        case RNNT_ERR_UNSUPPORTED: return "RNNT_ERR_UNSUPPORTED: Umax + 1 > 1024";
+        case RNNT_ERR_CUDA: return "RNNT_ERR_CUDA: CUDA launch or copy failed";
+    }
+    return "unknown rnnt_status";
+}
+
+const char* rnnt_version(void) { return "rnnt_b200 0.1 sm_100a"; }
+
+}  // extern "C"

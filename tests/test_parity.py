@@ -1,0 +1,277 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by element, on the same seeded
+inputs.  Bar (BASELINE.json north_star): loss within 1e-5 relative (floor |L| >= 1, DESIGN.md reading
+R19), grads within 1e-4 absolute.  Full-size configs (c3, c4) run in the launch configuration bench.py
+times and compare sampled utterances; invariants cover the rest."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import workloads
+
+pytestmark = pytest.mark.gpu
+
+LOSS_RTOL = 1e-5
+GRAD_ATOL = 1e-4
+VARIANTS = ("rnnt", "force_final", "allow_ignore")
+
+
+@pytest.fixture(scope="module")
+def rb():
+    import paper_2303_10384_b200
+    return paper_2303_10384_b200
+
+
+def _threads():
+    import os
+    return max(1, len(os.sched_getaffinity(0)))
+
+
+def _gpu(rb, pb, variant, grads=True, grad_scale=None, logits=None):
+    z = pb["logits"].cuda() if logits is None else logits
+    l, g = rb.loss(z, pb["targets"], pb["logit_lens"], pb["target_lens"], pb["blank"], variant, grads=grads,
+                   grad_scale=grad_scale)
+    torch.cuda.synchronize()
+    return l.cpu().numpy().astype(np.float64), (None if g is None else g.cpu().numpy())
+
+
+def _oracle(pb, variant, z=None):
+    z = pb["logits"].numpy() if z is None else z
+    return oracle.batch(z, pb["targets"], pb["logit_lens"], pb["target_lens"], pb["blank"], variant,
+                        nthreads=_threads())
+
+
+def _assert_close(l, g, ref_l, ref_g, what=""):
+    both_inf = np.isinf(l) & np.isinf(ref_l) & (np.sign(l) == np.sign(ref_l))
+    rel = np.where(both_inf, 0.0, np.abs(l - ref_l) / np.maximum(np.abs(ref_l), 1.0))
+    assert np.all(np.isfinite(rel)) and rel.max() <= LOSS_RTOL, (what, rel.max(), l, ref_l)
+    if g is not None:
+        err = np.abs(g.astype(np.float64) - ref_g).max()
+        assert err <= GRAD_ATOL, (what, err)
+
+
+# ---------------------------------------------------------------------------------------------- c1
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_fig1_toy(rb, variant):
+    """c1: Fig.1 toy, N(0,1) logits and uniform logits (exact enumerated values, golden file)."""
+    pb = workloads.problem(workloads.CONFIGS["c1"])
+    _assert_close(*_gpu(rb, pb, variant), *_oracle(pb, variant), "c1")
+    pb["logits"].zero_()
+    l, g = _gpu(rb, pb, variant)
+    exact = {"rnnt": 5 / 2048, "force_final": 229 / 2048, "allow_ignore": 697 / 2048}[variant]
+    assert abs(l[0] + math.log(exact)) <= 1e-5 * max(1, abs(math.log(exact)))
+
+
+# --------------------------------------------------------------------------------- random shapes
+SHAPES = [  # (B, Tmax, Umax, V, blank) -- several tiles of 32 threads / 128 float4, ragged tails
+    (3, 9, 4, 8, 0), (4, 33, 31, 129, 128), (2, 70, 40, 260, 77), (5, 41, 63, 1000, 999),
+    (3, 17, 96, 64, 5), (2, 120, 200, 36, 3), (6, 5, 2, 2, 1), (2, 300, 33, 512, 0)]
+
+
+@pytest.mark.parametrize("shape", SHAPES, ids=lambda s: "B{}_T{}_U{}_V{}_b{}".format(*s))
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_random_shapes(rb, shape, variant):
+    B, T, U, V, blank = shape
+    cfg = workloads.random_config(B, T, U, V, seed=sum(shape), blank=blank, variant=variant)
+    pb = workloads.problem(cfg)
+    _assert_close(*_gpu(rb, pb, variant), *_oracle(pb, variant), cfg.name)
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_peaky_logits(rb, variant):
+    """Scale-6 logits push occupancies to ~1, where fp32 alpha/beta would fail (reading R11)."""
+    cfg = workloads.random_config(3, 150, 40, 128, seed=12, variant=variant)
+    pb = workloads.problem(cfg, scale=6.0)
+    _assert_close(*_gpu(rb, pb, variant), *_oracle(pb, variant), "peaky")
+
+
+# ---------------------------------------------------------------------------------------------- c2
+def test_c2_full(rb):
+    """c2: B=16, T=200, U=50, V=256, variable lengths, compared in full."""
+    pb = workloads.problem(workloads.CONFIGS["c2"])
+    _assert_close(*_gpu(rb, pb, "rnnt"), *_oracle(pb, "rnnt"), "c2")
+
+
+# ------------------------------------------------------------------------------------------ c3 / c4
+def _full_size_sampled(rb, cfg_name, variant, sample=(0, 17, 31)):
+    cfg = workloads.CONFIGS[cfg_name]
+    pb = workloads.problem(cfg, device="cuda")        # the full batch, generated on the device
+    z = pb["logits"]
+    zs = z[list(sample)].cpu().numpy()                # oracle inputs: the same values, copied before the call
+    l, g = rb.loss(z, pb["targets"], pb["logit_lens"], pb["target_lens"], cfg.blank, variant,
+                   grads="inplace")                   # in place, as c5 must run
+    torch.cuda.synchronize()
+    sub = dict(pb, targets=pb["targets"][list(sample)], logit_lens=pb["logit_lens"][list(sample)],
+               target_lens=pb["target_lens"][list(sample)])
+    ref_l, ref_g = _oracle(sub, variant, z=zs)
+    lc = l.cpu().numpy().astype(np.float64)
+    gs = g[list(sample)].cpu().numpy()
+    _assert_close(lc[list(sample)], gs, ref_l, ref_g, cfg_name)
+    # invariants at full size: every loss finite and positive; sum_v grad = 0 for every row of every utterance
+    assert np.all(np.isfinite(lc))
+    row_sums = g.sum(dim=-1).abs().max().item()
+    assert row_sums < 1e-4
+    del z, g
+    torch.cuda.empty_cache()
+
+
+def test_c3_full_size_sampled(rb):
+    _full_size_sampled(rb, "c3", "rnnt")
+
+
+@pytest.mark.parametrize("variant", ("force_final", "allow_ignore"))
+def test_c4_full_size_sampled(rb, variant):
+    _full_size_sampled(rb, "c4", variant, sample=(1, 20))
+
+
+# ------------------------------------------------------------------------------------- edge cases
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_degenerate_lengths(rb, variant):
+    """U_b = 0, T_b = 1, U_b > T_b, T_b = Tmax with U_b = 0, in one padded batch."""
+    rng = np.random.default_rng(1)
+    B, Tmax, Umax, V = 6, 12, 20, 33
+    z = torch.from_numpy(rng.standard_normal((B, Tmax, Umax + 1, V)).astype(np.float32))
+    T_b = np.array([1, 1, 12, 3, 12, 7], np.int32)
+    U_b = np.array([0, 20, 0, 20, 20, 5], np.int32)
+    y = rng.integers(1, V, size=(B, Umax)).astype(np.int32)
+    pb = {"logits": z, "targets": y, "logit_lens": T_b, "target_lens": U_b, "blank": 0}
+    _assert_close(*_gpu(rb, pb, variant), *_oracle(pb, variant), "degenerate")
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_nan_padding_never_read(rb, variant):
+    """NaN in every padded cell: losses match and padded grads are exactly zero (K1 never reads them)."""
+    cfg = workloads.random_config(4, 60, 25, 96, seed=4, variant=variant)
+    pb = workloads.problem(cfg, pad_value=float("nan"))
+    l, g = _gpu(rb, pb, variant)
+    ref_l, ref_g = _oracle(pb, variant)
+    _assert_close(l, g, ref_l, ref_g, "nanpad")
+    for b in range(cfg.B):
+        T, U = pb["logit_lens"][b], pb["target_lens"][b]
+        assert not g[b, T:].any() and not g[b, :, U + 1:].any()
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_misaligned_and_odd_v(rb, variant):
+    """A logits base offset by 4 bytes and an odd V force the scalar (non-float4) path."""
+    cfg = workloads.random_config(3, 30, 9, 130, seed=8, variant=variant)
+    pb = workloads.problem(cfg)
+    flat = torch.empty(pb["logits"].numel() + 1, dtype=torch.float32, device="cuda")
+    z = flat[1:].view(pb["logits"].shape)
+    z.copy_(pb["logits"].cuda())
+    _assert_close(*_gpu(rb, pb, variant, logits=z), *_oracle(pb, variant), "misaligned")
+    cfg = workloads.random_config(3, 30, 9, 131, seed=9, variant=variant, blank=130)
+    pb = workloads.problem(cfg)
+    _assert_close(*_gpu(rb, pb, variant), *_oracle(pb, variant), "oddV")
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_minus_inf_logits_and_no_path(rb, variant):
+    rng = np.random.default_rng(2)
+    B, Tmax, Umax, V = 3, 6, 3, 5
+    zn = rng.standard_normal((B, Tmax, Umax + 1, V)).astype(np.float32)
+    zn[0, 0, 0, 0] = -np.inf          # blank forbidden at (0,0) of utterance 0
+    zn[1, :, :, 0] = -np.inf          # utterance 1: no blank anywhere -> no path
+    zn[2, 2, 1, :] = -np.inf          # utterance 2: an all -inf row
+    T_b = np.array([6, 4, 5], np.int32)
+    U_b = np.array([3, 2, 3], np.int32)
+    y = rng.integers(1, V, size=(B, Umax)).astype(np.int32)
+    pb = {"logits": torch.from_numpy(zn), "targets": y, "logit_lens": T_b, "target_lens": U_b, "blank": 0}
+    l, g = _gpu(rb, pb, variant)
+    ref_l, ref_g = _oracle(pb, variant)
+    assert ref_l[1] == math.inf and l[1] == math.inf and not g[1].any()
+    _assert_close(l, g, ref_l, ref_g, "-inf")
+
+
+def test_invalid_targets_give_nan_and_zero_grads(rb):
+    rng = np.random.default_rng(3)
+    z = torch.from_numpy(rng.standard_normal((3, 5, 4, 6)).astype(np.float32))
+    y = np.array([[1, 2, 3], [1, 0, 2], [1, 9, 2]], np.int32)  # utt1: target == blank; utt2: >= V
+    pb = {"logits": z, "targets": y, "logit_lens": np.array([5, 5, 5], np.int32),
+          "target_lens": np.array([3, 3, 3], np.int32), "blank": 0}
+    l, g = _gpu(rb, pb, "rnnt")
+    ref_l, ref_g = _oracle(pb, "rnnt")
+    assert np.isnan(l[1]) and np.isnan(l[2]) and not g[1].any() and not g[2].any()
+    _assert_close(l[:1], g[:1], ref_l[:1], ref_g[:1])
+    # invalid lengths
+    pb["logit_lens"] = np.array([5, 6, 0], np.int32)
+    pb["targets"] = np.array([[1, 2, 3]] * 3, np.int32)
+    l, g = _gpu(rb, pb, "rnnt")
+    assert np.isnan(l[1]) and np.isnan(l[2]) and not g[1:].any()
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_inplace_loss_only_and_grad_scale(rb, variant):
+    cfg = workloads.random_config(4, 40, 12, 256, seed=6, variant=variant)
+    pb = workloads.problem(cfg)
+    ref_l, ref_g = _oracle(pb, variant)
+    z = pb["logits"].cuda()
+    scale = torch.tensor([1.0, 0.5, 0.25, 2.0])
+    l, g = _gpu(rb, pb, variant, grads="inplace", grad_scale=scale, logits=z)
+    assert g is not None
+    _assert_close(l, g, ref_l, ref_g * scale.numpy()[:, None, None, None], "inplace+scale")
+    l2, g2 = _gpu(rb, pb, variant, grads=False)
+    assert g2 is None
+    assert np.array_equal(l2, _gpu(rb, pb, variant)[0])
+
+
+def test_v2_minimal_vocab(rb):
+    cfg = workloads.random_config(3, 10, 4, 2, seed=5, blank=1)
+    pb = workloads.problem(cfg)
+    for variant in VARIANTS:
+        _assert_close(*_gpu(rb, pb, variant), *_oracle(pb, variant), "V=2")
+
+
+def test_max_umax_1023(rb):
+    """Umax + 1 = 1024: the largest wavefront CTA (32 warps, 31 cross-warp hand-offs per step)."""
+    cfg = workloads.random_config(2, 40, 1023, 16, seed=13, variable=False)
+    pb = workloads.problem(cfg)
+    for variant in VARIANTS:
+        _assert_close(*_gpu(rb, pb, variant), *_oracle(pb, variant), "U1023")
+
+
+def test_empty_batch(rb):
+    z = torch.empty((0, 4, 3, 5), device="cuda")
+    l, g = rb.rnnt_loss(z, torch.empty((0, 2), dtype=torch.int32), torch.empty(0), torch.empty(0))
+    torch.cuda.synchronize()
+    assert l.numel() == 0
+
+
+# ------------------------------------------------------------------------------------ determinism
+def test_bitwise_independent_of_batch_composition(rb):
+    """Per-utterance results do not depend on B or on which other utterances share the call (this is what
+    makes sharded results equal the 1-GPU run bit for bit)."""
+    cfg = workloads.random_config(6, 50, 20, 300, seed=10)
+    pb = workloads.problem(cfg)
+    l_all, g_all = _gpu(rb, pb, "rnnt")
+    idx = [4, 1]
+    sub = {"logits": pb["logits"][idx].contiguous(), "targets": pb["targets"][idx],
+           "logit_lens": pb["logit_lens"][idx], "target_lens": pb["target_lens"][idx], "blank": pb["blank"]}
+    l_sub, g_sub = _gpu(rb, sub, "rnnt")
+    assert np.array_equal(l_all[idx], l_sub) and np.array_equal(g_all[idx], g_sub)
+    l_again, g_again = _gpu(rb, pb, "rnnt")
+    assert np.array_equal(l_all, l_again) and np.array_equal(g_all, g_again)
+
+
+def test_loss_sum(rb):
+    losses = torch.rand(1000, device="cuda") * 100
+    s = rb.rnnt_loss_sum(losses)
+    torch.cuda.synchronize()
+    assert abs(s.item() - losses.double().sum().item()) < 1e-9 * s.item()
+
+
+@pytest.mark.parametrize("variant", ("rnnt", "allow_ignore"))
+def test_host_path_matches_device_path(rb, variant):
+    cfg = workloads.random_config(11, 45, 14, 200, seed=14, variant=variant)
+    pb = workloads.problem(cfg)
+    l_dev, g_dev = _gpu(rb, pb, variant)
+    zh = pb["logits"].pin_memory()
+    gh = torch.empty_like(zh).pin_memory()
+    th = torch.from_numpy(pb["targets"]).pin_memory()
+    Th = torch.from_numpy(pb["logit_lens"]).pin_memory()
+    Uh = torch.from_numpy(pb["target_lens"]).pin_memory()
+    lh, gh = rb.rnnt_loss_host(zh, th, Th, Uh, pb["blank"], variant, grads_host=gh)
+    torch.cuda.synchronize()
+    assert np.array_equal(lh.numpy().astype(np.float64), l_dev) and np.array_equal(gh.numpy(), g_dev)
