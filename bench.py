@@ -214,7 +214,7 @@ def main():
     workspace = torch.empty(rb.rnnt_workspace_bytes(B, Tmax, Umax), dtype=torch.uint8, device=dev)
 
     K, W = args.steps, args.warmup
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(K)]
     for row in evs:
         for e in row:
             e.record()  # create the CUDA handles
@@ -247,9 +247,11 @@ def main():
     ms_step = ms_total / K
     value = B * world / (ms_step / 1e3)
 
-    # per-kernel device durations inside the timed region
-    k_ms = {name: statistics.mean(evs[i][j].elapsed_time(evs[i][j + 1]) for i in range(K))
-            for j, name in enumerate(("k1_lse_gather", "k2_alpha_beta", "k3_grad"))}
+    # per-kernel device durations inside the timed region (events: K1 start/end, K3 start/end, K2 start/end)
+    def span(a, b_):
+        return statistics.mean(evs[i][a].elapsed_time(evs[i][b_]) for i in range(K))
+    k_ms = {"k1_lse_gather": span(0, 1), "k2_alpha_beta": span(4, 5), "k3_grad": span(2, 3),
+            "k2_exposed_wait": span(1, 2)}
     T_np, U_np = pb["logit_lens"], pb["target_lens"]
     valid_elems = int(sum(int(t) * (int(u) + 1) for t, u in zip(T_np, U_np))) * V
     all_elems = B * Tmax * Up1 * V

@@ -19,8 +19,10 @@
  *
  * Conventions shared by every entry point:
  *   - All tensor pointers are DEVICE pointers owned by the caller unless the name ends in _host.  The
- *     library allocates no device memory and keeps no state between calls; every call is asynchronous on
- *     `stream` (a cudaStream_t passed as void*; NULL = the legacy default stream).
+ *     library allocates no device memory and keeps no data between calls; every call is asynchronous on
+ *     `stream` (a cudaStream_t passed as void*; NULL = the legacy default stream).  Large calls fork
+ *     internal work onto up to 4 high-priority streams (a per-host-thread, per-device cache created on
+ *     first use) and join it back into `stream` before returning, so stream semantics are unchanged.
  *   - logits  fp32 [B][Tmax][Umax+1][V], contiguous, V innermost.  Cells with t >= T_b or u > U_b are
  *             padding: never read.
  *   - targets int32 [B][Umax] (may be NULL when Umax == 0); targets[b][u], u < U_b, is unit u+1 of
@@ -81,9 +83,12 @@ rnnt_status wrnnt_loss(const float* logits, const int32_t* targets, const int32_
                        void* workspace, size_t workspace_bytes, void* stream, wrnnt_variant variant);
 
 /* rnnt_loss / wrnnt_loss with per-kernel timing (the profiling hook bench.py uses).  variant: -1 = plain
- * RNN-T, else a wrnnt_variant.  If events != NULL, events[0..3] are cudaEvent_t handles recorded on
- * `stream` before K1 (log-softmax + gather), before K2 (alpha/beta wavefront), before K3 (gradient) and
- * after K3, so cudaEventElapsedTime between consecutive events is each kernel's device duration. */
+ * RNN-T, else a wrnnt_variant.  If events != NULL, events[0..5] are cudaEvent_t handles recorded as:
+ * [0] before K1 (log-softmax + gather) and [1] after it, [2] before K3 (gradient) and [3] after it -- all on
+ * `stream` -- and [4] before / [5] after K2 (alpha/beta wavefront).  Large calls run K2 of one half of the
+ * batch concurrently with K1 / K3 of the other half on an internal high-priority stream, where [4] / [5]
+ * are recorded; [2] - [1] is then the time `stream` waited for K2.  Small calls run K1, K2, K3 in order on
+ * `stream` ([1] = [4], [5] = [2]). */
 rnnt_status rnnt_loss_timed(const float* logits, const int32_t* targets, const int32_t* logit_lens,
                             const int32_t* target_lens, int B, int Tmax, int Umax, int V, int blank,
                             float* losses, float* grads, const float* grad_scale,

@@ -120,9 +120,9 @@ def _call(fn_variant, logits, targets, logit_lens, target_lens, blank, grads, gr
             _ptr(losses), _ptr(grads), _ptr(grad_scale), _ptr(workspace), workspace.numel(), _stream(stream)]
     if events is not None:
         handles = [e.cuda_event for e in events]
-        if len(handles) != 4 or not all(handles):
-            raise ValueError("need 4 recorded torch.cuda.Events")
-        arr = (ctypes.c_void_p * 4)(*handles)
+        if len(handles) != 6 or not all(handles):
+            raise ValueError("need 6 recorded torch.cuda.Events")
+        arr = (ctypes.c_void_p * 6)(*handles)
         _check(library.rnnt_loss_timed(*args, fn_variant, ctypes.cast(arr, ctypes.c_void_p)))
     elif fn_variant < 0:
         _check(library.rnnt_loss(*args))
@@ -158,8 +158,8 @@ def loss(logits, targets, logit_lens, target_lens, blank=0, variant="rnnt", **kw
 
 def rnnt_loss_timed(logits, targets, logit_lens, target_lens, blank=0, variant="rnnt", events=None, grads=True,
                     grad_scale=None, losses=None, workspace=None, stream=None):
-    """rnnt_loss / wrnnt_loss recording 4 torch.cuda.Events around K1, K2, K3 (events must be recorded once
-    beforehand so that their CUDA handles exist)."""
+    """rnnt_loss / wrnnt_loss recording 6 torch.cuda.Events: K1 start/end, K3 start/end, K2 start/end
+    (see include/rnnt_b200.h; the events must be recorded once beforehand so that their handles exist)."""
     return _call(VARIANTS[variant], logits, targets, logit_lens, target_lens, blank, grads, grad_scale, losses,
                  workspace, stream, events)
 

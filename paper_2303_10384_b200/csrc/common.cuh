@@ -12,22 +12,24 @@ constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr int kMaxUp1 = 1024;         // Umax + 1 limit of the one-CTA-per-utterance wavefront
 constexpr int kRowWarpsPerBlock = 8;  // K1 / K3: one warp per (b,t,u) row, 8 rows per 256-thread block
+constexpr int kLpPad = 8;             // diagonals of slack before/after the lp array (K2 prefetch distance)
 
 enum Variant : int { kRnnt = 0, kForceFinal = 1, kAllowIgnore = 2 };
 
 // ---------------------------------------------------------------------------------------------------
 // Workspace layout (all offsets 256-byte aligned).  Cell (b,t,u) of a padded [B][Tmax][Umax+1] grid.
 //   lse    fp32   [B][Tmax][Up1]            log sum_v exp(z[b,t,u,v])                (K1 -> K3)
-//   lp     float2 [B][Tmax+Umax][Up1]       (X[t,u,blank], X[t,u,y_u]) at diagonal d = t+u, slot u
+//   lp     double2 [B][Tmax+Umax][Up1]      (X[t,u,blank], X[t,u,y_u]) at diagonal d = t+u, slot u
 //                                           (anti-diagonal major: one wavefront step reads one
-//                                           contiguous run)                          (K1 -> K2, K3)
-//   alpha  fp64   [B][Tmax][Up1]                                                     (K2 -> K3)
-//   beta   fp64   [B][Tmax][Up1]                                                     (K2 -> K3)
+//                                           contiguous run; kLpPad*Up1 entries of slack on both
+//                                           ends so K2's prefetches need no bounds checks)  (K1 -> K2, K3)
+//   alpha  fp64   [B][Tmax+Umax][Up1]      alpha(t,u) at diagonal t+u, slot u        (K2 -> K3)
+//   beta   fp64   [B][Tmax+Umax][Up1]      beta(t,u)  at diagonal t+u, slot u        (K2 -> K3)
 //   logp   fp64   [B]       log P_b from the forward pass (NaN = invalid utterance)  (K2 -> K3)
 // ---------------------------------------------------------------------------------------------------
 struct Workspace {
     float* lse;
-    float2* lp;
+    double2* lp;
     double* alpha;
     double* beta;
     double* logp;
@@ -39,9 +41,9 @@ inline size_t workspace_bytes(int64_t B, int64_t Tmax, int64_t Umax) {
     const int64_t Up1 = Umax + 1;
     size_t s = 0;
     s += align256(sizeof(float) * B * Tmax * Up1);
-    s += align256(sizeof(float2) * B * (Tmax + Umax) * Up1);
-    s += align256(sizeof(double) * B * Tmax * Up1);
-    s += align256(sizeof(double) * B * Tmax * Up1);
+    s += align256(sizeof(double2) * (B * (Tmax + Umax) + 2 * kLpPad) * Up1);
+    s += align256(sizeof(double) * B * (Tmax + Umax) * Up1);
+    s += align256(sizeof(double) * B * (Tmax + Umax) * Up1);
     s += align256(sizeof(double) * B);
     return s;
 }
@@ -52,12 +54,12 @@ inline Workspace carve(void* base, int64_t B, int64_t Tmax, int64_t Umax) {
     Workspace w;
     w.lse = reinterpret_cast<float*>(p);
     p += align256(sizeof(float) * B * Tmax * Up1);
-    w.lp = reinterpret_cast<float2*>(p);
-    p += align256(sizeof(float2) * B * (Tmax + Umax) * Up1);
+    w.lp = reinterpret_cast<double2*>(p) + kLpPad * Up1;
+    p += align256(sizeof(double2) * (B * (Tmax + Umax) + 2 * kLpPad) * Up1);
     w.alpha = reinterpret_cast<double*>(p);
-    p += align256(sizeof(double) * B * Tmax * Up1);
+    p += align256(sizeof(double) * B * (Tmax + Umax) * Up1);
     w.beta = reinterpret_cast<double*>(p);
-    p += align256(sizeof(double) * B * Tmax * Up1);
+    p += align256(sizeof(double) * B * (Tmax + Umax) * Up1);
     w.logp = reinterpret_cast<double*>(p);
     return w;
 }
@@ -113,13 +115,75 @@ __device__ __forceinline__ void st_stream(float* p, float v) {
     asm volatile("st.global.cs.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
 
-// log(e^a + e^b) with fp64 max/add and an fp32 log1p(exp(-|a-b|)) correction (reading R11:
-// alpha/beta accumulate in fp64; the correction term is < ln 2 and needs only fp32 relative accuracy).
-__device__ __forceinline__ double lse2(double a, double b) {
-    const double m = fmax(a, b);
-    if (m == -INFINITY) return -INFINITY;
-    const float d = static_cast<float>(fmin(a, b) - m);  // <= 0, possibly -inf
-    return m + static_cast<double>(log1pf(__expf(d)));
+// Packed fp32x2 arithmetic (sm_100: FFMA2 / FADD2 / FMUL2 -- two lanes of work per issue slot).
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 pk(float lo, float hi) {
+    f32x2 r;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ float2 upk(f32x2 v) {
+    float2 r;
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+    return r;
+}
+__device__ __forceinline__ f32x2 ffma2(f32x2 a, f32x2 b, f32x2 c) {
+    f32x2 d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ f32x2 fadd2(f32x2 a, f32x2 b) {
+    f32x2 d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ f32x2 fmul2(f32x2 a, f32x2 b) {
+    f32x2 d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+// 2^x on both halves (two MUFU.EX2)
+__device__ __forceinline__ f32x2 ex2x2(f32x2 a) {
+    const float2 v = upk(a);
+    return pk(ex2(v.x), ex2(v.y));
+}
+// three-input max (sm_100: FMNMX3)
+__device__ __forceinline__ float max3(float a, float b, float c) {
+    float d;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+
+// L2 eviction policy for the once-read joint tensor: evict-first, so the streamed logits do not push the
+// (reused) workspace out of L2.
+__device__ __forceinline__ uint64_t l2_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ float4 ld_stream_ro(const float4* p, uint64_t pol) {
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ float4 ld_stream(const float4* p, uint64_t pol) {
+    float4 v;
+    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p), "l"(pol)
+                 : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_stream(float4* p, float4 v, uint64_t pol) {
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "f"(v.x),
+                 "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
+                 : "memory");
+}
+
+__device__ __forceinline__ float pick4(const float4& v, int k) {
+    return k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
 }
 
 // ---------------------------------------------------------------------------------------------------

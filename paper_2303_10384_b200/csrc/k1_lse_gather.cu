@@ -5,9 +5,12 @@
 // X[t,u,blank], every vertical arc X[t,u,y_{u+1}]).
 //
 // One warp per (b,t,u) row of V logits, streamed once from HBM with 128-bit loads (8 per lane in flight
-// per chunk = 4 KB per warp), reduced with a lane-local online max/sum and a 5-step butterfly.  Exactly
-// one ex2 per element.  Writes lse (fp32, row-major) and (X_blank, X_label) into the anti-diagonal-major
-// lp array that the K2 wavefront reads coalesced.  Padded rows (t >= T_b or u > U_b) are skipped: never read.
+// per chunk = 4 KB per warp) under an L2 evict-first policy, so the workspace the next kernels reuse stays
+// in L2.  Per lane: 3-input max (FMNMX3), one ex2 per element with packed FFMA2/FADD2 around it; across
+// chunks a lane-local online rescale; across lanes one max-reduce, one rescale, one sum-reduce.  The two
+// gathered logits are fetched by lanes 0 / 1 with scalar loads that merge in L2 with the row's loads.
+// Writes lse (fp32, row-major) and (X_blank, X_label) into the anti-diagonal-major lp array that the K2 wavefront reads.  Padded rows
+// (t >= T_b or u > U_b) are skipped: never read.
 #include "common.cuh"
 
 namespace rnnt {
@@ -15,43 +18,18 @@ namespace {
 
 constexpr int kUnroll = 8;  // float4 per lane per chunk
 
-struct RowState {
-    float m;   // lane-local running max
-    float s;   // lane-local sum of 2^((x - m) * log2e)
-    float zb;  // z[blank]  (valid on the owning lane only)
-    float zy;  // z[y_u]    (valid on the owning lane only)
-};
-
-__device__ __forceinline__ void online_update(RowState& st, float cm, const float* xs, int n) {
-    // cm = max(st.m, max xs): rescale the running sum, then accumulate this chunk.
-    if (cm == -INFINITY) return;  // everything so far is -inf
-    const float sc = (st.m == -INFINITY) ? 0.f : ex2((st.m - cm) * kLog2e);
-    float acc = st.s * sc;
-    const float cml = cm * kLog2e;
-#pragma unroll
-    for (int i = 0; i < n; ++i) acc += ex2(fmaf(xs[i], kLog2e, -cml));
-    st.s = acc;
-    st.m = cm;
-}
-
-__device__ __forceinline__ float pick4(const float4& v, int k) {
-    return k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
-}
-
 template <bool kVec>
 __global__ void __launch_bounds__(kRowWarpsPerBlock * 32)
     k1_lse_gather(const float* __restrict__ logits, const int32_t* __restrict__ targets,
-                  const int32_t* __restrict__ T_b, const int32_t* __restrict__ U_b, int B, int Tmax,
-                  int Umax, int V, int blank, float* __restrict__ lse_out, float2* __restrict__ lp_out) {
+                  const int32_t* __restrict__ T_b, const int32_t* __restrict__ U_b, int b0, int Tmax, int Umax,
+                  int V, int blank, float* __restrict__ lse_out, double2* __restrict__ lp_out) {
     const int lane = threadIdx.x & 31;
-    const int64_t row = static_cast<int64_t>(blockIdx.x) * kRowWarpsPerBlock + (threadIdx.x >> 5);
+    const int b = b0 + static_cast<int>(blockIdx.y);
     const int Up1 = Umax + 1;
-    const int64_t nrows = static_cast<int64_t>(B) * Tmax * Up1;
-    if (row >= nrows) return;
-    const int u = static_cast<int>(row % Up1);
-    const int64_t bt = row / Up1;
-    const int t = static_cast<int>(bt % Tmax);
-    const int b = static_cast<int>(bt / Tmax);
+    const int r = static_cast<int>(blockIdx.x) * kRowWarpsPerBlock + (threadIdx.x >> 5);  // row in utterance
+    if (r >= Tmax * Up1) return;
+    const int t = r / Up1;
+    const int u = r - t * Up1;
     const int T = min(T_b[b], Tmax);
     const int U = min(U_b[b], Umax);
     if (t >= T || u > U) return;  // padding (or an invalid length, flagged by K2): never read
@@ -61,32 +39,44 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32)
     const bool ybad = (u < U) && (yv < 0 || yv >= V || yv == blank);
     if (ybad) yv = -1;
 
-    RowState st{-INFINITY, 0.f, 0.f, 0.f};
+    const int64_t row = static_cast<int64_t>(b) * Tmax * Up1 + r;
     const float* zrow = logits + row * static_cast<int64_t>(V);
+    float m = -INFINITY;  // lane-local running max
+    float s = 0.f;        // lane-local sum of e^(x - m)
+    // Populate gather: lanes 0 / 1 fetch z[blank] / z[y] with scalar loads issued alongside the row's
+    // loads (same sectors, merged in L2: no extra DRAM traffic, no register indexing).
+    float zb = 0.f, zy = 0.f;
+    if (lane == 0) zb = ld_stream_ro(zrow + blank);
+    if (lane == 1 && yv >= 0) zy = ld_stream_ro(zrow + yv);
 
     if constexpr (kVec) {
+        const uint64_t pol = l2_evict_first();
         const float4* row4 = reinterpret_cast<const float4*>(zrow);
         const int nvec = V >> 2;
-        const int bq = blank >> 2, yq = yv >> 2;  // float4 index holding blank / y
+        const f32x2 l2e = pk(kLog2e, kLog2e);
         for (int base = 0; base < nvec; base += 32 * kUnroll) {
             float4 x[kUnroll];
 #pragma unroll
             for (int j = 0; j < kUnroll; ++j) {
                 const int i = base + j * 32 + lane;
-                x[j] = (i < nvec) ? ld_stream_ro(row4 + i)
+                x[j] = (i < nvec) ? ld_stream_ro(row4 + i, pol)
                                   : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
             }
-            float cm = st.m;
+            float cm = m;
 #pragma unroll
-            for (int j = 0; j < kUnroll; ++j)
-                cm = fmaxf(cm, fmaxf(fmaxf(x[j].x, x[j].y), fmaxf(x[j].z, x[j].w)));
-            online_update(st, cm, reinterpret_cast<const float*>(x), 4 * kUnroll);
-            // Populate gather: only the owning lane of the chunk holding blank / y picks its value.
+            for (int j = 0; j < kUnroll; ++j) cm = max3(max3(cm, x[j].x, x[j].y), x[j].z, x[j].w);
+            if (cm != -INFINITY) {
+                const float sc = (m == -INFINITY) ? 0.f : ex2((m - cm) * kLog2e);
+                const f32x2 nml = pk(-cm * kLog2e, -cm * kLog2e);
+                f32x2 acc0 = pk(0.f, 0.f), acc1 = pk(0.f, 0.f);
 #pragma unroll
-            for (int j = 0; j < kUnroll; ++j) {
-                const int i = base + j * 32 + lane;
-                if (i == bq) st.zb = pick4(x[j], blank & 3);
-                if (i == yq) st.zy = pick4(x[j], yv & 3);
+                for (int j = 0; j < kUnroll; ++j) {
+                    acc0 = fadd2(acc0, ex2x2(ffma2(pk(x[j].x, x[j].y), l2e, nml)));
+                    acc1 = fadd2(acc1, ex2x2(ffma2(pk(x[j].z, x[j].w), l2e, nml)));
+                }
+                const float2 a = upk(fadd2(acc0, acc1));
+                s = fmaf(s, sc, a.x + a.y);
+                m = cm;
             }
         }
     } else {
@@ -98,42 +88,35 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32)
                 const int i = base + j * 32 + lane;
                 x[j] = (i < V) ? ld_stream_ro(zrow + i) : -INFINITY;
             }
-            float cm = st.m;
+            float cm = m;
 #pragma unroll
             for (int j = 0; j < kS; ++j) cm = fmaxf(cm, x[j]);
-            online_update(st, cm, x, kS);
+            if (cm != -INFINITY) {
+                const float sc = (m == -INFINITY) ? 0.f : ex2((m - cm) * kLog2e);
+                const float nml = -cm * kLog2e;
+                float acc = 0.f;
 #pragma unroll
-            for (int j = 0; j < kS; ++j) {
-                const int i = base + j * 32 + lane;
-                if (i == blank) st.zb = x[j];
-                if (i == yv) st.zy = x[j];
+                for (int j = 0; j < kS; ++j) acc += ex2(fmaf(x[j], kLog2e, nml));
+                s = fmaf(s, sc, acc);
+                m = cm;
             }
         }
     }
 
-    // Butterfly combine of (m, s); IEEE add/max are commutative so all lanes end bit-identical.
-    float m = st.m, s = st.s;
+    // Warp combine: M = max over lanes; S = sum over lanes of s * e^(m - M).  Butterflies leave every lane
+    // with bit-identical M and S (IEEE max/add are commutative), independent of grid shape.
+    float M = m;
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-        const float m2 = __shfl_xor_sync(0xffffffffu, m, off);
-        const float s2 = __shfl_xor_sync(0xffffffffu, s, off);
-        const float M = fmaxf(m, m2);
-        float acc = 0.f;
-        if (M != -INFINITY) {
-            if (m != -INFINITY) acc += s * ex2((m - M) * kLog2e);
-            if (m2 != -INFINITY) acc += s2 * ex2((m2 - M) * kLog2e);
-        }
-        m = M;
-        s = acc;
-    }
-    // Fetch the gathered values from their owning lanes.
-    const int owner_b = kVec ? ((blank >> 2) & 31) : (blank & 31);
-    const float zb = __shfl_sync(0xffffffffu, st.zb, owner_b);
-    const int owner_y = (yv < 0) ? 0 : (kVec ? ((yv >> 2) & 31) : (yv & 31));
-    const float zy = __shfl_sync(0xffffffffu, st.zy, owner_y);
+    for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+    float S = (m == -INFINITY) ? 0.f : s * ex2((m - M) * kLog2e);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) S += __shfl_xor_sync(0xffffffffu, S, off);
+
+    zb = __shfl_sync(0xffffffffu, zb, 0);
+    zy = __shfl_sync(0xffffffffu, zy, 1);
 
     if (lane == 0) {
-        const float lse = (m == -INFINITY) ? -INFINITY : m + lg2(s) * kLn2;
+        const float lse = (M == -INFINITY) ? -INFINITY : M + lg2(S) * kLn2;
         lse_out[row] = lse;
         float xb, xy;
         if (lse == -INFINITY) {  // an all -inf row forbids its arcs (reading R12)
@@ -144,23 +127,26 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32)
             xy = (u < U) ? (ybad ? __int_as_float(0x7fc00000) : zy - lse) : -INFINITY;
         }
         const int64_t diag = static_cast<int64_t>(b) * (Tmax + Umax) + (t + u);
-        lp_out[diag * Up1 + u] = make_float2(xb, xy);
+        lp_out[diag * Up1 + u] = make_double2(xb, xy);
     }
 }
 
 }  // namespace
 
 cudaError_t launch_k1_lse_gather(const Problem& p, const Workspace& w, cudaStream_t s) {
-    const int64_t nrows = static_cast<int64_t>(p.B) * p.Tmax * (p.Umax + 1);
-    const int64_t blocks = (nrows + kRowWarpsPerBlock - 1) / kRowWarpsPerBlock;
-    if (blocks > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+    const int64_t rows_per_utt = static_cast<int64_t>(p.Tmax) * (p.Umax + 1);
+    const int64_t bx = (rows_per_utt + kRowWarpsPerBlock - 1) / kRowWarpsPerBlock;
+    if (rows_per_utt > 0x7fffffffLL || bx > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
     const bool vec = (p.V % 4 == 0) && (reinterpret_cast<uintptr_t>(p.logits) % 16 == 0);
-    if (vec)
-        k1_lse_gather<true><<<static_cast<unsigned>(blocks), kRowWarpsPerBlock * 32, 0, s>>>(
-            p.logits, p.targets, p.T_b, p.U_b, p.B, p.Tmax, p.Umax, p.V, p.blank, w.lse, w.lp);
-    else
-        k1_lse_gather<false><<<static_cast<unsigned>(blocks), kRowWarpsPerBlock * 32, 0, s>>>(
-            p.logits, p.targets, p.T_b, p.U_b, p.B, p.Tmax, p.Umax, p.V, p.blank, w.lse, w.lp);
+    for (int b0 = 0; b0 < p.B; b0 += 65535) {
+        const dim3 grid(static_cast<unsigned>(bx), static_cast<unsigned>(min(65535, p.B - b0)));
+        if (vec)
+            k1_lse_gather<true><<<grid, kRowWarpsPerBlock * 32, 0, s>>>(
+                p.logits, p.targets, p.T_b, p.U_b, b0, p.Tmax, p.Umax, p.V, p.blank, w.lse, w.lp);
+        else
+            k1_lse_gather<false><<<grid, kRowWarpsPerBlock * 32, 0, s>>>(
+                p.logits, p.targets, p.T_b, p.U_b, b0, p.Tmax, p.Umax, p.V, p.blank, w.lse, w.lp);
+    }
     return cudaGetLastError();
 }
 

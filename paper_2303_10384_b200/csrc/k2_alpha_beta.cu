@@ -1,7 +1,7 @@
 // k2_alpha_beta.cu -- K2: forward (alpha) and backward (beta) scores over the T x (U+1) grid lattice as an
 // anti-diagonal wavefront; plain RNN-T and the two W-Transducer variants.
 //
-// Recursions (DESIGN.md §"Path"; Eq.(1), §2.3, §3.2, §4.3):
+// Recursions (Eq.(1), §2.3, §3.2, §4.3):
 //   alpha(0,0) = 0
 //   alpha(t,u) = LSE( alpha(t-1,u) + X_b(t-1,u),  alpha(t,u-1) + X_y(t,u-1),
 //                     [W, u=0, t>=1]  0                               (initial skips)
@@ -12,160 +12,193 @@
 //                     [FF, u=U, t<T-1] beta(T-1,U),  [AI, u=U, t<T-1] 0,
 //                     [W, (t,u)=(0,0)] LSE_{t'>=1} beta(t',0) )
 //
-// Cell (t,u) depends only on cells of diagonal t+u-1 (plus running skip accumulators owned by one
-// thread), so diagonal d is one parallel step: thread u handles cell (d-u, u).  One CTA per
-// (utterance, direction): grid = 2*B, the alpha and beta CTAs of an utterance run concurrently.
-// Per step a thread needs one value from its neighbour (u-1 for alpha, u+1 for beta): a warp shuffle,
-// plus a shared-memory hand-off across warp boundaries and one named barrier over the active warps
-// (none at all when U_b+1 <= 32).  Its own (X_b, X_y) pair is one 8-byte load from the anti-diagonal-
-// major lp array, software-prefetched kPrefetch diagonals ahead.  Accumulation is fp64; the LSE
-// correction term runs in fp32 MUFU (reading R11).
+// Cell (t,u) depends only on cells of diagonal t+u-1 (plus skip accumulators owned by the lane holding
+// column 0 / column U), so one anti-diagonal is one parallel step.  One CTA per (utterance, direction):
+// grid = 2*B, the alpha and beta CTAs of an utterance run concurrently.  Lane l owns the kC consecutive
+// columns u = l*kC .. l*kC+kC-1: per step its kC cells are independent LSE chains; the boundary column
+// crosses lanes by one warp shuffle, and warps by a shared-memory slot + one named barrier per step
+// (none when the utterance fits one warp).  The lp operands of a step are one contiguous run of the
+// anti-diagonal-major fp64 lp array, loaded kPf steps ahead through running pointers (the array is padded
+// by kLpPad diagonals on both ends, so prefetches never need bounds checks).  fp64 accumulation; the LSE
+// correction log(1 + e^{-|a-b|}) is two MUFU ops in fp32 (reading R11).  alpha / beta are
+// stored anti-diagonal major: [b][t+u][u].
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace rnnt {
 namespace {
 
-constexpr int kPrefetch = 4;
-
 __device__ __forceinline__ void named_barrier(int nthreads) {
     asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
 }
 
-template <int kVariant>
-__global__ void __launch_bounds__(kMaxUp1)
-    k2_alpha_beta(const float2* __restrict__ lp, const int32_t* __restrict__ targets,
+// log(e^a + e^b).  fp64 difference and max, fp32 MUFU correction.  -inf operands need no branch: if one
+// side is -inf the correction is exactly 0; if both are, diff is NaN, fminf(NaN, 0) = 0 and the result is
+// -inf + ln 2 = -inf.
+__device__ __forceinline__ double lse2f(double a, double b) {
+    const double diff = a - b;
+    const double m = (diff > 0.0) ? a : b;
+    const float x = fminf(-fabsf(static_cast<float>(diff)) * kLog2e, 0.f);
+    const float c = lg2(1.f + ex2(x)) * kLn2;
+    return m + static_cast<double>(c);
+}
+
+template <int kVariant, int kC, int kPf>
+__global__ void __launch_bounds__(128)
+    k2_alpha_beta(const double2* __restrict__ lp, const int32_t* __restrict__ targets,
                   const int32_t* __restrict__ T_b, const int32_t* __restrict__ U_b, int Tmax, int Umax,
                   int V, int blank, double* __restrict__ alpha, double* __restrict__ beta,
                   double* __restrict__ logp, float* __restrict__ losses) {
     constexpr bool kW = kVariant != kRnnt;
-    __shared__ double xfer[2][kMaxUp1 / 32];
+    __shared__ double xfer[2][4];
 
     const int b = blockIdx.x >> 1;
     const bool fwd = (blockIdx.x & 1) == 0;
-    const int u = threadIdx.x;
-    const int lane = u & 31, warp = u >> 5;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int u0 = threadIdx.x * kC;  // first column of this lane
     const int T = T_b[b], U = U_b[b];
 
     // Validate the utterance (data-dependent errors -> NaN loss, zero grads in K3).
     const bool len_bad = (T < 1 || T > Tmax || U < 0 || U > Umax);
     int mybad = 0;
-    if (!len_bad && u < U) {
-        const int y = targets[static_cast<int64_t>(b) * Umax + u];
-        mybad = (y < 0 || y >= V || y == blank);
+    if (!len_bad) {
+#pragma unroll
+        for (int j = 0; j < kC; ++j) {
+            const int u = u0 + j;
+            if (u < U) {
+                const int y = targets[static_cast<int64_t>(b) * Umax + u];
+                mybad |= (y < 0 || y >= V || y == blank);
+            }
+        }
     }
     if (__syncthreads_or(len_bad || mybad)) {
-        if (fwd && u == 0) {
+        if (fwd && threadIdx.x == 0) {
             logp[b] = __longlong_as_double(0x7ff8000000000000LL);
             losses[b] = __int_as_float(0x7fc00000);
         }
         return;
     }
-    const int nact = ((U + 1 + 31) >> 5) << 5;  // threads in the warps that own cells
-    if (u >= nact) return;
-    const int nwarps = nact >> 5;
+    const int nact_lanes = (U + 1 + kC - 1) / kC;  // lanes owning at least one column
+    const int nwarps = (nact_lanes + 31) >> 5;
+    if (warp >= nwarps) return;
+    const int nthr = nwarps << 5;
 
     const int Up1 = Umax + 1;
     const int Dmax = Tmax + Umax;
-    const float2* lpu = lp + static_cast<int64_t>(b) * Dmax * Up1 + u;  // slot u of diagonal 0
-    double* const tab = (fwd ? alpha : beta) + static_cast<int64_t>(b) * Tmax * Up1 + u;
     const int D = T + U;  // diagonals 0 .. T+U-1
     const unsigned full = 0xffffffffu;
-
-    // Prefetch ring: pf[k] holds diagonal (d + k) of the traversal.
-    float2 pf[kPrefetch];
-    auto diag_of_step = [&](int i) { return fwd ? i : D - 1 - i; };
-    auto load_lp = [&](int i) -> float2 {
-        if (i >= D) return make_float2(0.f, 0.f);
-        const int d = diag_of_step(i);
-        const int t = d - u;
-        if (t < 0 || t >= T || u > U) return make_float2(0.f, 0.f);
-        return lpu[static_cast<int64_t>(d) * Up1];
-    };
+    const int64_t ubase = static_cast<int64_t>(b) * Dmax * Up1 + u0;
+    // Per-cell validity: cell (d-u, u) exists iff 0 <= d-u < T and u <= U.
+    int Teff[kC];
 #pragma unroll
-    for (int k = 0; k < kPrefetch; ++k) pf[k] = load_lp(k);
+    for (int j = 0; j < kC; ++j) Teff[j] = (u0 + j <= U) ? T : 0;
+
+    const int step = fwd ? Up1 : -Up1;        // pointer stride of one wavefront step
+    const int d_first = fwd ? 0 : D - 1;
+    const double2* ld_ptr = lp + ubase + static_cast<int64_t>(d_first) * Up1;  // padded: kPf steps of slack
+    double* st_ptr = (fwd ? alpha : beta) + ubase + static_cast<int64_t>(d_first) * Up1;
+
+    double2 ring[kPf][kC];
+#pragma unroll
+    for (int s = 0; s < kPf; ++s) {
+#pragma unroll
+        for (int j = 0; j < kC; ++j) ring[s][j] = ld_ptr[j];
+        ld_ptr += step;
+    }
+
+    double self[kC], pub[kC];
+#pragma unroll
+    for (int j = 0; j < kC; ++j) self[j] = pub[j] = -INFINITY;
 
     if (fwd) {
-        double self = -INFINITY;   // alpha(t-1,u) + X_b(t-1,u) for the cell this thread handles next
-        double pub = -INFINITY;    // alpha(t,u) + X_y(t,u): what thread u+1 needs next step
-        double skip = -INFINITY;   // LSE_{t' <= T-2} alpha(t', U)   (thread U only, W variants)
-        for (int i0 = 0; i0 < D; i0 += kPrefetch) {
+        // self[j]: alpha(t-1,u) + X_b(t-1,u) for the next cell of column u0+j (column 0 starts at 0 so that
+        // cell (0,0) = LSE(0, -inf) = 0 exactly).  pub[j]: alpha(t,u) + X_y(t,u) of the last computed cell.
+        if (u0 == 0) self[0] = 0.0;
+        double skip = -INFINITY;  // LSE_{t' <= T-2} alpha(t', U)   (lane owning column U, W variants)
+        for (int i0 = 0; i0 < D; i0 += kPf) {
 #pragma unroll
-            for (int k = 0; k < kPrefetch; ++k) {
-                const int d = i0 + k;
+            for (int s = 0; s < kPf; ++s) {
+                const int d = i0 + s;
                 if (d < D) {  // block-uniform
-                    double nb = __shfl_up_sync(full, pub, 1);
-                    if (lane == 0) nb = (warp > 0 && d > 0) ? xfer[(d - 1) & 1][warp - 1] : -INFINITY;
-                    const float2 l = pf[k];
-                    pf[k] = load_lp(d + kPrefetch);
-                    const int t = d - u;
-                    if (t >= 0 && t < T && u <= U) {
-                        double cur;
-                        if (d == 0) {
-                            cur = 0.0;
-                        } else {
-                            cur = lse2(self, nb);
-                            if (kW && u == 0) cur = lse2(cur, 0.0);  // initial skip (0,0)->(t,0)
-                            if (kVariant == kForceFinal && u == U && t == T - 1) cur = lse2(cur, skip);
-                        }
-                        tab[static_cast<int64_t>(t) * Up1] = cur;
-                        self = cur + static_cast<double>(l.x);
-                        pub = (u < U) ? cur + static_cast<double>(l.y) : -INFINITY;
-                        if (kW && u == U && t <= T - 2) skip = lse2(skip, cur);
-                        if (u == U && t == T - 1) {
-                            double lp_total = self;  // terminating blank (T-1,U) -> F
-                            if (kVariant == kAllowIgnore) lp_total = lse2(lp_total, skip);
-                            logp[b] = lp_total;
-                            losses[b] = static_cast<float>(-lp_total);
-                        }
-                    } else {
-                        pub = -INFINITY;
+                    double left = __shfl_up_sync(full, pub[kC - 1], 1);
+                    if (nwarps > 1 && lane == 0) left = (warp > 0 && d > 0) ? xfer[(d - 1) & 1][warp - 1] : -INFINITY;
+                    if (lane == 0 && warp == 0) left = -INFINITY;
+                    double2 x[kC];
+#pragma unroll
+                    for (int j = 0; j < kC; ++j) {
+                        x[j] = ring[s][j];
+                        ring[s][j] = ld_ptr[j];
                     }
+                    ld_ptr += step;
+#pragma unroll
+                    for (int j = kC - 1; j >= 0; --j) {  // high to low: pub[j-1] is still last step's
+                        const int u = u0 + j;
+                        const int t = d - u;
+                        const bool valid = static_cast<unsigned>(t) < static_cast<unsigned>(Teff[j]);
+                        double cur = lse2f(self[j], (j == 0) ? left : pub[j - 1]);
+                        if (kW && u == 0 && t >= 1) cur = lse2f(cur, 0.0);  // initial skip (0,0)->(t,0)
+                        if (kVariant == kForceFinal && u == U && t == T - 1) cur = lse2f(cur, skip);
+                        if (valid) st_ptr[j] = cur;
+                        self[j] = valid ? cur + x[j].x : -INFINITY;
+                        pub[j] = valid ? cur + x[j].y : -INFINITY;  // X_y(t,U) = -inf: no label arc leaves row U
+                        if (kW && valid && u == U && t <= T - 2) skip = lse2f(skip, cur);
+                        if (valid && u == U && t == T - 1) {
+                            double total = self[j];  // terminating blank (T-1,U) -> F
+                            if (kVariant == kAllowIgnore) total = lse2f(total, skip);
+                            logp[b] = total;
+                            losses[b] = static_cast<float>(-total);
+                        }
+                    }
+                    st_ptr += step;
                     if (nwarps > 1) {
-                        if (lane == 31) xfer[d & 1][warp] = pub;
-                        named_barrier(nact);
+                        if (lane == 31) xfer[d & 1][warp] = pub[kC - 1];
+                        named_barrier(nthr);
                     }
                 }
             }
         }
     } else {
-        double self = -INFINITY;   // beta(t+1,u)
-        double pub = -INFINITY;    // beta(t,u): what thread u-1 needs next step
-        double fin = -INFINITY;    // beta(T-1,U)                   (thread U, force-final)
-        double skip0 = -INFINITY;  // LSE_{t' >= 1} beta(t', 0)     (thread 0, W variants)
-        for (int i0 = 0; i0 < D; i0 += kPrefetch) {
+        // self[j]: beta(t+1,u) (this column's previous cell); pub[j]: beta(t,u) for column u-1's next step.
+        double fin = -INFINITY;    // beta(T-1,U)                  (lane owning column U, force-final)
+        double skip0 = -INFINITY;  // LSE_{t' >= 1} beta(t', 0)    (lane 0, W variants)
+        for (int i0 = 0; i0 < D; i0 += kPf) {
 #pragma unroll
-            for (int k = 0; k < kPrefetch; ++k) {
-                const int i = i0 + k;
+            for (int s = 0; s < kPf; ++s) {
+                const int i = i0 + s;
                 if (i < D) {
                     const int d = D - 1 - i;
-                    double nb = __shfl_down_sync(full, pub, 1);
-                    if (lane == 31) nb = (warp + 1 < nwarps && i > 0) ? xfer[(i - 1) & 1][warp + 1] : -INFINITY;
-                    const float2 l = pf[k];
-                    pf[k] = load_lp(i + kPrefetch);
-                    const int t = d - u;
-                    if (t >= 0 && t < T && u <= U) {
-                        double cur;
-                        if (t == T - 1 && u == U) {
-                            cur = static_cast<double>(l.x);  // terminating blank to F
-                            fin = cur;
-                        } else {
-                            const double x1 = (t < T - 1) ? self + static_cast<double>(l.x) : -INFINITY;
-                            const double x2 = (u < U) ? nb + static_cast<double>(l.y) : -INFINITY;
-                            cur = lse2(x1, x2);
-                            if (kVariant == kForceFinal && u == U) cur = lse2(cur, fin);
-                            if (kVariant == kAllowIgnore && u == U) cur = lse2(cur, 0.0);
-                            if (kW && t == 0 && u == 0) cur = lse2(cur, skip0);
-                        }
-                        if (kW && u == 0 && t >= 1) skip0 = lse2(skip0, cur);
-                        tab[static_cast<int64_t>(t) * Up1] = cur;
-                        self = cur;
-                        pub = cur;
-                    } else {
-                        pub = -INFINITY;
+                    double right = __shfl_down_sync(full, pub[0], 1);
+                    if (nwarps > 1 && lane == 31)
+                        right = (warp + 1 < nwarps && i > 0) ? xfer[(i - 1) & 1][warp + 1] : -INFINITY;
+                    double2 x[kC];
+#pragma unroll
+                    for (int j = 0; j < kC; ++j) {
+                        x[j] = ring[s][j];
+                        ring[s][j] = ld_ptr[j];
                     }
+                    ld_ptr += step;
+#pragma unroll
+                    for (int j = 0; j < kC; ++j) {  // low to high: pub[j+1] is still last step's
+                        const int u = u0 + j;
+                        const int t = d - u;
+                        const bool valid = static_cast<unsigned>(t) < static_cast<unsigned>(Teff[j]);
+                        const double nb = (j == kC - 1) ? right : pub[j + 1];
+                        const bool last = (t == T - 1) && (u == U);  // terminating blank (T-1,U) -> F
+                        double cur = last ? x[j].x : lse2f(self[j] + x[j].x, nb + x[j].y);
+                        if (kVariant == kForceFinal && u == U && !last) cur = lse2f(cur, fin);
+                        if (kVariant == kAllowIgnore && u == U && !last) cur = lse2f(cur, 0.0);
+                        if (kW && t == 0 && u == 0) cur = lse2f(cur, skip0);
+                        if (valid) st_ptr[j] = cur;
+                        if (kVariant == kForceFinal && valid && last) fin = cur;
+                        if (kW && valid && u == 0 && t >= 1) skip0 = lse2f(skip0, cur);
+                        self[j] = valid ? cur : -INFINITY;
+                        pub[j] = self[j];
+                    }
+                    st_ptr += step;
                     if (nwarps > 1) {
-                        if (lane == 0) xfer[i & 1][warp] = pub;
-                        named_barrier(nact);
+                        if (lane == 0) xfer[i & 1][warp] = pub[0];
+                        named_barrier(nthr);
                     }
                 }
             }
@@ -173,20 +206,42 @@ __global__ void __launch_bounds__(kMaxUp1)
     }
 }
 
+template <int kVariant, int kC, int kPf>
+void launch_c(const Problem& p, const Workspace& w, cudaStream_t s) {
+    const int lanes = (p.Umax + 1 + kC - 1) / kC;
+    const int threads = ((lanes + 31) / 32) * 32;
+    k2_alpha_beta<kVariant, kC, kPf><<<2 * p.B, threads, 0, s>>>(w.lp, p.targets, p.T_b, p.U_b, p.Tmax, p.Umax,
+                                                                 p.V, p.blank, w.alpha, w.beta, w.logp, p.losses);
+}
+
+// Columns per lane: the smallest kC that keeps the CTA within 4 warps (128 threads), unless the
+// RNNT_K2_CELLS environment variable (1, 2, 4 or 8; a tuning knob) asks for more.
+int cells_per_lane(int up1) {
+    int c = (up1 <= 128) ? 1 : (up1 <= 256) ? 2 : (up1 <= 512) ? 4 : 8;
+    if (const char* e = getenv("RNNT_K2_CELLS")) {
+        const int want = atoi(e);
+        if ((want == 1 || want == 2 || want == 4 || want == 8) && want > c) c = want;
+    }
+    return c;
+}
+
 template <int kVariant>
-void launch_variant(const Problem& p, const Workspace& w, cudaStream_t s, int threads) {
-    k2_alpha_beta<kVariant><<<2 * p.B, threads, 0, s>>>(w.lp, p.targets, p.T_b, p.U_b, p.Tmax, p.Umax, p.V,
-                                                        p.blank, w.alpha, w.beta, w.logp, p.losses);
+void launch_variant(const Problem& p, const Workspace& w, cudaStream_t s) {
+    switch (cells_per_lane(p.Umax + 1)) {
+        case 1: launch_c<kVariant, 1, kLpPad>(p, w, s); break;
+        case 2: launch_c<kVariant, 2, kLpPad>(p, w, s); break;
+        case 4: launch_c<kVariant, 4, kLpPad / 2>(p, w, s); break;
+        default: launch_c<kVariant, 8, kLpPad / 4>(p, w, s); break;
+    }
 }
 
 }  // namespace
 
 cudaError_t launch_k2_alpha_beta(const Problem& p, const Workspace& w, cudaStream_t s) {
-    const int threads = ((p.Umax + 1 + 31) / 32) * 32;
     switch (p.variant) {
-        case kRnnt: launch_variant<kRnnt>(p, w, s, threads); break;
-        case kForceFinal: launch_variant<kForceFinal>(p, w, s, threads); break;
-        case kAllowIgnore: launch_variant<kAllowIgnore>(p, w, s, threads); break;
+        case kRnnt: launch_variant<kRnnt>(p, w, s); break;
+        case kForceFinal: launch_variant<kForceFinal>(p, w, s); break;
+        case kAllowIgnore: launch_variant<kAllowIgnore>(p, w, s); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

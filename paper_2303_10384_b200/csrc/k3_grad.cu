@@ -22,24 +22,23 @@ constexpr int kUnroll = 8;
 template <bool kVec>
 __global__ void __launch_bounds__(kRowWarpsPerBlock * 32)
     k3_grad(const float* logits, const int32_t* __restrict__ targets, const int32_t* __restrict__ T_b,
-            const int32_t* __restrict__ U_b, int B, int Tmax, int Umax, int V, int blank,
+            const int32_t* __restrict__ U_b, int b0, int Tmax, int Umax, int V, int blank,
             const float* __restrict__ grad_scale, const float* __restrict__ lse_in,
-            const float2* __restrict__ lp_in, const double* __restrict__ alpha,
+            const double2* __restrict__ lp_in, const double* __restrict__ alpha,
             const double* __restrict__ beta, const double* __restrict__ logp, float* grads) {
     const int lane = threadIdx.x & 31;
-    const int64_t row = static_cast<int64_t>(blockIdx.x) * kRowWarpsPerBlock + (threadIdx.x >> 5);
+    const int b = b0 + static_cast<int>(blockIdx.y);
     const int Up1 = Umax + 1;
-    const int64_t nrows = static_cast<int64_t>(B) * Tmax * Up1;
-    if (row >= nrows) return;
-    const int u = static_cast<int>(row % Up1);
-    const int64_t bt = row / Up1;
-    const int t = static_cast<int>(bt % Tmax);
-    const int b = static_cast<int>(bt / Tmax);
+    const int r = static_cast<int>(blockIdx.x) * kRowWarpsPerBlock + (threadIdx.x >> 5);  // row in utterance
+    if (r >= Tmax * Up1) return;
+    const int t = r / Up1;
+    const int u = r - t * Up1;
     const int T = T_b[b], U = U_b[b];
     const double lP = logp[b];
     // Valid lengths are guaranteed whenever lP is finite (K2 writes NaN otherwise).
     const bool live = (t < T) && (u <= U) && isfinite(lP);
 
+    const int64_t row = static_cast<int64_t>(b) * Tmax * Up1 + r;
     float* grow = grads + row * static_cast<int64_t>(V);
     const float* zrow = logits + row * static_cast<int64_t>(V);
 
@@ -55,18 +54,18 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32)
     }
 
     // Per-row scalars: occupancies of the two scored arcs leaving (t,u).
-    const int64_t cell = bt * Up1 + u;  // (b*Tmax + t)*Up1 + u
-    const float lse = lse_in[cell];
-    const float2 l = lp_in[(static_cast<int64_t>(b) * (Tmax + Umax) + (t + u)) * Up1 + u];
-    const double a = alpha[cell];
+    const int64_t dcell = (static_cast<int64_t>(b) * (Tmax + Umax) + (t + u)) * Up1 + u;  // diagonal t+u, slot u
+    const float lse = lse_in[row];
+    const double2 l = lp_in[dcell];
+    const double a = alpha[dcell];
     float occ_b = 0.f, occ_y = 0.f;
-    if (t < T - 1)
-        occ_b = __expf(static_cast<float>(a + static_cast<double>(l.x) + beta[cell + Up1] - lP));
+    if (t < T - 1)  // beta(t+1,u): diagonal t+u+1, slot u
+        occ_b = __expf(static_cast<float>(a + l.x + beta[dcell + Up1] - lP));
     else if (u == U)
-        occ_b = __expf(static_cast<float>(a + static_cast<double>(l.x) - lP));
+        occ_b = __expf(static_cast<float>(a + l.x - lP));
     int yv = -1;
-    if (u < U) {
-        occ_y = __expf(static_cast<float>(a + static_cast<double>(l.y) + beta[cell + 1] - lP));
+    if (u < U) {    // beta(t,u+1): diagonal t+u+1, slot u+1
+        occ_y = __expf(static_cast<float>(a + l.y + beta[dcell + Up1 + 1] - lP));
         yv = targets[static_cast<int64_t>(b) * Umax + u];
     }
     const float scale = grad_scale ? grad_scale[b] : 1.f;
@@ -75,27 +74,35 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32)
     const float lsel = (lse == -INFINITY) ? INFINITY : lse * kLog2e;  // all -inf row -> p = 0
 
     if constexpr (kVec) {
+        const uint64_t pol = l2_evict_first();
         const float4* z4 = reinterpret_cast<const float4*>(zrow);
         float4* g4 = reinterpret_cast<float4*>(grow);
         const int nvec = V >> 2;
+        const int bq = blank >> 2, yq = (yv < 0) ? -1 : (yv >> 2);
+        const f32x2 l2e = pk(kLog2e, kLog2e), nl = pk(-lsel, -lsel), g2 = pk(gam, gam);
         for (int base = 0; base < nvec; base += 32 * kUnroll) {
             float4 x[kUnroll];
 #pragma unroll
             for (int j = 0; j < kUnroll; ++j) {
                 const int i = base + j * 32 + lane;
-                if (i < nvec) x[j] = ld_stream(z4 + i);
+                if (i < nvec) x[j] = ld_stream(z4 + i, pol);
             }
 #pragma unroll
             for (int j = 0; j < kUnroll; ++j) {
                 const int i = base + j * 32 + lane;
                 if (i < nvec) {
-                    const int v0 = i << 2;
-                    float4 g;
-                    g.x = ex2(fmaf(x[j].x, kLog2e, -lsel)) * gam - (v0 + 0 == blank ? sb : 0.f) - (v0 + 0 == yv ? sy : 0.f);
-                    g.y = ex2(fmaf(x[j].y, kLog2e, -lsel)) * gam - (v0 + 1 == blank ? sb : 0.f) - (v0 + 1 == yv ? sy : 0.f);
-                    g.z = ex2(fmaf(x[j].z, kLog2e, -lsel)) * gam - (v0 + 2 == blank ? sb : 0.f) - (v0 + 2 == yv ? sy : 0.f);
-                    g.w = ex2(fmaf(x[j].w, kLog2e, -lsel)) * gam - (v0 + 3 == blank ? sb : 0.f) - (v0 + 3 == yv ? sy : 0.f);
-                    st_stream(g4 + i, g);
+                    const float2 lo = upk(fmul2(ex2x2(ffma2(pk(x[j].x, x[j].y), l2e, nl)), g2));
+                    const float2 hi = upk(fmul2(ex2x2(ffma2(pk(x[j].z, x[j].w), l2e, nl)), g2));
+                    float4 g = make_float4(lo.x, lo.y, hi.x, hi.y);
+                    if (i == bq) {  // the arcs' own logits: subtract their occupancies (owner lane only)
+                        const int k = blank & 3;
+                        if (k == 0) g.x -= sb; else if (k == 1) g.y -= sb; else if (k == 2) g.z -= sb; else g.w -= sb;
+                    }
+                    if (i == yq) {
+                        const int k = yv & 3;
+                        if (k == 0) g.x -= sy; else if (k == 1) g.y -= sy; else if (k == 2) g.z -= sy; else g.w -= sy;
+                    }
+                    st_stream(g4 + i, g, pol);
                 }
             }
         }
@@ -124,19 +131,22 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32)
 }  // namespace
 
 cudaError_t launch_k3_grad(const Problem& p, const Workspace& w, cudaStream_t s) {
-    const int64_t nrows = static_cast<int64_t>(p.B) * p.Tmax * (p.Umax + 1);
-    const int64_t blocks = (nrows + kRowWarpsPerBlock - 1) / kRowWarpsPerBlock;
-    if (blocks > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+    const int64_t rows_per_utt = static_cast<int64_t>(p.Tmax) * (p.Umax + 1);
+    const int64_t bx = (rows_per_utt + kRowWarpsPerBlock - 1) / kRowWarpsPerBlock;
+    if (rows_per_utt > 0x7fffffffLL || bx > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
     const bool vec = (p.V % 4 == 0) && (reinterpret_cast<uintptr_t>(p.logits) % 16 == 0) &&
                      (reinterpret_cast<uintptr_t>(p.grads) % 16 == 0);
-    if (vec)
-        k3_grad<true><<<static_cast<unsigned>(blocks), kRowWarpsPerBlock * 32, 0, s>>>(
-            p.logits, p.targets, p.T_b, p.U_b, p.B, p.Tmax, p.Umax, p.V, p.blank, p.grad_scale, w.lse,
-            w.lp, w.alpha, w.beta, w.logp, p.grads);
-    else
-        k3_grad<false><<<static_cast<unsigned>(blocks), kRowWarpsPerBlock * 32, 0, s>>>(
-            p.logits, p.targets, p.T_b, p.U_b, p.B, p.Tmax, p.Umax, p.V, p.blank, p.grad_scale, w.lse,
-            w.lp, w.alpha, w.beta, w.logp, p.grads);
+    for (int b0 = 0; b0 < p.B; b0 += 65535) {
+        const dim3 grid(static_cast<unsigned>(bx), static_cast<unsigned>(min(65535, p.B - b0)));
+        if (vec)
+            k3_grad<true><<<grid, kRowWarpsPerBlock * 32, 0, s>>>(
+                p.logits, p.targets, p.T_b, p.U_b, b0, p.Tmax, p.Umax, p.V, p.blank, p.grad_scale, w.lse, w.lp,
+                w.alpha, w.beta, w.logp, p.grads);
+        else
+            k3_grad<false><<<grid, kRowWarpsPerBlock * 32, 0, s>>>(
+                p.logits, p.targets, p.T_b, p.U_b, b0, p.Tmax, p.Umax, p.V, p.blank, p.grad_scale, w.lse, w.lp,
+                w.alpha, w.beta, w.logp, p.grads);
+    }
     return cudaGetLastError();
 }
 

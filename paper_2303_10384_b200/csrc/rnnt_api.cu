@@ -24,6 +24,9 @@ rnnt_status check_sizes(int B, int Tmax, int Umax, int V, int blank) {
     return RNNT_OK;
 }
 
+rnnt_status launch_path(const rnnt::Problem& p, const rnnt::Workspace& w, cudaStream_t s,
+                        void* const* events);
+
 rnnt_status run(const float* logits, const int32_t* targets, const int32_t* logit_lens,
                 const int32_t* target_lens, int B, int Tmax, int Umax, int V, int blank, float* losses,
                 float* grads, const float* grad_scale, void* workspace, size_t workspace_bytes, void* stream,
@@ -42,16 +45,120 @@ rnnt_status run(const float* logits, const int32_t* targets, const int32_t* logi
     Problem p{logits, targets, logit_lens, target_lens, B, Tmax, Umax, V, blank, variant, losses, grads,
               grad_scale};
     const Workspace w = rnnt::carve(workspace, B, Tmax, Umax);
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    auto mark = [&](int i) {
-        return !events || cudaEventRecord(static_cast<cudaEvent_t>(events[i]), s) == cudaSuccess;
-    };
-    if (!mark(0) || rnnt::launch_k1_lse_gather(p, w, s) != cudaSuccess) return RNNT_ERR_CUDA;
-    if (!mark(1) || rnnt::launch_k2_alpha_beta(p, w, s) != cudaSuccess) return RNNT_ERR_CUDA;
-    if (!mark(2) || (grads && rnnt::launch_k3_grad(p, w, s) != cudaSuccess)) return RNNT_ERR_CUDA;
-    if (!mark(3)) return RNNT_ERR_CUDA;
+    return launch_path(p, w, static_cast<cudaStream_t>(stream), events);
+}
+
+// Utterances [b0, b0+nb) of a call: every array is utterance-major, so a chunk is a pointer offset.
+void slice(const Problem& p, const Workspace& w, int b0, int nb, Problem& pc, Workspace& wc) {
+    const int64_t Up1 = p.Umax + 1, Dmax = static_cast<int64_t>(p.Tmax) + p.Umax;
+    const int64_t cells = static_cast<int64_t>(p.Tmax) * Up1;
+    pc = p;
+    pc.B = nb;
+    pc.logits = p.logits + b0 * cells * p.V;
+    pc.targets = p.targets ? p.targets + static_cast<int64_t>(b0) * p.Umax : nullptr;
+    pc.T_b = p.T_b + b0;
+    pc.U_b = p.U_b + b0;
+    pc.losses = p.losses + b0;
+    pc.grads = p.grads ? p.grads + b0 * cells * p.V : nullptr;
+    pc.grad_scale = p.grad_scale ? p.grad_scale + b0 : nullptr;
+    wc.lse = w.lse + b0 * cells;
+    wc.lp = w.lp + b0 * Dmax * Up1;
+    wc.alpha = w.alpha + b0 * Dmax * Up1;
+    wc.beta = w.beta + b0 * Dmax * Up1;
+    wc.logp = w.logp + b0;
+}
+
+// Number of utterance chunks the call is split into so that K2 (latency-bound, 2 CTAs per utterance) of one
+// chunk runs concurrently with K1 / K3 (bandwidth-bound, the whole GPU) of the others.  Small calls (where
+// the split buys nothing) stay sequential.
+constexpr int kMaxChunks = 4;
+int overlap_chunks(const Problem& p) {
+    const int64_t elems = static_cast<int64_t>(p.B) * p.Tmax * (p.Umax + 1) * p.V;
+    if (p.B < 2 || elems < (int64_t(1) << 24)) return 1;
+    return std::min(p.B, kMaxChunks);
+}
+
+// Per-host-thread, per-device cache of the internal streams / events of the overlapped path (creating
+// them per call would cost tens of microseconds of host time, comparable to a small call's device time).
+// Thread-local, so concurrent callers on different threads never share an event.
+struct AuxPool {
+    bool ready = false;
+    cudaStream_t aux[kMaxChunks] = {};
+    cudaEvent_t k1_done[kMaxChunks] = {}, k2_done[kMaxChunks] = {};
+};
+constexpr int kMaxDevices = 64;
+thread_local AuxPool t_pools[kMaxDevices];
+
+AuxPool* aux_pool() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return nullptr;
+    AuxPool& pool = t_pools[dev];
+    if (pool.ready) return &pool;
+    int lo = 0, hi = 0;
+    if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) return nullptr;
+    for (int c = 0; c < kMaxChunks; ++c) {
+        if (cudaStreamCreateWithPriority(&pool.aux[c], cudaStreamNonBlocking, hi) != cudaSuccess ||
+            cudaEventCreateWithFlags(&pool.k1_done[c], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&pool.k2_done[c], cudaEventDisableTiming) != cudaSuccess)
+            return nullptr;
+    }
+    pool.ready = true;
+    return &pool;
+}
+
+// K1 -> K2 -> K3 for one call.  With chunks c = 0..n-1 the order is
+//   stream s:       K1(0) K1(1) .. K1(n-1)  [wait K2(0)] K3(0)  [wait K2(1)] K3(1) ..
+//   stream aux[c]:  [wait K1(c)] K2(c)                              (high priority, one stream per chunk)
+// so every K2 hides under the remaining K1 / K3 traffic.  events[0..5] (optional): K1 start / end and K3
+// start (after the first K2 wait) / end on s; K2 start / end on aux[0] (the first chunk's wavefront).
+rnnt_status launch_path(const Problem& p, const Workspace& w, cudaStream_t s, void* const* events) {
+    auto ev = [&](int i) { return static_cast<cudaEvent_t>(events[i]); };
+    const int nch = overlap_chunks(p);
+    AuxPool* pool = (nch > 1) ? aux_pool() : nullptr;
+    if (nch == 1 || pool == nullptr) {
+        if (events && cudaEventRecord(ev(0), s) != cudaSuccess) return RNNT_ERR_CUDA;
+        if (rnnt::launch_k1_lse_gather(p, w, s) != cudaSuccess) return RNNT_ERR_CUDA;
+        if (events && (cudaEventRecord(ev(1), s) != cudaSuccess || cudaEventRecord(ev(4), s) != cudaSuccess))
+            return RNNT_ERR_CUDA;
+        if (rnnt::launch_k2_alpha_beta(p, w, s) != cudaSuccess) return RNNT_ERR_CUDA;
+        if (events && (cudaEventRecord(ev(5), s) != cudaSuccess || cudaEventRecord(ev(2), s) != cudaSuccess))
+            return RNNT_ERR_CUDA;
+        if (p.grads && rnnt::launch_k3_grad(p, w, s) != cudaSuccess) return RNNT_ERR_CUDA;
+        if (events && cudaEventRecord(ev(3), s) != cudaSuccess) return RNNT_ERR_CUDA;
+        return RNNT_OK;
+    }
+    Problem pc[kMaxChunks];
+    Workspace wc[kMaxChunks];
+    for (int c = 0, b0 = 0; c < nch; ++c) {
+        const int nb = p.B / nch + (c < p.B % nch ? 1 : 0);
+        slice(p, w, b0, nb, pc[c], wc[c]);
+        b0 += nb;
+    }
+    auto ok = [](cudaError_t e) { return e == cudaSuccess; };
+    if (events && !ok(cudaEventRecord(ev(0), s))) return RNNT_ERR_CUDA;
+    for (int c = 0; c < nch; ++c) {
+        cudaStream_t a = pool->aux[c];
+        if (!ok(rnnt::launch_k1_lse_gather(pc[c], wc[c], s)) || !ok(cudaEventRecord(pool->k1_done[c], s)) ||
+            !ok(cudaStreamWaitEvent(a, pool->k1_done[c], 0)))
+            return RNNT_ERR_CUDA;
+        if (c == 0 && events && !ok(cudaEventRecord(ev(4), a))) return RNNT_ERR_CUDA;
+        if (!ok(rnnt::launch_k2_alpha_beta(pc[c], wc[c], a)) || !ok(cudaEventRecord(pool->k2_done[c], a)))
+            return RNNT_ERR_CUDA;
+        if (c == 0 && events && !ok(cudaEventRecord(ev(5), a))) return RNNT_ERR_CUDA;
+    }
+    if (events && !ok(cudaEventRecord(ev(1), s))) return RNNT_ERR_CUDA;
+    for (int c = 0; c < nch; ++c) {
+        if (!ok(cudaStreamWaitEvent(s, pool->k2_done[c], 0))) return RNNT_ERR_CUDA;
+        if (c == 0 && events && !ok(cudaEventRecord(ev(2), s))) return RNNT_ERR_CUDA;
+        if (p.grads && !ok(rnnt::launch_k3_grad(pc[c], wc[c], s))) return RNNT_ERR_CUDA;
+    }
+    if (events && !ok(cudaEventRecord(ev(3), s))) return RNNT_ERR_CUDA;
     return RNNT_OK;
 }
+
+}  // namespace
+
+namespace {
 
 // Chunk size of the host path: enough chunks to overlap H2D(c+1) / compute(c) / D2H(c-1).
 int host_chunk(int B) { return std::max(1, (B + 7) / 8); }

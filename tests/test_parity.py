@@ -259,6 +259,21 @@ def test_bitwise_independent_of_batch_composition(rb):
     assert np.array_equal(l_all, l_again) and np.array_equal(g_all, g_again)
 
 
+def test_chunked_overlap_path_bitwise_equals_per_utterance_calls(rb):
+    """Calls with >= 2^24 elements run K2 of one half concurrently with K1/K3 of the other (two streams);
+    every utterance must still equal its own single-utterance (sequential-path) call bit for bit."""
+    cfg = workloads.random_config(4, 120, 40, 1024, seed=15, variable=False)
+    pb = workloads.problem(cfg)
+    for variant in VARIANTS:
+        l_all, g_all = _gpu(rb, pb, variant)
+        for b in range(cfg.B):
+            sub = {"logits": pb["logits"][b:b + 1].contiguous(), "targets": pb["targets"][b:b + 1],
+                   "logit_lens": pb["logit_lens"][b:b + 1], "target_lens": pb["target_lens"][b:b + 1],
+                   "blank": pb["blank"]}
+            l1, g1 = _gpu(rb, sub, variant)
+            assert np.array_equal(l_all[b:b + 1], l1) and np.array_equal(g_all[b:b + 1], g1)
+
+
 def test_loss_sum(rb):
     losses = torch.rand(1000, device="cuda") * 100
     s = rb.rnnt_loss_sum(losses)
