@@ -12,7 +12,7 @@ constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr int kMaxUp1 = 1024;         // Umax + 1 limit of the one-CTA-per-utterance wavefront
 constexpr int kRowWarpsPerBlock = 8;  // K1 / K3: one warp per (b,t,u) row, 8 rows per 256-thread block
-constexpr int kLpPad = 8;             // diagonals of slack before/after the lp array (K2 prefetch distance)
+constexpr int kLpPad = 16;            // diagonals of slack before/after the lp array (>= K2 staging group)
 
 enum Variant : int { kRnnt = 0, kForceFinal = 1, kAllowIgnore = 2 };
 

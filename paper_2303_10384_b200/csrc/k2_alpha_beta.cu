@@ -18,8 +18,9 @@
 // columns u = l*kC .. l*kC+kC-1: per step its kC cells are independent LSE chains; the boundary column
 // crosses lanes by one warp shuffle, and warps by a shared-memory slot + one named barrier per step
 // (none when the utterance fits one warp).  The lp operands of a step are one contiguous run of the
-// anti-diagonal-major fp64 lp array, loaded kPf steps ahead through running pointers (the array is padded
-// by kLpPad diagonals on both ends, so prefetches never need bounds checks).  fp64 accumulation; the LSE
+// anti-diagonal-major fp64 lp array, staged through two register groups of kPf steps (group g+1 loads
+// while group g computes; the array is padded by kLpPad diagonals on both ends, so loads need no bounds
+// checks).  fp64 accumulation; the LSE
 // correction log(1 + e^{-|a-b|}) is two MUFU ops in fp32 (reading R11).  alpha / beta are
 // stored anti-diagonal major: [b][t+u][u].
 #include <stdlib.h>
@@ -99,110 +100,131 @@ __global__ void __launch_bounds__(128)
     const double2* ld_ptr = lp + ubase + static_cast<int64_t>(d_first) * Up1;  // padded: kPf steps of slack
     double* st_ptr = (fwd ? alpha : beta) + ubase + static_cast<int64_t>(d_first) * Up1;
 
-    double2 ring[kPf][kC];
+    // Operand staging: two register groups of kPf steps each.  Group g+1 is loaded while group g is being
+    // consumed, so every load has a whole group (kPf wavefront steps) to land.  Loads past the last
+    // diagonal stay inside the padded lp array (kLpPad >= kPf diagonals of slack).
+    double2 ga[kPf][kC], gb[kPf][kC];
+    auto load_group = [&](double2 (&g)[kPf][kC]) {
 #pragma unroll
-    for (int s = 0; s < kPf; ++s) {
+        for (int s = 0; s < kPf; ++s) {
 #pragma unroll
-        for (int j = 0; j < kC; ++j) ring[s][j] = ld_ptr[j];
-        ld_ptr += step;
-    }
+            for (int j = 0; j < kC; ++j) g[s][j] = ld_ptr[j];
+            ld_ptr += step;
+        }
+    };
+    load_group(ga);
 
     double self[kC], pub[kC];
 #pragma unroll
     for (int j = 0; j < kC; ++j) self[j] = pub[j] = -INFINITY;
+
+    // Drive steps 0 .. D-1 through the two staging groups (full groups run as straight-line code).
+    auto run_groups = [&](auto&& step_fn) {
+        for (int i0 = 0; i0 < D; i0 += 2 * kPf) {
+            if (i0 + kPf < D) load_group(gb);
+            if (i0 + kPf <= D) {
+#pragma unroll
+                for (int s = 0; s < kPf; ++s) step_fn(i0 + s, ga[s]);
+            } else {
+#pragma unroll
+                for (int s = 0; s < kPf; ++s)
+                    if (i0 + s < D) step_fn(i0 + s, ga[s]);
+            }
+            const int i1 = i0 + kPf;
+            if (i1 >= D) break;
+            if (i1 + kPf < D) load_group(ga);
+            if (i1 + kPf <= D) {
+#pragma unroll
+                for (int s = 0; s < kPf; ++s) step_fn(i1 + s, gb[s]);
+            } else {
+#pragma unroll
+                for (int s = 0; s < kPf; ++s)
+                    if (i1 + s < D) step_fn(i1 + s, gb[s]);
+            }
+        }
+    };
 
     if (fwd) {
         // self[j]: alpha(t-1,u) + X_b(t-1,u) for the next cell of column u0+j (column 0 starts at 0 so that
         // cell (0,0) = LSE(0, -inf) = 0 exactly).  pub[j]: alpha(t,u) + X_y(t,u) of the last computed cell.
         if (u0 == 0) self[0] = 0.0;
         double skip = -INFINITY;  // LSE_{t' <= T-2} alpha(t', U)   (lane owning column U, W variants)
-        for (int i0 = 0; i0 < D; i0 += kPf) {
+        // One wavefront step d; x holds the step's (X_b, X_y) operands (staged a group ahead).
+        auto fwd_step = [&](int d, const double2 (&x)[kC]) {
+            double left = __shfl_up_sync(full, pub[kC - 1], 1);
+            if (nwarps > 1 && lane == 0) left = (warp > 0 && d > 0) ? xfer[(d - 1) & 1][warp - 1] : -INFINITY;
+            if (lane == 0 && warp == 0) left = -INFINITY;
 #pragma unroll
-            for (int s = 0; s < kPf; ++s) {
-                const int d = i0 + s;
-                if (d < D) {  // block-uniform
-                    double left = __shfl_up_sync(full, pub[kC - 1], 1);
-                    if (nwarps > 1 && lane == 0) left = (warp > 0 && d > 0) ? xfer[(d - 1) & 1][warp - 1] : -INFINITY;
-                    if (lane == 0 && warp == 0) left = -INFINITY;
-                    double2 x[kC];
-#pragma unroll
-                    for (int j = 0; j < kC; ++j) {
-                        x[j] = ring[s][j];
-                        ring[s][j] = ld_ptr[j];
-                    }
-                    ld_ptr += step;
-#pragma unroll
-                    for (int j = kC - 1; j >= 0; --j) {  // high to low: pub[j-1] is still last step's
-                        const int u = u0 + j;
-                        const int t = d - u;
-                        const bool valid = static_cast<unsigned>(t) < static_cast<unsigned>(Teff[j]);
-                        double cur = lse2f(self[j], (j == 0) ? left : pub[j - 1]);
-                        if (kW && u == 0 && t >= 1) cur = lse2f(cur, 0.0);  // initial skip (0,0)->(t,0)
-                        if (kVariant == kForceFinal && u == U && t == T - 1) cur = lse2f(cur, skip);
-                        if (valid) st_ptr[j] = cur;
-                        self[j] = valid ? cur + x[j].x : -INFINITY;
-                        pub[j] = valid ? cur + x[j].y : -INFINITY;  // X_y(t,U) = -inf: no label arc leaves row U
-                        if (kW && valid && u == U && t <= T - 2) skip = lse2f(skip, cur);
-                        if (valid && u == U && t == T - 1) {
-                            double total = self[j];  // terminating blank (T-1,U) -> F
-                            if (kVariant == kAllowIgnore) total = lse2f(total, skip);
-                            logp[b] = total;
-                            losses[b] = static_cast<float>(-total);
-                        }
-                    }
-                    st_ptr += step;
-                    if (nwarps > 1) {
-                        if (lane == 31) xfer[d & 1][warp] = pub[kC - 1];
-                        named_barrier(nthr);
-                    }
+            for (int j = kC - 1; j >= 0; --j) {  // high to low: pub[j-1] is still last step's
+                const int u = u0 + j;
+                const int t = d - u;
+                const bool valid = static_cast<unsigned>(t) < static_cast<unsigned>(Teff[j]);
+                double nb = (j == 0) ? left : pub[j - 1];
+                // Column 0 has no left neighbour; under W its second incoming arc is the initial skip
+                // (0,0)->(t,0) of weight 0, so one LSE per cell suffices on every column.
+                if (kW && u == 0) nb = (t >= 1) ? 0.0 : -INFINITY;
+                double cur = lse2f(self[j], nb);
+                if (kVariant == kForceFinal && u == U && t == T - 1) cur = lse2f(cur, skip);  // once
+                if (valid) st_ptr[j] = cur;
+                self[j] = valid ? cur + x[j].x : -INFINITY;
+                pub[j] = valid ? cur + x[j].y : -INFINITY;  // X_y(t,U) = -inf: no label arc leaves row U
+                if (kW) {  // running LSE of alpha(t', U), t' <= T-2: computed by every lane, kept by column U
+                    const double nskip = lse2f(skip, cur);
+                    skip = (valid && u == U && t <= T - 2) ? nskip : skip;
+                }
+                if (valid && u == U && t == T - 1) {
+                    double total = self[j];  // terminating blank (T-1,U) -> F
+                    if (kVariant == kAllowIgnore) total = lse2f(total, skip);
+                    logp[b] = total;
+                    losses[b] = static_cast<float>(-total);
                 }
             }
-        }
+            st_ptr += step;
+            if (nwarps > 1) {
+                if (lane == 31) xfer[d & 1][warp] = pub[kC - 1];
+                named_barrier(nthr);
+            }
+        };
+        run_groups(fwd_step);
     } else {
         // self[j]: beta(t+1,u) (this column's previous cell); pub[j]: beta(t,u) for column u-1's next step.
         double fin = -INFINITY;    // beta(T-1,U)                  (lane owning column U, force-final)
         double skip0 = -INFINITY;  // LSE_{t' >= 1} beta(t', 0)    (lane 0, W variants)
-        for (int i0 = 0; i0 < D; i0 += kPf) {
+        auto bwd_step = [&](int i, const double2 (&x)[kC]) {
+            const int d = D - 1 - i;
+            double right = __shfl_down_sync(full, pub[0], 1);
+            if (nwarps > 1 && lane == 31)
+                right = (warp + 1 < nwarps && i > 0) ? xfer[(i - 1) & 1][warp + 1] : -INFINITY;
 #pragma unroll
-            for (int s = 0; s < kPf; ++s) {
-                const int i = i0 + s;
-                if (i < D) {
-                    const int d = D - 1 - i;
-                    double right = __shfl_down_sync(full, pub[0], 1);
-                    if (nwarps > 1 && lane == 31)
-                        right = (warp + 1 < nwarps && i > 0) ? xfer[(i - 1) & 1][warp + 1] : -INFINITY;
-                    double2 x[kC];
-#pragma unroll
-                    for (int j = 0; j < kC; ++j) {
-                        x[j] = ring[s][j];
-                        ring[s][j] = ld_ptr[j];
-                    }
-                    ld_ptr += step;
-#pragma unroll
-                    for (int j = 0; j < kC; ++j) {  // low to high: pub[j+1] is still last step's
-                        const int u = u0 + j;
-                        const int t = d - u;
-                        const bool valid = static_cast<unsigned>(t) < static_cast<unsigned>(Teff[j]);
-                        const double nb = (j == kC - 1) ? right : pub[j + 1];
-                        const bool last = (t == T - 1) && (u == U);  // terminating blank (T-1,U) -> F
-                        double cur = last ? x[j].x : lse2f(self[j] + x[j].x, nb + x[j].y);
-                        if (kVariant == kForceFinal && u == U && !last) cur = lse2f(cur, fin);
-                        if (kVariant == kAllowIgnore && u == U && !last) cur = lse2f(cur, 0.0);
-                        if (kW && t == 0 && u == 0) cur = lse2f(cur, skip0);
-                        if (valid) st_ptr[j] = cur;
-                        if (kVariant == kForceFinal && valid && last) fin = cur;
-                        if (kW && valid && u == 0 && t >= 1) skip0 = lse2f(skip0, cur);
-                        self[j] = valid ? cur : -INFINITY;
-                        pub[j] = self[j];
-                    }
-                    st_ptr += step;
-                    if (nwarps > 1) {
-                        if (lane == 0) xfer[i & 1][warp] = pub[0];
-                        named_barrier(nthr);
-                    }
+            for (int j = 0; j < kC; ++j) {  // low to high: pub[j+1] is still last step's
+                const int u = u0 + j;
+                const int t = d - u;
+                const bool valid = static_cast<unsigned>(t) < static_cast<unsigned>(Teff[j]);
+                const bool last = (t == T - 1) && (u == U);  // terminating blank (T-1,U) -> F
+                // Row U has no label arc; under W its second outgoing arc is the final skip (P:116 / P:167):
+                // to (T-1,U) for force-final (beta(T-1,U)), to F for allow-ignore (0).
+                double op2 = ((j == kC - 1) ? right : pub[j + 1]) + x[j].y;
+                if (kVariant == kForceFinal && u == U) op2 = fin;
+                if (kVariant == kAllowIgnore && u == U) op2 = 0.0;
+                double cur = lse2f(self[j] + x[j].x, op2);
+                cur = last ? x[j].x : cur;
+                if (kW && t == 0 && u == 0) cur = lse2f(cur, skip0);  // initial skips, once
+                if (valid) st_ptr[j] = cur;
+                if (kVariant == kForceFinal) fin = (valid && last) ? cur : fin;
+                if (kW) {  // running LSE of beta(t', 0), t' >= 1: computed by every lane, kept by column 0
+                    const double nskip = lse2f(skip0, cur);
+                    skip0 = (valid && u == 0 && t >= 1) ? nskip : skip0;
                 }
+                self[j] = valid ? cur : -INFINITY;
+                pub[j] = self[j];
             }
-        }
+            st_ptr += step;
+            if (nwarps > 1) {
+                if (lane == 0) xfer[i & 1][warp] = pub[0];
+                named_barrier(nthr);
+            }
+        };
+        run_groups(bwd_step);
     }
 }
 
@@ -227,11 +249,11 @@ int cells_per_lane(int up1) {
 
 template <int kVariant>
 void launch_variant(const Problem& p, const Workspace& w, cudaStream_t s) {
-    switch (cells_per_lane(p.Umax + 1)) {
-        case 1: launch_c<kVariant, 1, kLpPad>(p, w, s); break;
-        case 2: launch_c<kVariant, 2, kLpPad>(p, w, s); break;
-        case 4: launch_c<kVariant, 4, kLpPad / 2>(p, w, s); break;
-        default: launch_c<kVariant, 8, kLpPad / 4>(p, w, s); break;
+    switch (cells_per_lane(p.Umax + 1)) {  // staging group = kPf steps, i.e. kPf..2*kPf steps of load slack
+        case 1: launch_c<kVariant, 1, 16>(p, w, s); break;
+        case 2: launch_c<kVariant, 2, 8>(p, w, s); break;
+        case 4: launch_c<kVariant, 4, 4>(p, w, s); break;
+        default: launch_c<kVariant, 8, 2>(p, w, s); break;
     }
 }
 

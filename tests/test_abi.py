@@ -49,7 +49,7 @@ def test_workspace_bytes(rb):
     B, T, U = 3, 50, 7
     ws = rb.rnnt_workspace_bytes(B, T, U)
     cells = B * T * (U + 1)
-    expect_min = cells * 4 + (B * (T + U) + 16) * (U + 1) * 16 + B * (T + U) * (U + 1) * (8 + 8) + B * 8
+    expect_min = cells * 4 + (B * (T + U) + 32) * (U + 1) * 16 + B * (T + U) * (U + 1) * (8 + 8) + B * 8
     assert expect_min <= ws <= expect_min + 5 * 256
     assert rb.rnnt_workspace_bytes(0, 1, 0) >= 0
     assert rb.rnnt_workspace_bytes(-1, 1, 0) == 0
