@@ -48,12 +48,15 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=16)
+    ap.add_argument("--inplace", action="store_true",
+                    help="write grads over the logits (automatic when two copies do not fit in HBM, e.g. c5)")
     return ap.parse_args()
 
 
 def workload_desc(cfg, variant):
-    return (f"{cfg.name}: B={cfg.B}/GPU, Tmax={cfg.Tmax}, Umax={cfg.Umax}, V={cfg.V}, fp32 logits, "
+    return (f"{cfg.name}: B={cfg.B_per_gpu}/GPU, Tmax={cfg.Tmax}, Umax={cfg.Umax}, V={cfg.V}, fp32 logits, "
             f"{'RNN-T' if variant == 'rnnt' else 'W-RNNT ' + variant}"
+            f"{f' ({cfg.B} over {cfg.B // cfg.B_per_gpu} GPUs)' if cfg.B != cfg.B_per_gpu else ''}"
             f"{', variable lengths' if cfg.variable_lengths else ', full lengths'}")
 
 
@@ -152,6 +155,25 @@ def host_cores():
     return len(os.sched_getaffinity(0))
 
 
+def host_avail_bytes():
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 64 << 30
+
+
+def oracle_threads(cfg, want):
+    """Threads (= utterances in flight) for the CPU oracle, bounded by cores and host memory (each utterance
+    holds its fp32 logits and fp64 grads)."""
+    per_utt = cfg.cells_per_utt * cfg.V * (4 + 8) * 1.1
+    by_mem = int(0.5 * host_avail_bytes() // per_utt)
+    return max(1, min(host_cores(), want, by_mem))
+
+
 def run_reference(args):
     """--impl reference: the oracle on the host cores; each step = one utterance per thread."""
     rank = int(os.environ.get("RANK", 0))
@@ -159,7 +181,7 @@ def run_reference(args):
         return
     cfg = workloads.CONFIGS[args.config]
     variant = args.variant or cfg.variant
-    threads = max(1, min(host_cores(), args.cpu_threads))
+    threads = oracle_threads(cfg, args.cpu_threads)
     import oracle
     oracle.build()
     b_ids = [i % cfg.B for i in range(threads)]
@@ -199,7 +221,7 @@ def main():
 
     base = workloads.CONFIGS[args.config]
     variant = args.variant or base.variant
-    gcfg = dataclasses.replace(base, B=base.B * world)           # weak scaling: B per GPU fixed
+    gcfg = dataclasses.replace(base, B=base.B_per_gpu * world)   # weak scaling: B per GPU fixed
     b_ids = rdist.contiguous_shard(gcfg.B, rank, world)
     pb = workloads.problem(gcfg, b_ids=b_ids, device=dev)
     z = pb["logits"]
@@ -208,7 +230,11 @@ def main():
     targets = torch.from_numpy(pb["targets"]).to(dev)
     T_b = torch.from_numpy(pb["logit_lens"]).to(dev)
     U_b = torch.from_numpy(pb["target_lens"]).to(dev)
-    grads = torch.empty_like(z)                                  # out of place: logits stay fixed across steps
+    free, _ = torch.cuda.mem_get_info(dev)
+    inplace = args.inplace or free < 1.05 * z.numel() * 4 + (4 << 30)
+    # out of place: logits stay fixed across steps; in place: later steps run on the previous step's grads
+    # (same work -- the kernels' cost does not depend on the values)
+    grads = z if inplace else torch.empty_like(z)
     losses = torch.empty(B, dtype=torch.float32, device=dev)
     loss_sum = torch.empty((), dtype=torch.float64, device=dev)
     workspace = torch.empty(rb.rnnt_workspace_bytes(B, Tmax, Umax), dtype=torch.uint8, device=dev)
@@ -274,7 +300,7 @@ def main():
             "config": {"workload": workload_desc(base, variant), "variant": variant, "B_per_gpu": B,
                        "global_batch": B * world, "parallelism": f"dp{world} (batch shards, NCCL all-reduce of "
                        f"the fp64 loss sum)", "l2": f"inputs {z.numel() * 4 / 1e9:.2f} GB/GPU > 126 MB L2: no flush",
-                       "grads": "out of place"},
+                       "grads": "in place" if inplace else "out of place"},
             "roofline": {"bound": "hbm", "kernel": "k3_grad", "achieved": k3_gbs, "peak": peak, "unit": "GB/s",
                          "frac": k3_gbs / peak, "traffic": ncu_traffic("k3_grad", args.config),
                          "algorithmic_bytes_per_launch": k3_bytes, "peak_source": peak_src},
@@ -289,14 +315,19 @@ def main():
 
     # ---- end to end through the host-buffer C-ABI entry point (pinned host in/out, copies in the timed region)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and 2.2 * z.numel() * 4 > host_avail_bytes():
+        e2e = {"value": None, "unit": UNIT, "reason": "pinned host copies of logits + grads exceed host RAM"}
+    elif not args.no_e2e:
         zh = z.cpu().pin_memory()
         gh = torch.empty_like(zh).pin_memory()
         th = torch.from_numpy(pb["targets"]).contiguous().pin_memory()
         Th = torch.from_numpy(pb["logit_lens"]).pin_memory()
         Uh = torch.from_numpy(pb["target_lens"]).pin_memory()
         lh = torch.empty(B, dtype=torch.float32).pin_memory()
-        del grads
+        if not inplace:
+            del grads
+        del z
+        pb["logits"] = None
         torch.cuda.empty_cache()
         dbuf = torch.empty(rb.rnnt_host_buffer_bytes(B, Tmax, Umax, V), dtype=torch.uint8, device=dev)
         for _ in range(1):
@@ -322,8 +353,8 @@ def main():
 
     # ---- CPU baseline: the oracle as it stands, on the host cores, rank 0 at N=1 only
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        threads = max(1, min(host_cores(), args.cpu_threads))
-        ids = [i % base.B for i in range(threads)]
+        threads = oracle_threads(base, args.cpu_threads)
+        ids = [i % base.B_per_gpu for i in range(threads)]
         secs = oracle_sample(base, variant, threads, ids)
         line["cpu_baseline"] = {"value": len(ids) / secs, "unit": UNIT, "cores": threads, "kind": "oracle",
                                 "sample": f"{len(ids)} utterances of {base.name} (one per OpenMP thread), full "

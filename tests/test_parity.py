@@ -95,9 +95,9 @@ def test_c2_full(rb):
 
 
 # ------------------------------------------------------------------------------------------ c3 / c4
-def _full_size_sampled(rb, cfg_name, variant, sample=(0, 17, 31)):
+def _full_size_sampled(rb, cfg_name, variant, sample=(0, 17, 31), b_ids=None):
     cfg = workloads.CONFIGS[cfg_name]
-    pb = workloads.problem(cfg, device="cuda")        # the full batch, generated on the device
+    pb = workloads.problem(cfg, b_ids=b_ids, device="cuda")  # the full (per-GPU) batch, generated on the device
     z = pb["logits"]
     zs = z[list(sample)].cpu().numpy()                # oracle inputs: the same values, copied before the call
     l, g = rb.loss(z, pb["targets"], pb["logit_lens"], pb["target_lens"], cfg.blank, variant,
@@ -124,6 +124,18 @@ def test_c3_full_size_sampled(rb):
 @pytest.mark.parametrize("variant", ("force_final", "allow_ignore"))
 def test_c4_full_size_sampled(rb, variant):
     _full_size_sampled(rb, "c4", variant, sample=(1, 20))
+
+
+def test_c5_per_gpu_shard_in_place_sampled(rb):
+    """c5: one GPU's shard of B=256, T=1000, U=200, V=4096 (32 utterances, 105 GB of logits, 2.6e10 elements:
+    64-bit offsets), gradients written in place; utterances 0 and 31 compared with the oracle element by
+    element, every row checked for sum_v grad = 0."""
+    free, _ = torch.cuda.mem_get_info()
+    cfg = workloads.CONFIGS["c5"]
+    need = 32 * cfg.cells_per_utt * cfg.V * 4 + (2 << 30)
+    if free < need:
+        pytest.skip(f"needs {need / 1e9:.0f} GB of device memory, {free / 1e9:.0f} GB free")
+    _full_size_sampled(rb, "c5", "rnnt", sample=(0, 31), b_ids=range(32))
 
 
 # ------------------------------------------------------------------------------------- edge cases

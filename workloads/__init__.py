@@ -42,6 +42,11 @@ class Config:
     drop: tuple = ()                 # c4: word-drop fractions, cycled over b
     drop_seed: int = 3
     fixed_targets: tuple = ()        # c1: explicit transcript
+    per_gpu: int = 0                 # utterances per GPU when B is a multi-GPU global batch (c5); 0 = B
+
+    @property
+    def B_per_gpu(self) -> int:
+        return self.per_gpu or self.B
 
     @property
     def cells_per_utt(self) -> int:
@@ -61,7 +66,7 @@ CONFIGS = {
     "c3": Config("B32_T500_U100_V1024", B=32, Tmax=500, Umax=100, V=1024, logit_seed=2000),
     "c4": Config("B32_T500_U100_V1024_wrnnt", B=32, Tmax=500, Umax=100, V=1024, logit_seed=2000,
                  variant="force_final", drop=(0.2, 0.5)),
-    "c5": Config("B256_T1000_U200_V4096", B=256, Tmax=1000, Umax=200, V=4096, logit_seed=5000),
+    "c5": Config("B256_T1000_U200_V4096", B=256, Tmax=1000, Umax=200, V=4096, logit_seed=5000, per_gpu=32),
 }
 
 
