@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=16)
+    ap.add_argument("--dtype", default="f32", choices=["f32", "bf16", "f16"],
+                    help="storage type of logits/grads (arithmetic is fp32/fp64 either way); the BASELINE "
+                         "metric is quoted on f32")
     ap.add_argument("--inplace", action="store_true",
                     help="write grads over the logits (automatic when two copies do not fit in HBM, e.g. c5)")
     return ap.parse_args()
@@ -224,14 +227,19 @@ def main():
     gcfg = dataclasses.replace(base, B=base.B_per_gpu * world)   # weak scaling: B per GPU fixed
     b_ids = rdist.contiguous_shard(gcfg.B, rank, world)
     pb = workloads.problem(gcfg, b_ids=b_ids, device=dev)
+    tdtype = {"f32": torch.float32, "bf16": torch.bfloat16, "f16": torch.float16}[args.dtype]
+    if tdtype != torch.float32:
+        pb["logits"] = pb["logits"].to(tdtype)
+        torch.cuda.empty_cache()
     z = pb["logits"]
+    esize = z.element_size()
     B, Tmax, Up1, V = z.shape
     Umax = Up1 - 1
     targets = torch.from_numpy(pb["targets"]).to(dev)
     T_b = torch.from_numpy(pb["logit_lens"]).to(dev)
     U_b = torch.from_numpy(pb["target_lens"]).to(dev)
     free, _ = torch.cuda.mem_get_info(dev)
-    inplace = args.inplace or free < 1.05 * z.numel() * 4 + (4 << 30)
+    inplace = args.inplace or free < 1.05 * z.numel() * esize + (4 << 30)
     # out of place: logits stay fixed across steps; in place: later steps run on the previous step's grads
     # (same work -- the kernels' cost does not depend on the values)
     grads = z if inplace else torch.empty_like(z)
@@ -281,8 +289,8 @@ def main():
     T_np, U_np = pb["logit_lens"], pb["target_lens"]
     valid_elems = int(sum(int(t) * (int(u) + 1) for t, u in zip(T_np, U_np))) * V
     all_elems = B * Tmax * Up1 * V
-    k3_bytes = 8 * valid_elems + 4 * (all_elems - valid_elems)   # read + write valid, zero-write padding
-    k1_bytes = 4 * valid_elems
+    k3_bytes = 2 * esize * valid_elems + esize * (all_elems - valid_elems)  # read+write valid, zero-write pad
+    k1_bytes = esize * valid_elems
     peak, peak_src = measured_peaks()
     k3_gbs = k3_bytes / (k_ms["k3_grad"] / 1e3) / 1e9
     k1_gbs = k1_bytes / (k_ms["k1_lse_gather"] / 1e3) / 1e9
@@ -296,18 +304,20 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
             "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f32", "data": "synthetic",
+            "dtype": args.dtype, "data": "synthetic",
             "config": {"workload": workload_desc(base, variant), "variant": variant, "B_per_gpu": B,
                        "global_batch": B * world, "parallelism": f"dp{world} (batch shards, NCCL all-reduce of "
-                       f"the fp64 loss sum)", "l2": f"inputs {z.numel() * 4 / 1e9:.2f} GB/GPU > 126 MB L2: no flush",
+                       f"the fp64 loss sum)", "l2": f"inputs {z.numel() * esize / 1e9:.2f} GB/GPU > 126 MB L2: no flush",
                        "grads": "in place" if inplace else "out of place"},
             "roofline": {"bound": "hbm", "kernel": "k3_grad", "achieved": k3_gbs, "peak": peak, "unit": "GB/s",
                          "frac": k3_gbs / peak, "traffic": ncu_traffic("k3_grad", args.config),
                          "algorithmic_bytes_per_launch": k3_bytes, "peak_source": peak_src},
             "kernels_ms": k_ms,
             "kernel_gbs": {"k1_lse_gather": k1_gbs, "k3_grad": k3_gbs},
+            "note": None if args.dtype == "f32" else "16-bit storage run (SURVEY §8(f) NEXT-1); the BASELINE "
+                    "metric itself is fp32",
             "kernel_frac_of_peak": {"k1_lse_gather": k1_gbs / peak, "k3_grad": k3_gbs / peak},
-            "step_frac_of_12B_roofline": (12 * valid_elems / (ms_step / 1e3) / 1e9) / peak,
+            "step_frac_of_3pass_roofline": (3 * esize * valid_elems / (ms_step / 1e3) / 1e9) / peak,
             "clocks": clk,
             "gpu_launches": 4 * K,
             "loss_sum_last_step": loss_total,
@@ -315,7 +325,9 @@ def main():
 
     # ---- end to end through the host-buffer C-ABI entry point (pinned host in/out, copies in the timed region)
     e2e = None
-    if not args.no_e2e and 2.2 * z.numel() * 4 > host_avail_bytes():
+    if not args.no_e2e and args.dtype != "f32":
+        e2e = {"value": None, "unit": UNIT, "reason": "the host-buffer entry point takes fp32 only"}
+    elif not args.no_e2e and 2.2 * z.numel() * 4 > host_avail_bytes():
         e2e = {"value": None, "unit": UNIT, "reason": "pinned host copies of logits + grads exceed host RAM"}
     elif not args.no_e2e:
         zh = z.cpu().pin_memory()

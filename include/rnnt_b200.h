@@ -61,6 +61,14 @@ typedef enum {
 } rnnt_status;
 
 typedef enum {
+    RNNT_F32 = 0,   /* fp32 logits / grads (the default entry points) */
+    RNNT_F16 = 1,   /* IEEE fp16 storage; all arithmetic fp32 / fp64 (§4.2: "populate the
+                       lattice with a half (fp16) precision tensor and cast it to fp32 or fp64 only for the
+                       forward-backward score calculation") */
+    RNNT_BF16 = 2   /* bfloat16 storage, same arithmetic */
+} rnnt_dtype;
+
+typedef enum {
     WRNNT_FORCE_FINAL = 0,   /* final skips land on (T_b-1, U_b): the last blank is still emitted */
     WRNNT_ALLOW_IGNORE = 1   /* final skips land on the final state */
 } wrnnt_variant;
@@ -94,6 +102,14 @@ rnnt_status rnnt_loss_timed(const float* logits, const int32_t* targets, const i
                             float* losses, float* grads, const float* grad_scale,
                             void* workspace, size_t workspace_bytes, void* stream, int variant,
                             void* const* events);
+
+/* The general entry point: logits / grads in any rnnt_dtype (grads have the logits' type and are rounded to
+ * nearest from the fp32 result), variant -1 = plain RNN-T or a wrnnt_variant, optional 6 timing events as in
+ * rnnt_loss_timed.  Losses are fp32 whatever the storage type.  Same conventions as rnnt_loss otherwise. */
+rnnt_status rnnt_loss_ex(const void* logits, rnnt_dtype dtype, const int32_t* targets,
+                         const int32_t* logit_lens, const int32_t* target_lens, int B, int Tmax, int Umax,
+                         int V, int blank, int variant, float* losses, void* grads, const float* grad_scale,
+                         void* workspace, size_t workspace_bytes, void* stream, void* const* events);
 
 /* Deterministic fp64 sum of losses[0..B) into *loss_sum (device), fixed summation order for a given B.
  * This is the per-rank operand of the cross-GPU all-reduce of the loss sum (BASELINE.json north_star (5)). */

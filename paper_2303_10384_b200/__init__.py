@@ -21,8 +21,9 @@ RNNT_OK = 0
 VARIANTS = {"rnnt": -1, "force_final": 0, "allow_ignore": 1}
 
 # Every symbol include/rnnt_b200.h declares.
-EXPORTS = ("rnnt_workspace_bytes", "rnnt_loss", "wrnnt_loss", "rnnt_loss_timed", "rnnt_loss_sum", "rnnt_host_buffer_bytes",
-           "rnnt_loss_host", "rnnt_status_string", "rnnt_version")
+EXPORTS = ("rnnt_workspace_bytes", "rnnt_loss", "wrnnt_loss", "rnnt_loss_timed", "rnnt_loss_ex", "rnnt_loss_sum",
+           "rnnt_host_buffer_bytes", "rnnt_loss_host", "rnnt_status_string", "rnnt_version")
+DTYPES = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2}
 
 
 class RnntError(RuntimeError):
@@ -44,6 +45,8 @@ def _load():
     lib.wrnnt_loss.restype = I
     lib.rnnt_loss_timed.argtypes = common + [I, P]
     lib.rnnt_loss_timed.restype = I
+    lib.rnnt_loss_ex.argtypes = [P, I, P, P, P, I, I, I, I, I, I, P, P, P, P, S, P, P]
+    lib.rnnt_loss_ex.restype = I
     lib.rnnt_loss_sum.argtypes = [P, I, P, P]
     lib.rnnt_loss_sum.restype = I
     lib.rnnt_host_buffer_bytes.argtypes = [I, I, I, I]
@@ -91,8 +94,9 @@ def _as_i32(x, device):
 
 def _call(fn_variant, logits, targets, logit_lens, target_lens, blank, grads, grad_scale, losses, workspace,
           stream, events=None):
-    if not (isinstance(logits, torch.Tensor) and logits.is_cuda and logits.dtype == torch.float32):
-        raise TypeError("logits must be a CUDA float32 tensor [B, Tmax, Umax+1, V] (no CPU fallback)")
+    if not (isinstance(logits, torch.Tensor) and logits.is_cuda and logits.dtype in DTYPES):
+        raise TypeError("logits must be a CUDA float32 / float16 / bfloat16 tensor [B, Tmax, Umax+1, V] "
+                        "(no CPU fallback)")
     if not logits.is_contiguous():
         raise ValueError("logits must be contiguous")
     B, Tmax, Up1, V = logits.shape
@@ -109,8 +113,9 @@ def _call(fn_variant, logits, targets, logit_lens, target_lens, blank, grads, gr
         grads = torch.empty_like(logits)
     elif grads is False:
         grads = None
-    if grads is not None and (grads.shape != logits.shape or not grads.is_contiguous()):
-        raise ValueError("grads must be contiguous and shaped like logits")
+    if grads is not None and (grads.shape != logits.shape or not grads.is_contiguous()
+                              or grads.dtype != logits.dtype or grads.device != dev):
+        raise ValueError("grads must be contiguous, on the logits' device, with the logits' shape and dtype")
     if grad_scale is not None:
         grad_scale = grad_scale.to(device=dev, dtype=torch.float32).contiguous()
     need = rnnt_workspace_bytes(B, Tmax, Umax)
@@ -118,16 +123,19 @@ def _call(fn_variant, logits, targets, logit_lens, target_lens, blank, grads, gr
         workspace = torch.empty(max(need, 1), dtype=torch.uint8, device=dev)
     args = [_ptr(logits), _ptr(targets), _ptr(logit_lens), _ptr(target_lens), B, Tmax, Umax, V, int(blank),
             _ptr(losses), _ptr(grads), _ptr(grad_scale), _ptr(workspace), workspace.numel(), _stream(stream)]
+    ev = None
     if events is not None:
         handles = [e.cuda_event for e in events]
         if len(handles) != 6 or not all(handles):
             raise ValueError("need 6 recorded torch.cuda.Events")
-        arr = (ctypes.c_void_p * 6)(*handles)
-        _check(library.rnnt_loss_timed(*args, fn_variant, ctypes.cast(arr, ctypes.c_void_p)))
-    elif fn_variant < 0:
-        _check(library.rnnt_loss(*args))
+        ev = ctypes.cast((ctypes.c_void_p * 6)(*handles), ctypes.c_void_p)
+    if logits.dtype == torch.float32 and ev is None:
+        if fn_variant < 0:
+            _check(library.rnnt_loss(*args))
+        else:
+            _check(library.wrnnt_loss(*args, fn_variant))
     else:
-        _check(library.wrnnt_loss(*args, fn_variant))
+        _check(library.rnnt_loss_ex(args[0], DTYPES[logits.dtype], *args[1:9], fn_variant, *args[9:], ev))
     return losses, grads
 
 

@@ -190,14 +190,15 @@ __device__ __forceinline__ float pick4(const float4& v, int k) {
 // Kernel launchers (defined in k1_lse_gather.cu, k2_alpha_beta.cu, k3_grad.cu).
 // ---------------------------------------------------------------------------------------------------
 struct Problem {
-    const float* logits;
+    const void* logits;  // fp32 / fp16 / bf16 per `dtype` (elem.cuh)
     const int32_t* targets;
     const int32_t* T_b;
     const int32_t* U_b;
     int B, Tmax, Umax, V, blank, variant;
     float* losses;
-    float* grads;
+    void* grads;  // same storage type as logits, or nullptr
     const float* grad_scale;
+    int dtype;
 };
 
 cudaError_t launch_k1_lse_gather(const Problem& p, const Workspace& w, cudaStream_t s);

@@ -4,23 +4,26 @@
 // and §2.2 P:88 / §2.3 P:92 (Populate = "indexed selection": every horizontal arc of the grid takes
 // X[t,u,blank], every vertical arc X[t,u,y_{u+1}]).
 //
-// One warp per (b,t,u) row of V logits, streamed once from HBM with 128-bit loads (8 per lane in flight
-// per chunk = 4 KB per warp) under an L2 evict-first policy, so the workspace the next kernels reuse stays
-// in L2.  Per lane: 3-input max (FMNMX3), one ex2 per element with packed FFMA2/FADD2 around it; across
-// chunks a lane-local online rescale; across lanes one max-reduce, one rescale, one sum-reduce.  The two
-// gathered logits are fetched by lanes 0 / 1 with scalar loads that merge in L2 with the row's loads.
-// Writes lse (fp32, row-major) and (X_blank, X_label) into the anti-diagonal-major lp array that the K2 wavefront reads.  Padded rows
-// (t >= T_b or u > U_b) are skipped: never read.
+// One warp per (b,t,u) row of V logits, streamed once from HBM with 128-bit loads (32 elements per lane in
+// flight per chunk: 4 KB per warp for fp32, 2 KB for fp16/bf16) under an L2 evict-first policy, so the
+// workspace the next kernels reuse stays in L2.  Per lane: 3-input max (FMNMX3), one ex2 per element with
+// packed FFMA2/FADD2 around it; across chunks a lane-local online rescale; across lanes one max-reduce,
+// one rescale, one sum-reduce.  16-bit logits are widened to fp32 in registers (half-precision
+// populate, fp32/fp64 scores).  The two gathered logits are fetched by lanes 0 / 1 with scalar loads
+// that merge in L2 with the row's loads.  Writes lse (fp32, row-major) and (X_blank, X_label) into the
+// anti-diagonal-major lp array that the K2 wavefront reads.  Padded rows (t >= T_b or u > U_b) are
+// skipped: never read.
 #include "common.cuh"
+#include "elem.cuh"
 
 namespace rnnt {
 namespace {
 
-constexpr int kUnroll = 8;  // float4 per lane per chunk
+constexpr int kPerLane = 32;  // elements per lane per chunk
 
-template <bool kVec>
+template <typename Z, bool kVec>
 __global__ void __launch_bounds__(kRowWarpsPerBlock * 32)
-    k1_lse_gather(const float* __restrict__ logits, const int32_t* __restrict__ targets,
+    k1_lse_gather(const Z* __restrict__ logits, const int32_t* __restrict__ targets,
                   const int32_t* __restrict__ T_b, const int32_t* __restrict__ U_b, int b0, int Tmax, int Umax,
                   int V, int blank, float* __restrict__ lse_out, double2* __restrict__ lp_out) {
     const int lane = threadIdx.x & 31;
@@ -40,66 +43,66 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32)
     if (ybad) yv = -1;
 
     const int64_t row = static_cast<int64_t>(b) * Tmax * Up1 + r;
-    const float* zrow = logits + row * static_cast<int64_t>(V);
-    float m = -INFINITY;  // lane-local running max
-    float s = 0.f;        // lane-local sum of e^(x - m)
+    const Z* zrow = logits + row * static_cast<int64_t>(V);
     // Populate gather: lanes 0 / 1 fetch z[blank] / z[y] with scalar loads issued alongside the row's
     // loads (same sectors, merged in L2: no extra DRAM traffic, no register indexing).
     float zb = 0.f, zy = 0.f;
-    if (lane == 0) zb = ld_stream_ro(zrow + blank);
-    if (lane == 1 && yv >= 0) zy = ld_stream_ro(zrow + yv);
+    if (lane == 0) zb = lds_scalar(zrow + blank);
+    if (lane == 1 && yv >= 0) zy = lds_scalar(zrow + yv);
+
+    float m = -INFINITY;  // lane-local running max
+    float s = 0.f;        // lane-local sum of e^(x - m)
+    const f32x2 l2e = pk(kLog2e, kLog2e);
+    auto absorb = [&](const float (&x)[kPerLane]) {  // online max / sum-exp update with one chunk
+        float cm = m;
+#pragma unroll
+        for (int i = 0; i < kPerLane; i += 2) cm = max3(cm, x[i], x[i + 1]);
+        if (cm == -INFINITY) return;
+        const float sc = (m == -INFINITY) ? 0.f : ex2((m - cm) * kLog2e);
+        const f32x2 nml = pk(-cm * kLog2e, -cm * kLog2e);
+        f32x2 acc0 = pk(0.f, 0.f), acc1 = pk(0.f, 0.f);
+#pragma unroll
+        for (int i = 0; i < kPerLane; i += 4) {
+            acc0 = fadd2(acc0, ex2x2(ffma2(pk(x[i], x[i + 1]), l2e, nml)));
+            acc1 = fadd2(acc1, ex2x2(ffma2(pk(x[i + 2], x[i + 3]), l2e, nml)));
+        }
+        const float2 a = upk(fadd2(acc0, acc1));
+        s = fmaf(s, sc, a.x + a.y);
+        m = cm;
+    };
 
     if constexpr (kVec) {
+        constexpr int E = Elem<Z>::kPerVec, kU = kPerLane / E;
         const uint64_t pol = l2_evict_first();
-        const float4* row4 = reinterpret_cast<const float4*>(zrow);
-        const int nvec = V >> 2;
-        const f32x2 l2e = pk(kLog2e, kLog2e);
-        for (int base = 0; base < nvec; base += 32 * kUnroll) {
-            float4 x[kUnroll];
+        const uint4* row4 = reinterpret_cast<const uint4*>(zrow);
+        const int nvec = V / E;
+        for (int base = 0; base < nvec; base += 32 * kU) {
+            uint4 raw[kU];
 #pragma unroll
-            for (int j = 0; j < kUnroll; ++j) {
+            for (int j = 0; j < kU; ++j) {
                 const int i = base + j * 32 + lane;
-                x[j] = (i < nvec) ? ld_stream_ro(row4 + i, pol)
-                                  : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+                raw[j] = (i < nvec) ? ldv_ro(row4 + i, pol) : make_uint4(0u, 0u, 0u, 0u);
             }
-            float cm = m;
+            float x[kPerLane];
 #pragma unroll
-            for (int j = 0; j < kUnroll; ++j) cm = max3(max3(cm, x[j].x, x[j].y), x[j].z, x[j].w);
-            if (cm != -INFINITY) {
-                const float sc = (m == -INFINITY) ? 0.f : ex2((m - cm) * kLog2e);
-                const f32x2 nml = pk(-cm * kLog2e, -cm * kLog2e);
-                f32x2 acc0 = pk(0.f, 0.f), acc1 = pk(0.f, 0.f);
+            for (int j = 0; j < kU; ++j) {
+                float f[E];
+                Elem<Z>::unpack(raw[j], f);
+                const bool in = base + j * 32 + lane < nvec;
 #pragma unroll
-                for (int j = 0; j < kUnroll; ++j) {
-                    acc0 = fadd2(acc0, ex2x2(ffma2(pk(x[j].x, x[j].y), l2e, nml)));
-                    acc1 = fadd2(acc1, ex2x2(ffma2(pk(x[j].z, x[j].w), l2e, nml)));
-                }
-                const float2 a = upk(fadd2(acc0, acc1));
-                s = fmaf(s, sc, a.x + a.y);
-                m = cm;
+                for (int e = 0; e < E; ++e) x[j * E + e] = in ? f[e] : -INFINITY;
             }
+            absorb(x);
         }
     } else {
-        constexpr int kS = 4 * kUnroll;  // scalars per lane per chunk
-        for (int base = 0; base < V; base += 32 * kS) {
-            float x[kS];
+        for (int base = 0; base < V; base += 32 * kPerLane) {
+            float x[kPerLane];
 #pragma unroll
-            for (int j = 0; j < kS; ++j) {
+            for (int j = 0; j < kPerLane; ++j) {
                 const int i = base + j * 32 + lane;
-                x[j] = (i < V) ? ld_stream_ro(zrow + i) : -INFINITY;
+                x[j] = (i < V) ? lds_scalar(zrow + i) : -INFINITY;
             }
-            float cm = m;
-#pragma unroll
-            for (int j = 0; j < kS; ++j) cm = fmaxf(cm, x[j]);
-            if (cm != -INFINITY) {
-                const float sc = (m == -INFINITY) ? 0.f : ex2((m - cm) * kLog2e);
-                const float nml = -cm * kLog2e;
-                float acc = 0.f;
-#pragma unroll
-                for (int j = 0; j < kS; ++j) acc += ex2(fmaf(x[j], kLog2e, nml));
-                s = fmaf(s, sc, acc);
-                m = cm;
-            }
+            absorb(x);
         }
     }
 
@@ -111,7 +114,6 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32)
     float S = (m == -INFINITY) ? 0.f : s * ex2((m - M) * kLog2e);
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) S += __shfl_xor_sync(0xffffffffu, S, off);
-
     zb = __shfl_sync(0xffffffffu, zb, 0);
     zy = __shfl_sync(0xffffffffu, zy, 1);
 
@@ -131,23 +133,34 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32)
     }
 }
 
-}  // namespace
-
-cudaError_t launch_k1_lse_gather(const Problem& p, const Workspace& w, cudaStream_t s) {
+template <typename Z>
+cudaError_t launch_t(const Problem& p, const Workspace& w, cudaStream_t s) {
     const int64_t rows_per_utt = static_cast<int64_t>(p.Tmax) * (p.Umax + 1);
     const int64_t bx = (rows_per_utt + kRowWarpsPerBlock - 1) / kRowWarpsPerBlock;
     if (rows_per_utt > 0x7fffffffLL || bx > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-    const bool vec = (p.V % 4 == 0) && (reinterpret_cast<uintptr_t>(p.logits) % 16 == 0);
+    const Z* z = static_cast<const Z*>(p.logits);
+    const bool vec = (p.V % Elem<Z>::kPerVec == 0) && (reinterpret_cast<uintptr_t>(z) % 16 == 0);
     for (int b0 = 0; b0 < p.B; b0 += 65535) {
         const dim3 grid(static_cast<unsigned>(bx), static_cast<unsigned>(min(65535, p.B - b0)));
         if (vec)
-            k1_lse_gather<true><<<grid, kRowWarpsPerBlock * 32, 0, s>>>(
-                p.logits, p.targets, p.T_b, p.U_b, b0, p.Tmax, p.Umax, p.V, p.blank, w.lse, w.lp);
+            k1_lse_gather<Z, true><<<grid, kRowWarpsPerBlock * 32, 0, s>>>(
+                z, p.targets, p.T_b, p.U_b, b0, p.Tmax, p.Umax, p.V, p.blank, w.lse, w.lp);
         else
-            k1_lse_gather<false><<<grid, kRowWarpsPerBlock * 32, 0, s>>>(
-                p.logits, p.targets, p.T_b, p.U_b, b0, p.Tmax, p.Umax, p.V, p.blank, w.lse, w.lp);
+            k1_lse_gather<Z, false><<<grid, kRowWarpsPerBlock * 32, 0, s>>>(
+                z, p.targets, p.T_b, p.U_b, b0, p.Tmax, p.Umax, p.V, p.blank, w.lse, w.lp);
     }
     return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_k1_lse_gather(const Problem& p, const Workspace& w, cudaStream_t s) {
+    switch (p.dtype) {
+        case kF32: return launch_t<float>(p, w, s);
+        case kF16: return launch_t<__half>(p, w, s);
+        case kBF16: return launch_t<__nv_bfloat16>(p, w, s);
+    }
+    return cudaErrorInvalidValue;
 }
 
 }  // namespace rnnt

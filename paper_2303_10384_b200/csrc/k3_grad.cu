@@ -10,22 +10,25 @@
 // not equal exp(alpha + beta - logP).  Padded cells, invalid utterances (logP NaN) and no-path
 // utterances (logP = -inf) get exact zeros, written without reading the logits.
 //
-// One warp per row; 128-bit loads and evict-first 128-bit stores; one ex2 per element.  In place is
-// safe: every element is loaded by the thread that later stores its gradient, and rows never share data.
+// One warp per row; 128-bit loads and 128-bit stores under an L2 evict-first policy; one ex2 per element;
+// fp32 arithmetic, grads stored in the logits' storage type (fp32 / fp16 / bf16, round to nearest).  In
+// place is safe: every element is loaded by the thread that later stores its gradient, and rows never
+// share data.
 #include "common.cuh"
+#include "elem.cuh"
 
 namespace rnnt {
 namespace {
 
-constexpr int kUnroll = 8;
+constexpr int kPerLane = 32;  // elements per lane per chunk
 
-template <bool kVec>
+template <typename Z, bool kVec>
 __global__ void __launch_bounds__(kRowWarpsPerBlock * 32)
-    k3_grad(const float* logits, const int32_t* __restrict__ targets, const int32_t* __restrict__ T_b,
+    k3_grad(const Z* logits, const int32_t* __restrict__ targets, const int32_t* __restrict__ T_b,
             const int32_t* __restrict__ U_b, int b0, int Tmax, int Umax, int V, int blank,
             const float* __restrict__ grad_scale, const float* __restrict__ lse_in,
             const double2* __restrict__ lp_in, const double* __restrict__ alpha,
-            const double* __restrict__ beta, const double* __restrict__ logp, float* grads) {
+            const double* __restrict__ beta, const double* __restrict__ logp, Z* grads) {
     const int lane = threadIdx.x & 31;
     const int b = b0 + static_cast<int>(blockIdx.y);
     const int Up1 = Umax + 1;
@@ -39,16 +42,17 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32)
     const bool live = (t < T) && (u <= U) && isfinite(lP);
 
     const int64_t row = static_cast<int64_t>(b) * Tmax * Up1 + r;
-    float* grow = grads + row * static_cast<int64_t>(V);
-    const float* zrow = logits + row * static_cast<int64_t>(V);
+    Z* grow = grads + row * static_cast<int64_t>(V);
+    const Z* zrow = logits + row * static_cast<int64_t>(V);
+    constexpr int E = Elem<Z>::kPerVec;
 
     if (!live) {
         if constexpr (kVec) {
-            float4* g4 = reinterpret_cast<float4*>(grow);
-            const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int i = lane; i < (V >> 2); i += 32) st_stream(g4 + i, zero);
+            const uint64_t pol = l2_evict_first();
+            uint4* g4 = reinterpret_cast<uint4*>(grow);
+            for (int i = lane; i < V / E; i += 32) stv(g4 + i, make_uint4(0u, 0u, 0u, 0u), pol);
         } else {
-            for (int i = lane; i < V; i += 32) st_stream(grow + i, 0.f);
+            for (int i = lane; i < V; i += 32) grow[i] = Elem<Z>::from_f32(0.f);
         }
         return;
     }
@@ -74,80 +78,98 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32)
     const float lsel = (lse == -INFINITY) ? INFINITY : lse * kLog2e;  // all -inf row -> p = 0
 
     if constexpr (kVec) {
+        constexpr int kU = kPerLane / E;
         const uint64_t pol = l2_evict_first();
-        const float4* z4 = reinterpret_cast<const float4*>(zrow);
-        float4* g4 = reinterpret_cast<float4*>(grow);
-        const int nvec = V >> 2;
-        const int bq = blank >> 2, yq = (yv < 0) ? -1 : (yv >> 2);
+        const uint4* z4 = reinterpret_cast<const uint4*>(zrow);
+        uint4* g4 = reinterpret_cast<uint4*>(grow);
+        const int nvec = V / E;
+        const int bq = blank / E, yq = (yv < 0) ? -1 : (yv / E);
+        const int bk = blank % E, yk = (yv < 0) ? 0 : (yv % E);
         const f32x2 l2e = pk(kLog2e, kLog2e), nl = pk(-lsel, -lsel), g2 = pk(gam, gam);
-        for (int base = 0; base < nvec; base += 32 * kUnroll) {
-            float4 x[kUnroll];
+        for (int base = 0; base < nvec; base += 32 * kU) {
+            uint4 raw[kU];
 #pragma unroll
-            for (int j = 0; j < kUnroll; ++j) {
+            for (int j = 0; j < kU; ++j) {
                 const int i = base + j * 32 + lane;
-                if (i < nvec) x[j] = ld_stream(z4 + i, pol);
+                if (i < nvec) raw[j] = ldv(z4 + i, pol);
             }
 #pragma unroll
-            for (int j = 0; j < kUnroll; ++j) {
+            for (int j = 0; j < kU; ++j) {
                 const int i = base + j * 32 + lane;
                 if (i < nvec) {
-                    const float2 lo = upk(fmul2(ex2x2(ffma2(pk(x[j].x, x[j].y), l2e, nl)), g2));
-                    const float2 hi = upk(fmul2(ex2x2(ffma2(pk(x[j].z, x[j].w), l2e, nl)), g2));
-                    float4 g = make_float4(lo.x, lo.y, hi.x, hi.y);
+                    float x[E], g[E];
+                    Elem<Z>::unpack(raw[j], x);
+#pragma unroll
+                    for (int e = 0; e < E; e += 2) {
+                        const float2 p = upk(fmul2(ex2x2(ffma2(pk(x[e], x[e + 1]), l2e, nl)), g2));
+                        g[e] = p.x;
+                        g[e + 1] = p.y;
+                    }
                     if (i == bq) {  // the arcs' own logits: subtract their occupancies (owner lane only)
-                        const int k = blank & 3;
-                        if (k == 0) g.x -= sb; else if (k == 1) g.y -= sb; else if (k == 2) g.z -= sb; else g.w -= sb;
+#pragma unroll
+                        for (int e = 0; e < E; ++e) g[e] -= (e == bk) ? sb : 0.f;
                     }
                     if (i == yq) {
-                        const int k = yv & 3;
-                        if (k == 0) g.x -= sy; else if (k == 1) g.y -= sy; else if (k == 2) g.z -= sy; else g.w -= sy;
+#pragma unroll
+                        for (int e = 0; e < E; ++e) g[e] -= (e == yk) ? sy : 0.f;
                     }
-                    st_stream(g4 + i, g, pol);
+                    stv(g4 + i, Elem<Z>::pack(g), pol);
                 }
             }
         }
     } else {
-        constexpr int kS = 4 * kUnroll;
-        for (int base = 0; base < V; base += 32 * kS) {
-            float x[kS];
+        for (int base = 0; base < V; base += 32 * kPerLane) {
+            float x[kPerLane];
 #pragma unroll
-            for (int j = 0; j < kS; ++j) {
+            for (int j = 0; j < kPerLane; ++j) {
                 const int i = base + j * 32 + lane;
-                if (i < V) x[j] = ld_stream(zrow + i);
+                if (i < V) x[j] = Elem<Z>::to_f32(zrow[i]);
             }
 #pragma unroll
-            for (int j = 0; j < kS; ++j) {
+            for (int j = 0; j < kPerLane; ++j) {
                 const int i = base + j * 32 + lane;
                 if (i < V) {
                     const float g = ex2(fmaf(x[j], kLog2e, -lsel)) * gam - (i == blank ? sb : 0.f) -
                                     (i == yv ? sy : 0.f);
-                    st_stream(grow + i, g);
+                    grow[i] = Elem<Z>::from_f32(g);
                 }
             }
         }
     }
 }
 
-}  // namespace
-
-cudaError_t launch_k3_grad(const Problem& p, const Workspace& w, cudaStream_t s) {
+template <typename Z>
+cudaError_t launch_t(const Problem& p, const Workspace& w, cudaStream_t s) {
     const int64_t rows_per_utt = static_cast<int64_t>(p.Tmax) * (p.Umax + 1);
     const int64_t bx = (rows_per_utt + kRowWarpsPerBlock - 1) / kRowWarpsPerBlock;
     if (rows_per_utt > 0x7fffffffLL || bx > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-    const bool vec = (p.V % 4 == 0) && (reinterpret_cast<uintptr_t>(p.logits) % 16 == 0) &&
-                     (reinterpret_cast<uintptr_t>(p.grads) % 16 == 0);
+    const Z* z = static_cast<const Z*>(p.logits);
+    Z* g = static_cast<Z*>(p.grads);
+    const bool vec = (p.V % Elem<Z>::kPerVec == 0) && (reinterpret_cast<uintptr_t>(z) % 16 == 0) &&
+                     (reinterpret_cast<uintptr_t>(g) % 16 == 0);
     for (int b0 = 0; b0 < p.B; b0 += 65535) {
         const dim3 grid(static_cast<unsigned>(bx), static_cast<unsigned>(min(65535, p.B - b0)));
         if (vec)
-            k3_grad<true><<<grid, kRowWarpsPerBlock * 32, 0, s>>>(
-                p.logits, p.targets, p.T_b, p.U_b, b0, p.Tmax, p.Umax, p.V, p.blank, p.grad_scale, w.lse, w.lp,
-                w.alpha, w.beta, w.logp, p.grads);
+            k3_grad<Z, true><<<grid, kRowWarpsPerBlock * 32, 0, s>>>(
+                z, p.targets, p.T_b, p.U_b, b0, p.Tmax, p.Umax, p.V, p.blank, p.grad_scale, w.lse, w.lp, w.alpha,
+                w.beta, w.logp, g);
         else
-            k3_grad<false><<<grid, kRowWarpsPerBlock * 32, 0, s>>>(
-                p.logits, p.targets, p.T_b, p.U_b, b0, p.Tmax, p.Umax, p.V, p.blank, p.grad_scale, w.lse, w.lp,
-                w.alpha, w.beta, w.logp, p.grads);
+            k3_grad<Z, false><<<grid, kRowWarpsPerBlock * 32, 0, s>>>(
+                z, p.targets, p.T_b, p.U_b, b0, p.Tmax, p.Umax, p.V, p.blank, p.grad_scale, w.lse, w.lp, w.alpha,
+                w.beta, w.logp, g);
     }
     return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_k3_grad(const Problem& p, const Workspace& w, cudaStream_t s) {
+    switch (p.dtype) {
+        case kF32: return launch_t<float>(p, w, s);
+        case kF16: return launch_t<__half>(p, w, s);
+        case kBF16: return launch_t<__nv_bfloat16>(p, w, s);
+    }
+    return cudaErrorInvalidValue;
 }
 
 // Deterministic fp64 loss sum: one CTA, thread-strided partial sums then a fixed-shape tree.

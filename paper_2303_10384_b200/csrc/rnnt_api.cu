@@ -6,6 +6,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "elem.cuh"
 #include "rnnt_b200.h"
 
 using rnnt::Problem;
@@ -27,25 +28,30 @@ rnnt_status check_sizes(int B, int Tmax, int Umax, int V, int blank) {
 rnnt_status launch_path(const rnnt::Problem& p, const rnnt::Workspace& w, cudaStream_t s,
                         void* const* events);
 
-rnnt_status run(const float* logits, const int32_t* targets, const int32_t* logit_lens,
+rnnt_status run(const void* logits, int dtype, const int32_t* targets, const int32_t* logit_lens,
                 const int32_t* target_lens, int B, int Tmax, int Umax, int V, int blank, float* losses,
-                float* grads, const float* grad_scale, void* workspace, size_t workspace_bytes, void* stream,
+                void* grads, const float* grad_scale, void* workspace, size_t workspace_bytes, void* stream,
                 int variant, void* const* events = nullptr) {
     rnnt_status st = check_sizes(B, Tmax, Umax, V, blank);
     if (st != RNNT_OK) return st;
     if (variant < rnnt::kRnnt || variant > rnnt::kAllowIgnore) return RNNT_ERR_INVALID_ARG;
+    if (dtype != rnnt::kF32 && dtype != rnnt::kF16 && dtype != rnnt::kBF16) return RNNT_ERR_INVALID_ARG;
     if (B == 0) return RNNT_OK;  // empty batch: nothing to do
     if (!logits || !logit_lens || !target_lens || !losses || !workspace) return RNNT_ERR_INVALID_ARG;
     if (Umax > 0 && !targets) return RNNT_ERR_INVALID_ARG;
     if (workspace_bytes < rnnt::workspace_bytes(B, Tmax, Umax)) return RNNT_ERR_WORKSPACE_TOO_SMALL;
-    const size_t tensor_bytes = sizeof(float) * static_cast<size_t>(B) * Tmax * (Umax + 1) * V;
+    const size_t tensor_bytes = rnnt::dtype_size(dtype) * static_cast<size_t>(B) * Tmax * (Umax + 1) * V;
     if (grads && grads != logits && ranges_overlap(grads, tensor_bytes, logits, tensor_bytes))
         return RNNT_ERR_INVALID_ARG;
 
     Problem p{logits, targets, logit_lens, target_lens, B, Tmax, Umax, V, blank, variant, losses, grads,
-              grad_scale};
+              grad_scale, dtype};
     const Workspace w = rnnt::carve(workspace, B, Tmax, Umax);
     return launch_path(p, w, static_cast<cudaStream_t>(stream), events);
+}
+
+int variant_kind(int variant) {  // C-ABI variant code (-1 RNN-T, wrnnt_variant) -> internal kind
+    return (variant < 0) ? rnnt::kRnnt : (variant == WRNNT_FORCE_FINAL ? rnnt::kForceFinal : rnnt::kAllowIgnore);
 }
 
 // Utterances [b0, b0+nb) of a call: every array is utterance-major, so a chunk is a pointer offset.
@@ -54,12 +60,13 @@ void slice(const Problem& p, const Workspace& w, int b0, int nb, Problem& pc, Wo
     const int64_t cells = static_cast<int64_t>(p.Tmax) * Up1;
     pc = p;
     pc.B = nb;
-    pc.logits = p.logits + b0 * cells * p.V;
+    const int64_t esize = static_cast<int64_t>(rnnt::dtype_size(p.dtype));
+    pc.logits = static_cast<const char*>(p.logits) + b0 * cells * p.V * esize;
     pc.targets = p.targets ? p.targets + static_cast<int64_t>(b0) * p.Umax : nullptr;
     pc.T_b = p.T_b + b0;
     pc.U_b = p.U_b + b0;
     pc.losses = p.losses + b0;
-    pc.grads = p.grads ? p.grads + b0 * cells * p.V : nullptr;
+    pc.grads = p.grads ? static_cast<char*>(p.grads) + b0 * cells * p.V * esize : nullptr;
     pc.grad_scale = p.grad_scale ? p.grad_scale + b0 : nullptr;
     wc.lse = w.lse + b0 * cells;
     wc.lp = w.lp + b0 * Dmax * Up1;
@@ -176,8 +183,8 @@ rnnt_status rnnt_loss(const float* logits, const int32_t* targets, const int32_t
                       const int32_t* target_lens, int B, int Tmax, int Umax, int V, int blank, float* losses,
                       float* grads, const float* grad_scale, void* workspace, size_t workspace_bytes,
                       void* stream) {
-    return run(logits, targets, logit_lens, target_lens, B, Tmax, Umax, V, blank, losses, grads, grad_scale,
-               workspace, workspace_bytes, stream, rnnt::kRnnt);
+    return run(logits, rnnt::kF32, targets, logit_lens, target_lens, B, Tmax, Umax, V, blank, losses, grads,
+               grad_scale, workspace, workspace_bytes, stream, rnnt::kRnnt);
 }
 
 rnnt_status wrnnt_loss(const float* logits, const int32_t* targets, const int32_t* logit_lens,
@@ -191,8 +198,8 @@ rnnt_status wrnnt_loss(const float* logits, const int32_t* targets, const int32_
         v = rnnt::kAllowIgnore;
     else
         return RNNT_ERR_INVALID_ARG;
-    return run(logits, targets, logit_lens, target_lens, B, Tmax, Umax, V, blank, losses, grads, grad_scale,
-               workspace, workspace_bytes, stream, v);
+    return run(logits, rnnt::kF32, targets, logit_lens, target_lens, B, Tmax, Umax, V, blank, losses, grads,
+               grad_scale, workspace, workspace_bytes, stream, v);
 }
 
 rnnt_status rnnt_loss_timed(const float* logits, const int32_t* targets, const int32_t* logit_lens,
@@ -200,9 +207,17 @@ rnnt_status rnnt_loss_timed(const float* logits, const int32_t* targets, const i
                             float* losses, float* grads, const float* grad_scale, void* workspace,
                             size_t workspace_bytes, void* stream, int variant, void* const* events) {
     if (variant < -1 || variant > 1) return RNNT_ERR_INVALID_ARG;
-    const int kind = (variant < 0) ? rnnt::kRnnt : (variant == 0 ? rnnt::kForceFinal : rnnt::kAllowIgnore);
-    return run(logits, targets, logit_lens, target_lens, B, Tmax, Umax, V, blank, losses, grads, grad_scale,
-               workspace, workspace_bytes, stream, kind, events);
+    return run(logits, rnnt::kF32, targets, logit_lens, target_lens, B, Tmax, Umax, V, blank, losses, grads,
+               grad_scale, workspace, workspace_bytes, stream, variant_kind(variant), events);
+}
+
+rnnt_status rnnt_loss_ex(const void* logits, rnnt_dtype dtype, const int32_t* targets, const int32_t* logit_lens,
+                         const int32_t* target_lens, int B, int Tmax, int Umax, int V, int blank, int variant,
+                         float* losses, void* grads, const float* grad_scale, void* workspace,
+                         size_t workspace_bytes, void* stream, void* const* events) {
+    if (variant < -1 || variant > 1) return RNNT_ERR_INVALID_ARG;
+    return run(logits, static_cast<int>(dtype), targets, logit_lens, target_lens, B, Tmax, Umax, V, blank, losses,
+               grads, grad_scale, workspace, workspace_bytes, stream, variant_kind(variant), events);
 }
 
 rnnt_status rnnt_loss_sum(const float* losses, int B, double* loss_sum, void* stream) {
@@ -302,9 +317,9 @@ rnnt_status rnnt_loss_host(const float* logits_host, const int32_t* targets_host
             if (!good) break;
             void* ws = p + static_cast<size_t>(c) * ws_chunk;
             float* zc = d_logits + b0 * utt_elems;
-            rnnt_status r = run(zc, d_targets + static_cast<int64_t>(b0) * Umax, d_T + b0, d_U + b0, nb, Tmax,
-                                Umax, V, blank, d_losses + b0, grads_host ? zc : nullptr, nullptr, ws, ws_chunk,
-                                s, kind);
+            rnnt_status r = run(zc, rnnt::kF32, d_targets + static_cast<int64_t>(b0) * Umax, d_T + b0, d_U + b0,
+                                nb, Tmax, Umax, V, blank, d_losses + b0, grads_host ? zc : nullptr, nullptr, ws,
+                                ws_chunk, s, kind);
             if (r != RNNT_OK) {
                 ret = r;
                 good = false;
