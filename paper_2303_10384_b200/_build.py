@@ -16,7 +16,9 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB_DIR = os.path.join(PKG, "lib")
-LIB_PATH = os.path.join(LIB_DIR, "librnnt_b200.so")
+BUILD_PATH = os.path.join(LIB_DIR, "librnnt_b200.so")
+# RNNT_B200_LIB overrides the library the binding loads (A/B timing of kernel variants on one box).
+LIB_PATH = os.environ.get("RNNT_B200_LIB") or BUILD_PATH
 OBJ_DIR = os.path.join(PKG, "lib", "obj")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -36,16 +38,16 @@ def sources():
 
 
 def _stale() -> bool:
-    if not os.path.exists(LIB_PATH):
+    if not os.path.exists(BUILD_PATH):
         return True
-    t = os.path.getmtime(LIB_PATH)
+    t = os.path.getmtime(BUILD_PATH)
     deps = sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(INCLUDE, "*.h"))
     return any(os.path.getmtime(d) > t for d in deps)
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
-        return LIB_PATH
+        return BUILD_PATH
     os.makedirs(OBJ_DIR, exist_ok=True)
     cc = nvcc()
 
@@ -61,13 +63,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         for _, log in results:
             print(log)
-    tmp = LIB_PATH + f".tmp{os.getpid()}"
+    tmp = BUILD_PATH + f".tmp{os.getpid()}"
     r = subprocess.run([cc, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *[o for o, _ in results]],
                        capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB_PATH)
-    return LIB_PATH
+    os.replace(tmp, BUILD_PATH)
+    return BUILD_PATH
 
 
 if __name__ == "__main__":

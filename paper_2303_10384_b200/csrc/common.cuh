@@ -186,6 +186,24 @@ __device__ __forceinline__ float pick4(const float4& v, int k) {
     return k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
 }
 
+// n / d for 0 <= n < 2^31 and d >= 1 with one IMAD.HI + shift (round-up reciprocal, 31 + ceil(log2 d) bits).
+struct FastDiv {
+    uint32_t d, m;
+    int s;
+    __device__ __forceinline__ uint32_t div(uint32_t n) const { return d == 1 ? n : (__umulhi(n, m) >> s); }
+};
+inline FastDiv make_fastdiv(uint32_t d) {
+    FastDiv f{d, 0u, 0};
+    if (d > 1) {
+        int l = 0;
+        while ((1ull << l) < d) ++l;  // ceil(log2 d)
+        const int p = 31 + l;
+        f.m = static_cast<uint32_t>(((1ull << p) + d - 1) / d);
+        f.s = p - 32;
+    }
+    return f;
+}
+
 // ---------------------------------------------------------------------------------------------------
 // Kernel launchers (defined in k1_lse_gather.cu, k2_alpha_beta.cu, k3_grad.cu).
 // ---------------------------------------------------------------------------------------------------
@@ -202,6 +220,7 @@ struct Problem {
 };
 
 cudaError_t launch_k1_lse_gather(const Problem& p, const Workspace& w, cudaStream_t s);
+int lanes_per_row(int nvec);  // K1 / K3 row-group width for a row of nvec 128-bit vectors
 cudaError_t launch_k2_alpha_beta(const Problem& p, const Workspace& w, cudaStream_t s);
 cudaError_t launch_k3_grad(const Problem& p, const Workspace& w, cudaStream_t s);
 cudaError_t launch_loss_sum(const float* losses, int B, double* out, cudaStream_t s);

@@ -4,15 +4,16 @@
 // and §2.2 P:88 / §2.3 P:92 (Populate = "indexed selection": every horizontal arc of the grid takes
 // X[t,u,blank], every vertical arc X[t,u,y_{u+1}]).
 //
-// One warp per (b,t,u) row of V logits, streamed once from HBM with 128-bit loads (32 elements per lane in
-// flight per chunk: 4 KB per warp for fp32, 2 KB for fp16/bf16) under an L2 evict-first policy, so the
-// workspace the next kernels reuse stays in L2.  Per lane: 3-input max (FMNMX3), one ex2 per element with
-// packed FFMA2/FADD2 around it; across chunks a lane-local online rescale; across lanes one max-reduce,
-// one rescale, one sum-reduce.  16-bit logits are widened to fp32 in registers (half-precision
-// populate, fp32/fp64 scores).  The two gathered logits are fetched by lanes 0 / 1 with scalar loads
-// that merge in L2 with the row's loads.  Writes lse (fp32, row-major) and (X_blank, X_label) into the
-// anti-diagonal-major lp array that the K2 wavefront reads.  Padded rows (t >= T_b or u > U_b) are
-// skipped: never read.
+// Rows of V logits are streamed once from HBM with 128-bit loads under an L2 evict-first policy (so the
+// workspace the next kernels reuse stays in L2).  Wide rows: one warp per (b,t,u) row, 32 elements per lane
+// per chunk (k1_lse_gather_w).  Narrow rows (fp32 V <= 512, 16-bit V <= 512): a group of G = 4..16 lanes
+// per row with 8 x 128-bit loads per lane, so a warp still keeps 4 KB in flight (k1_lse_gather_g).  Per lane: max over the chunk (FMNMX3), then one ex2 per element with packed
+// FFMA2/FADD2 around it; across chunks a lane-local online rescale; across the G lanes one max-reduce,
+// one rescale, one sum-reduce (xor butterflies stay inside the group).  16-bit logits are widened to fp32
+// in registers (half-precision populate, fp32/fp64 scores).  The two gathered logits are fetched
+// by the group's lanes 0 / 1 with scalar loads that merge in L2 with the row's loads.  Writes lse (fp32,
+// row-major) and (X_blank, X_label) into the anti-diagonal-major lp array that the K2 wavefront reads.
+// Padded rows (t >= T_b or u > U_b) are never read.
 #include "common.cuh"
 #include "elem.cuh"
 
@@ -23,7 +24,7 @@ constexpr int kPerLane = 32;  // elements per lane per chunk
 
 template <typename Z, bool kVec>
 __global__ void __launch_bounds__(kRowWarpsPerBlock * 32)
-    k1_lse_gather(const Z* __restrict__ logits, const int32_t* __restrict__ targets,
+    k1_lse_gather_w(const Z* __restrict__ logits, const int32_t* __restrict__ targets,
                   const int32_t* __restrict__ T_b, const int32_t* __restrict__ U_b, int b0, int Tmax, int Umax,
                   int V, int blank, float* __restrict__ lse_out, double2* __restrict__ lp_out) {
     const int lane = threadIdx.x & 31;
@@ -133,20 +134,168 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32)
     }
 }
 
+
+constexpr int kVecPerLane = 8;  // 128-bit loads per lane per chunk
+
+template <typename Z, int G>
+__global__ void __launch_bounds__(kRowWarpsPerBlock * 32)
+    k1_lse_gather_g(const Z* __restrict__ logits, const int32_t* __restrict__ targets,
+                  const int32_t* __restrict__ T_b, const int32_t* __restrict__ U_b, int b0, int Tmax, int Umax,
+                  int V, int blank, float* __restrict__ lse_out, double2* __restrict__ lp_out) {
+    constexpr int E = Elem<Z>::kPerVec, kU = kVecPerLane, kRowsPerWarp = 32 / G;
+    const int lane = threadIdx.x & 31;
+    const int sl = lane & (G - 1);  // lane within the row group
+    const int b = b0 + static_cast<int>(blockIdx.y);
+    const int Up1 = Umax + 1;
+    const int r = (static_cast<int>(blockIdx.x) * kRowWarpsPerBlock + (threadIdx.x >> 5)) * kRowsPerWarp + lane / G;
+    const int t = r / Up1;
+    const int u = r - t * Up1;
+    const int T = min(T_b[b], Tmax);
+    const int U = min(U_b[b], Umax);
+    // A group whose row is padding (or beyond the grid) loads nothing and stores nothing, but still takes
+    // part in the warp's shuffles.
+    const bool live = (r < Tmax * Up1) && (t < T) && (u <= U);
+    if (__all_sync(0xffffffffu, !live)) return;
+
+    int yv = -1;
+    if (live && u < U) yv = targets[static_cast<int64_t>(b) * Umax + u];
+    const bool ybad = (u < U) && (yv < 0 || yv >= V || yv == blank);
+    if (ybad) yv = -1;
+
+    const int64_t row = static_cast<int64_t>(b) * Tmax * Up1 + r;
+    const Z* zrow = logits + row * static_cast<int64_t>(V);
+    const uint4* row4 = reinterpret_cast<const uint4*>(zrow);
+    const uint64_t pol = l2_evict_first();
+    // Populate gather: lanes 0 / 1 of the group fetch z[blank] / z[y] with scalar loads issued alongside the
+    // row's loads (same sectors, merged in L2: no extra DRAM traffic, no register indexing).
+    float zb = 0.f, zy = 0.f;
+    if (live && sl == 0) zb = lds_scalar(zrow + blank);
+    if (live && sl == 1 && yv >= 0) zy = lds_scalar(zrow + yv);
+
+    const int nvec = V / E;
+    const f32x2 l2e = pk(kLog2e, kLog2e);
+    float m = -INFINITY;  // lane-local running max
+    float s = 0.f;        // lane-local sum of e^(x - m)
+    for (int base = 0; base < nvec; base += G * kU) {
+        uint4 raw[kU];
+#pragma unroll
+        for (int j = 0; j < kU; ++j) {
+            const int i = base + j * G + sl;
+            raw[j] = (live && i < nvec) ? ldv_ro(row4 + i, pol) : make_uint4(0u, 0u, 0u, 0u);
+        }
+        // Only a partial last chunk needs -inf fill for the slots past V (warp-uniform condition).
+        const bool partial = base + G * kU > nvec;
+        // Pass 1: chunk max (widening 16-bit values on the fly).
+        float cm = m;
+#pragma unroll
+        for (int j = 0; j < kU; ++j) {
+            float f[E];
+            Elem<Z>::unpack(raw[j], f);
+            if (partial && base + j * G + sl >= nvec) {
+#pragma unroll
+                for (int e = 0; e < E; ++e) f[e] = -INFINITY;
+            }
+#pragma unroll
+            for (int e = 0; e < E; e += 2) cm = max3(cm, f[e], f[e + 1]);
+        }
+        if (cm == -INFINITY) continue;
+        // Pass 2: sum of 2^((x - cm) log2 e), rescaling the running sum once.
+        const float sc = (m == -INFINITY) ? 0.f : ex2((m - cm) * kLog2e);
+        const f32x2 nml = pk(-cm * kLog2e, -cm * kLog2e);
+        f32x2 acc0 = pk(0.f, 0.f), acc1 = pk(0.f, 0.f);
+#pragma unroll
+        for (int j = 0; j < kU; ++j) {
+            float f[E];
+            Elem<Z>::unpack(raw[j], f);
+            if (partial && base + j * G + sl >= nvec) {
+#pragma unroll
+                for (int e = 0; e < E; ++e) f[e] = -INFINITY;
+            }
+#pragma unroll
+            for (int e = 0; e < E; e += 4) {
+                acc0 = fadd2(acc0, ex2x2(ffma2(pk(f[e], f[e + 1]), l2e, nml)));
+                acc1 = fadd2(acc1, ex2x2(ffma2(pk(f[e + 2], f[e + 3]), l2e, nml)));
+            }
+        }
+        const float2 a = upk(fadd2(acc0, acc1));
+        s = fmaf(s, sc, a.x + a.y);
+        m = cm;
+    }
+
+    // Group combine: M = max over the G lanes; S = sum of s * e^(m - M).  Xor butterflies with offsets < G
+    // stay inside the group and leave every lane bit-identical (IEEE max/add are commutative).
+    float M = m;
+#pragma unroll
+    for (int off = G / 2; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+    float S = (m == -INFINITY) ? 0.f : s * ex2((m - M) * kLog2e);
+#pragma unroll
+    for (int off = G / 2; off > 0; off >>= 1) S += __shfl_xor_sync(0xffffffffu, S, off);
+    const int g0 = lane & ~(G - 1);
+    zb = __shfl_sync(0xffffffffu, zb, g0);
+    zy = __shfl_sync(0xffffffffu, zy, g0 + 1);
+
+    if (live && sl == 0) {
+        const float lse = (M == -INFINITY) ? -INFINITY : M + lg2(S) * kLn2;
+        lse_out[row] = lse;
+        float xb, xy;
+        if (lse == -INFINITY) {  // an all -inf row forbids its arcs (reading R12)
+            xb = -INFINITY;
+            xy = -INFINITY;
+        } else {
+            xb = zb - lse;
+            xy = (u < U) ? (ybad ? __int_as_float(0x7fc00000) : zy - lse) : -INFINITY;
+        }
+        const int64_t diag = static_cast<int64_t>(b) * (Tmax + Umax) + (t + u);
+        lp_out[diag * Up1 + u] = make_double2(xb, xy);
+    }
+}
+
+template <typename Z, int G>
+void launch_g(const Problem& p, const Workspace& w, cudaStream_t s, const Z* z, int64_t rows_per_utt) {
+    constexpr int kRowsPerBlock = kRowWarpsPerBlock * (32 / G);
+    const int64_t bx = (rows_per_utt + kRowsPerBlock - 1) / kRowsPerBlock;
+    for (int b0 = 0; b0 < p.B; b0 += 65535) {
+        const dim3 grid(static_cast<unsigned>(bx), static_cast<unsigned>(min(65535, p.B - b0)));
+        k1_lse_gather_g<Z, G><<<grid, kRowWarpsPerBlock * 32, 0, s>>>(z, p.targets, p.T_b, p.U_b, b0, p.Tmax,
+                                                                       p.Umax, p.V, p.blank, w.lse, w.lp);
+    }
+}
+
+}  // namespace
+
+// Lanes per row for the grouped kernels: the smallest power of two in [4, 32] whose 8-vector-per-lane
+// chunk covers the row (32 = use the one-warp-per-row kernels).
+int lanes_per_row(int nvec) {
+    int g = 4;
+    while (g < 32 && g * kVecPerLane < nvec) g *= 2;
+    return g;
+}
+
+namespace {
+
 template <typename Z>
 cudaError_t launch_t(const Problem& p, const Workspace& w, cudaStream_t s) {
     const int64_t rows_per_utt = static_cast<int64_t>(p.Tmax) * (p.Umax + 1);
-    const int64_t bx = (rows_per_utt + kRowWarpsPerBlock - 1) / kRowWarpsPerBlock;
-    if (rows_per_utt > 0x7fffffffLL || bx > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+    if (rows_per_utt > 0x7fffffffLL / 2) return cudaErrorInvalidConfiguration;
     const Z* z = static_cast<const Z*>(p.logits);
-    const bool vec = (p.V % Elem<Z>::kPerVec == 0) && (reinterpret_cast<uintptr_t>(z) % 16 == 0);
+    constexpr int E = Elem<Z>::kPerVec;
+    const bool vec = (p.V % E == 0) && (reinterpret_cast<uintptr_t>(z) % 16 == 0);
+    const int g = vec ? lanes_per_row(p.V / E) : 32;
+    if (g <= 8) {  // narrow rows: grouped kernel (measured: 16-lane groups lose to one warp per row in K1)
+        switch (g) {
+            case 4: launch_g<Z, 4>(p, w, s, z, rows_per_utt); break;
+            default: launch_g<Z, 8>(p, w, s, z, rows_per_utt); break;
+        }
+        return cudaGetLastError();
+    }
+    const int64_t bx = (rows_per_utt + kRowWarpsPerBlock - 1) / kRowWarpsPerBlock;
     for (int b0 = 0; b0 < p.B; b0 += 65535) {
         const dim3 grid(static_cast<unsigned>(bx), static_cast<unsigned>(min(65535, p.B - b0)));
         if (vec)
-            k1_lse_gather<Z, true><<<grid, kRowWarpsPerBlock * 32, 0, s>>>(
+            k1_lse_gather_w<Z, true><<<grid, kRowWarpsPerBlock * 32, 0, s>>>(
                 z, p.targets, p.T_b, p.U_b, b0, p.Tmax, p.Umax, p.V, p.blank, w.lse, w.lp);
         else
-            k1_lse_gather<Z, false><<<grid, kRowWarpsPerBlock * 32, 0, s>>>(
+            k1_lse_gather_w<Z, false><<<grid, kRowWarpsPerBlock * 32, 0, s>>>(
                 z, p.targets, p.T_b, p.U_b, b0, p.Tmax, p.Umax, p.V, p.blank, w.lse, w.lp);
     }
     return cudaGetLastError();

@@ -10,7 +10,8 @@
 // not equal exp(alpha + beta - logP).  Padded cells, invalid utterances (logP NaN) and no-path
 // utterances (logP = -inf) get exact zeros, written without reading the logits.
 //
-// One warp per row; 128-bit loads and 128-bit stores under an L2 evict-first policy; one ex2 per element;
+// Wide rows: one warp per row (k3_grad_w); narrow rows (V/vector < 256): a group of 4..16 lanes per row
+// (k3_grad_g), as K1.  128-bit loads and stores under an L2 evict-first policy; one ex2 per element;
 // fp32 arithmetic, grads stored in the logits' storage type (fp32 / fp16 / bf16, round to nearest).  In
 // place is safe: every element is loaded by the thread that later stores its gradient, and rows never
 // share data.
@@ -24,7 +25,7 @@ constexpr int kPerLane = 32;  // elements per lane per chunk
 
 template <typename Z, bool kVec>
 __global__ void __launch_bounds__(kRowWarpsPerBlock * 32)
-    k3_grad(const Z* logits, const int32_t* __restrict__ targets, const int32_t* __restrict__ T_b,
+    k3_grad_w(const Z* logits, const int32_t* __restrict__ targets, const int32_t* __restrict__ T_b,
             const int32_t* __restrict__ U_b, int b0, int Tmax, int Umax, int V, int blank,
             const float* __restrict__ grad_scale, const float* __restrict__ lse_in,
             const double2* __restrict__ lp_in, const double* __restrict__ alpha,
@@ -138,23 +139,138 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32)
     }
 }
 
+
+constexpr int kVecPerLane = 8;  // 128-bit vectors per lane per chunk
+
+// G lanes per (b,t,u) row (G = 4..32, see lanes_per_row): a warp keeps 8 x 128-bit loads per lane in
+// flight whatever V and the storage type, exactly as K1.
+template <typename Z, int G>
+__global__ void __launch_bounds__(kRowWarpsPerBlock * 32)
+    k3_grad_g(const Z* logits, const int32_t* __restrict__ targets, const int32_t* __restrict__ T_b,
+            const int32_t* __restrict__ U_b, int b0, int Tmax, int Umax, int V, int blank,
+            const float* __restrict__ grad_scale, const float* __restrict__ lse_in,
+            const double2* __restrict__ lp_in, const double* __restrict__ alpha,
+            const double* __restrict__ beta, const double* __restrict__ logp, Z* grads) {
+    constexpr int E = Elem<Z>::kPerVec, kU = kVecPerLane, kRowsPerWarp = 32 / G;
+    const int lane = threadIdx.x & 31;
+    const int sl = lane & (G - 1);
+    const int b = b0 + static_cast<int>(blockIdx.y);
+    const int Up1 = Umax + 1;
+    const int r = (static_cast<int>(blockIdx.x) * kRowWarpsPerBlock + (threadIdx.x >> 5)) * kRowsPerWarp + lane / G;
+    if (r >= Tmax * Up1) return;  // no shuffles below: groups are independent
+    const int t = r / Up1;
+    const int u = r - t * Up1;
+    const int T = T_b[b], U = U_b[b];
+    const double lP = logp[b];
+    // Valid lengths are guaranteed whenever lP is finite (K2 writes NaN otherwise).
+    const bool live = (t < T) && (u <= U) && isfinite(lP);
+
+    const int64_t row = static_cast<int64_t>(b) * Tmax * Up1 + r;
+    const uint64_t pol = l2_evict_first();
+    uint4* g4 = reinterpret_cast<uint4*>(grads + row * static_cast<int64_t>(V));
+    const uint4* z4 = reinterpret_cast<const uint4*>(logits + row * static_cast<int64_t>(V));
+    const int nvec = V / E;
+
+    if (!live) {  // padding / invalid / no-path: exact zeros, the logits are never read
+        for (int i = sl; i < nvec; i += G) stv(g4 + i, make_uint4(0u, 0u, 0u, 0u), pol);
+        return;
+    }
+
+    // Per-row scalars: occupancies of the two scored arcs leaving (t,u).
+    const int64_t dcell = (static_cast<int64_t>(b) * (Tmax + Umax) + (t + u)) * Up1 + u;  // diagonal t+u, slot u
+    const float lse = lse_in[row];
+    const double2 l = lp_in[dcell];
+    const double a = alpha[dcell];
+    float occ_b = 0.f, occ_y = 0.f;
+    if (t < T - 1)  // beta(t+1,u): diagonal t+u+1, slot u
+        occ_b = __expf(static_cast<float>(a + l.x + beta[dcell + Up1] - lP));
+    else if (u == U)
+        occ_b = __expf(static_cast<float>(a + l.x - lP));
+    int yv = -1;
+    if (u < U) {    // beta(t,u+1): diagonal t+u+1, slot u+1
+        occ_y = __expf(static_cast<float>(a + l.y + beta[dcell + Up1 + 1] - lP));
+        yv = targets[static_cast<int64_t>(b) * Umax + u];
+    }
+    const float scale = grad_scale ? grad_scale[b] : 1.f;
+    const float gam = (occ_b + occ_y) * scale;
+    const float sb = occ_b * scale, sy = occ_y * scale;
+    const float lsel = (lse == -INFINITY) ? INFINITY : lse * kLog2e;  // all -inf row -> p = 0
+
+    const int bq = blank / E, yq = (yv < 0) ? -1 : (yv / E);
+    const int bk = blank % E, yk = (yv < 0) ? 0 : (yv % E);
+    const f32x2 l2e = pk(kLog2e, kLog2e), nl = pk(-lsel, -lsel), g2 = pk(gam, gam);
+    for (int base = 0; base < nvec; base += G * kU) {
+        uint4 raw[kU];
+#pragma unroll
+        for (int j = 0; j < kU; ++j) {
+            const int i = base + j * G + sl;
+            if (i < nvec) raw[j] = ldv(z4 + i, pol);
+        }
+#pragma unroll
+        for (int j = 0; j < kU; ++j) {
+            const int i = base + j * G + sl;
+            if (i < nvec) {
+                float x[E], g[E];
+                Elem<Z>::unpack(raw[j], x);
+#pragma unroll
+                for (int e = 0; e < E; e += 2) {
+                    const float2 q = upk(fmul2(ex2x2(ffma2(pk(x[e], x[e + 1]), l2e, nl)), g2));
+                    g[e] = q.x;
+                    g[e + 1] = q.y;
+                }
+                if (i == bq) {  // the arcs' own logits: subtract their occupancies (owner lane only)
+#pragma unroll
+                    for (int e = 0; e < E; ++e) g[e] -= (e == bk) ? sb : 0.f;
+                }
+                if (i == yq) {
+#pragma unroll
+                    for (int e = 0; e < E; ++e) g[e] -= (e == yk) ? sy : 0.f;
+                }
+                stv(g4 + i, Elem<Z>::pack(g), pol);
+            }
+        }
+    }
+}
+
+template <typename Z, int G>
+void launch_g(const Problem& p, const Workspace& w, cudaStream_t s, const Z* z, Z* g, int64_t rows_per_utt) {
+    constexpr int kRowsPerBlock = kRowWarpsPerBlock * (32 / G);
+    const int64_t bx = (rows_per_utt + kRowsPerBlock - 1) / kRowsPerBlock;
+    for (int b0 = 0; b0 < p.B; b0 += 65535) {
+        const dim3 grid(static_cast<unsigned>(bx), static_cast<unsigned>(min(65535, p.B - b0)));
+        k3_grad_g<Z, G><<<grid, kRowWarpsPerBlock * 32, 0, s>>>(z, p.targets, p.T_b, p.U_b, b0, p.Tmax, p.Umax,
+                                                                 p.V, p.blank, p.grad_scale, w.lse, w.lp, w.alpha,
+                                                                 w.beta, w.logp, g);
+    }
+}
+
 template <typename Z>
 cudaError_t launch_t(const Problem& p, const Workspace& w, cudaStream_t s) {
     const int64_t rows_per_utt = static_cast<int64_t>(p.Tmax) * (p.Umax + 1);
-    const int64_t bx = (rows_per_utt + kRowWarpsPerBlock - 1) / kRowWarpsPerBlock;
-    if (rows_per_utt > 0x7fffffffLL || bx > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+    if (rows_per_utt > 0x7fffffffLL / 2) return cudaErrorInvalidConfiguration;
     const Z* z = static_cast<const Z*>(p.logits);
     Z* g = static_cast<Z*>(p.grads);
-    const bool vec = (p.V % Elem<Z>::kPerVec == 0) && (reinterpret_cast<uintptr_t>(z) % 16 == 0) &&
+    constexpr int E = Elem<Z>::kPerVec;
+    const bool vec = (p.V % E == 0) && (reinterpret_cast<uintptr_t>(z) % 16 == 0) &&
                      (reinterpret_cast<uintptr_t>(g) % 16 == 0);
+    const int lanes = vec ? lanes_per_row(p.V / E) : 32;
+    if (lanes < 32) {  // narrow rows: grouped kernel
+        switch (lanes) {
+            case 4: launch_g<Z, 4>(p, w, s, z, g, rows_per_utt); break;
+            case 8: launch_g<Z, 8>(p, w, s, z, g, rows_per_utt); break;
+            default: launch_g<Z, 16>(p, w, s, z, g, rows_per_utt); break;
+        }
+        return cudaGetLastError();
+    }
+    const int64_t bx = (rows_per_utt + kRowWarpsPerBlock - 1) / kRowWarpsPerBlock;
     for (int b0 = 0; b0 < p.B; b0 += 65535) {
         const dim3 grid(static_cast<unsigned>(bx), static_cast<unsigned>(min(65535, p.B - b0)));
         if (vec)
-            k3_grad<Z, true><<<grid, kRowWarpsPerBlock * 32, 0, s>>>(
+            k3_grad_w<Z, true><<<grid, kRowWarpsPerBlock * 32, 0, s>>>(
                 z, p.targets, p.T_b, p.U_b, b0, p.Tmax, p.Umax, p.V, p.blank, p.grad_scale, w.lse, w.lp, w.alpha,
                 w.beta, w.logp, g);
         else
-            k3_grad<Z, false><<<grid, kRowWarpsPerBlock * 32, 0, s>>>(
+            k3_grad_w<Z, false><<<grid, kRowWarpsPerBlock * 32, 0, s>>>(
                 z, p.targets, p.T_b, p.U_b, b0, p.Tmax, p.Umax, p.V, p.blank, p.grad_scale, w.lse, w.lp, w.alpha,
                 w.beta, w.logp, g);
     }
