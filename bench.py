@@ -79,8 +79,10 @@ def ncu_traffic(kernel: str, cfg_name: str):
         return None
     with open(path) as f:
         d = json.load(f)
-    ent = d.get(cfg_name, {}).get(kernel)
-    return None if ent is None else float(ent["dram_bytes_per_launch"])
+    for fam, ent in d.get(cfg_name, {}).items():  # kernel families, e.g. "k3_grad_w" for "k3_grad"
+        if fam.startswith(kernel):
+            return float(ent["dram_bytes_per_launch"])
+    return None
 
 
 class ClockSampler:

@@ -167,8 +167,9 @@ rnnt_status launch_path(const Problem& p, const Workspace& w, cudaStream_t s, vo
 
 namespace {
 
-// Chunk size of the host path: enough chunks to overlap H2D(c+1) / compute(c) / D2H(c-1).
-int host_chunk(int B) { return std::max(1, (B + 7) / 8); }
+// Chunk size of the host path: ~16 chunks, so the pipeline fill (first H2D) and drain (last D2H) are short
+// against the overlapped middle where H2D(c+1), compute(c) and D2H(c-1) run together.
+int host_chunk(int B) { return std::max(1, (B + 15) / 16); }
 
 }  // namespace
 
