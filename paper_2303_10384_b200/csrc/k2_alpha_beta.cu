@@ -45,14 +45,22 @@ __device__ __forceinline__ double lse2f(double a, double b) {
     return m + static_cast<double>(c);
 }
 
-template <int kVariant, int kC, int kPf>
-__global__ void __launch_bounds__(128)
+// LSE over the 32 lanes of a warp; every lane ends with the same value (lse2f is symmetric).
+__device__ __forceinline__ double warp_lse(double v) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v = lse2f(v, __shfl_xor_sync(0xffffffffu, v, off));
+    return v;
+}
+
+template <int kVariant, int kC, int kPf, int kMaxThreads>
+__global__ void __launch_bounds__(kMaxThreads)
     k2_alpha_beta(const double2* __restrict__ lp, const int32_t* __restrict__ targets,
                   const int32_t* __restrict__ T_b, const int32_t* __restrict__ U_b, int Tmax, int Umax,
                   int V, int blank, double* __restrict__ alpha, double* __restrict__ beta,
                   double* __restrict__ logp, float* __restrict__ losses) {
     constexpr bool kW = kVariant != kRnnt;
-    __shared__ double xfer[2][4];
+    constexpr bool kMultiWarp = kMaxThreads > 32;
+    __shared__ double xfer[2][kMaxThreads / 32];
 
     const int b = blockIdx.x >> 1;
     const bool fwd = (blockIdx.x & 1) == 0;
@@ -81,7 +89,7 @@ __global__ void __launch_bounds__(128)
         return;
     }
     const int nact_lanes = (U + 1 + kC - 1) / kC;  // lanes owning at least one column
-    const int nwarps = (nact_lanes + 31) >> 5;
+    const int nwarps = kMultiWarp ? (nact_lanes + 31) >> 5 : 1;  // single-warp instances: no smem, no barrier
     if (warp >= nwarps) return;
     const int nthr = nwarps << 5;
 
@@ -148,11 +156,10 @@ __global__ void __launch_bounds__(128)
         // self[j]: alpha(t-1,u) + X_b(t-1,u) for the next cell of column u0+j (column 0 starts at 0 so that
         // cell (0,0) = LSE(0, -inf) = 0 exactly).  pub[j]: alpha(t,u) + X_y(t,u) of the last computed cell.
         if (u0 == 0) self[0] = 0.0;
-        double skip = -INFINITY;  // LSE_{t' <= T-2} alpha(t', U)   (lane owning column U, W variants)
         // One wavefront step d; x holds the step's (X_b, X_y) operands (staged a group ahead).
         auto fwd_step = [&](int d, const double2 (&x)[kC]) {
             double left = __shfl_up_sync(full, pub[kC - 1], 1);
-            if (nwarps > 1 && lane == 0) left = (warp > 0 && d > 0) ? xfer[(d - 1) & 1][warp - 1] : -INFINITY;
+            if (kMultiWarp && nwarps > 1 && lane == 0) left = (warp > 0 && d > 0) ? xfer[(d - 1) & 1][warp - 1] : -INFINITY;
             if (lane == 0 && warp == 0) left = -INFINITY;
 #pragma unroll
             for (int j = kC - 1; j >= 0; --j) {  // high to low: pub[j-1] is still last step's
@@ -163,37 +170,53 @@ __global__ void __launch_bounds__(128)
                 // Column 0 has no left neighbour; under W its second incoming arc is the initial skip
                 // (0,0)->(t,0) of weight 0, so one LSE per cell suffices on every column.
                 if (kW && u == 0) nb = (t >= 1) ? 0.0 : -INFINITY;
-                double cur = lse2f(self[j], nb);
-                if (kVariant == kForceFinal && u == U && t == T - 1) cur = lse2f(cur, skip);  // once
+                const double cur = lse2f(self[j], nb);
                 if (valid) st_ptr[j] = cur;
                 self[j] = valid ? cur + x[j].x : -INFINITY;
                 pub[j] = valid ? cur + x[j].y : -INFINITY;  // X_y(t,U) = -inf: no label arc leaves row U
-                if (kW) {  // running LSE of alpha(t', U), t' <= T-2: computed by every lane, kept by column U
-                    const double nskip = lse2f(skip, cur);
-                    skip = (valid && u == U && t <= T - 2) ? nskip : skip;
-                }
-                if (valid && u == U && t == T - 1) {
-                    double total = self[j];  // terminating blank (T-1,U) -> F
-                    if (kVariant == kAllowIgnore) total = lse2f(total, skip);
-                    logp[b] = total;
-                    losses[b] = static_cast<float>(-total);
-                }
             }
             st_ptr += step;
-            if (nwarps > 1) {
+            if (kMultiWarp && nwarps > 1) {
                 if (lane == 31) xfer[d & 1][warp] = pub[kC - 1];
                 named_barrier(nthr);
             }
         };
         run_groups(fwd_step);
+        // The final cell (T-1,U) is the last wavefront step and nothing but log P depends on it, so the final
+        // skip terms are applied afterwards by the warp owning column U: skip = LSE_{t'<=T-2} alpha(t',U)
+        // from the stored column (a warp reduction, not a per-step accumulator on the critical path), then
+        //   force-final:  alpha(T-1,U) <- LSE(alpha(T-1,U), skip),  log P = alpha(T-1,U) + X_b(T-1,U)
+        //   allow-ignore: log P = LSE(alpha(T-1,U) + X_b(T-1,U), skip)
+        const int ownerU = U / kC;
+        if (warp == (ownerU >> 5)) {
+            __syncwarp();
+            double* const colU = alpha + static_cast<int64_t>(b) * Dmax * Up1 + U;  // + (t+U)*Up1 -> alpha(t,U)
+            double skip = -INFINITY;
+            if (kW) {
+                for (int tp = lane; tp <= T - 2; tp += 32) skip = lse2f(skip, __ldcg(colU + static_cast<int64_t>(tp + U) * Up1));
+                skip = warp_lse(skip);
+            }
+            if (lane == (ownerU & 31)) {
+                const int64_t last = static_cast<int64_t>(T - 1 + U) * Up1;
+                double a = __ldcg(colU + last);
+                const double xb = __ldcg(&lp[static_cast<int64_t>(b) * Dmax * Up1 + last + U].x);
+                if (kVariant == kForceFinal) {
+                    a = lse2f(a, skip);
+                    colU[last] = a;
+                }
+                double total = a + xb;  // terminating blank (T-1,U) -> F
+                if (kVariant == kAllowIgnore) total = lse2f(total, skip);
+                logp[b] = total;
+                losses[b] = static_cast<float>(-total);
+            }
+        }
     } else {
         // self[j]: beta(t+1,u) (this column's previous cell); pub[j]: beta(t,u) for column u-1's next step.
         double fin = -INFINITY;    // beta(T-1,U)                  (lane owning column U, force-final)
-        double skip0 = -INFINITY;  // LSE_{t' >= 1} beta(t', 0)    (lane 0, W variants)
         auto bwd_step = [&](int i, const double2 (&x)[kC]) {
             const int d = D - 1 - i;
             double right = __shfl_down_sync(full, pub[0], 1);
-            if (nwarps > 1 && lane == 31)
+            if (kMultiWarp && nwarps > 1 && lane == 31)
                 right = (warp + 1 < nwarps && i > 0) ? xfer[(i - 1) & 1][warp + 1] : -INFINITY;
 #pragma unroll
             for (int j = 0; j < kC; ++j) {  // low to high: pub[j+1] is still last step's
@@ -208,53 +231,61 @@ __global__ void __launch_bounds__(128)
                 if (kVariant == kAllowIgnore && u == U) op2 = 0.0;
                 double cur = lse2f(self[j] + x[j].x, op2);
                 cur = last ? x[j].x : cur;
-                if (kW && t == 0 && u == 0) cur = lse2f(cur, skip0);  // initial skips, once
                 if (valid) st_ptr[j] = cur;
                 if (kVariant == kForceFinal) fin = (valid && last) ? cur : fin;
-                if (kW) {  // running LSE of beta(t', 0), t' >= 1: computed by every lane, kept by column 0
-                    const double nskip = lse2f(skip0, cur);
-                    skip0 = (valid && u == 0 && t >= 1) ? nskip : skip0;
-                }
                 self[j] = valid ? cur : -INFINITY;
                 pub[j] = self[j];
             }
             st_ptr += step;
-            if (nwarps > 1) {
+            if (kMultiWarp && nwarps > 1) {
                 if (lane == 0) xfer[i & 1][warp] = pub[0];
                 named_barrier(nthr);
             }
         };
         run_groups(bwd_step);
+        // Initial skips enter only beta(0,0) (the first cell, last step): warp 0 adds
+        // LSE_{t'>=1} beta(t',0) from the stored column afterwards.  beta(0,0) = log P is the check value.
+        if (kW && warp == 0) {
+            __syncwarp();
+            double* const col0 = beta + static_cast<int64_t>(b) * Dmax * Up1;  // + t*Up1 -> beta(t,0)
+            double skip0 = -INFINITY;
+            for (int tp = 1 + lane; tp <= T - 1; tp += 32) skip0 = lse2f(skip0, __ldcg(col0 + static_cast<int64_t>(tp) * Up1));
+            skip0 = warp_lse(skip0);
+            if (lane == 0) col0[0] = lse2f(__ldcg(col0), skip0);
+        }
     }
 }
 
-template <int kVariant, int kC, int kPf>
+template <int kVariant, int kC, int kPf, int kMaxThreads>
 void launch_c(const Problem& p, const Workspace& w, cudaStream_t s) {
     const int lanes = (p.Umax + 1 + kC - 1) / kC;
     const int threads = ((lanes + 31) / 32) * 32;
-    k2_alpha_beta<kVariant, kC, kPf><<<2 * p.B, threads, 0, s>>>(w.lp, p.targets, p.T_b, p.U_b, p.Tmax, p.Umax,
-                                                                 p.V, p.blank, w.alpha, w.beta, w.logp, p.losses);
+    k2_alpha_beta<kVariant, kC, kPf, kMaxThreads><<<2 * p.B, threads, 0, s>>>(
+        w.lp, p.targets, p.T_b, p.U_b, p.Tmax, p.Umax, p.V, p.blank, w.alpha, w.beta, w.logp, p.losses);
 }
 
-// Columns per lane: the smallest kC that keeps the CTA within 4 warps (128 threads), unless the
-// RNNT_K2_CELLS environment variable (1, 2, 4 or 8; a tuning knob) asks for more.
-int cells_per_lane(int up1) {
-    int c = (up1 <= 128) ? 1 : (up1 <= 256) ? 2 : (up1 <= 512) ? 4 : 8;
-    if (const char* e = getenv("RNNT_K2_CELLS")) {
-        const int want = atoi(e);
-        if ((want == 1 || want == 2 || want == 4 || want == 8) && want > c) c = want;
-    }
-    return c;
-}
-
+// Shape of the wavefront CTA (columns per lane kC, staging group kPf, thread bound) by Umax + 1.
+// Measured per step on B200 (T=500): one warp, 1 column per lane: 124 ns; one warp, 2 columns per lane:
+// 160 ns; 2-4 warps, 1 column per lane (a named barrier per step): ~200 ns.  So a single warp while
+// kC <= 2 covers the row, then one column per lane across warps; kPf shrinks as the per-thread register
+// budget does (65536 / threads).  RNNT_K2_CELLS=1|2 forces kC where the table allows it (tuning knob).
 template <int kVariant>
 void launch_variant(const Problem& p, const Workspace& w, cudaStream_t s) {
-    switch (cells_per_lane(p.Umax + 1)) {  // staging group = kPf steps, i.e. kPf..2*kPf steps of load slack
-        case 1: launch_c<kVariant, 1, 16>(p, w, s); break;
-        case 2: launch_c<kVariant, 2, 8>(p, w, s); break;
-        case 4: launch_c<kVariant, 4, 4>(p, w, s); break;
-        default: launch_c<kVariant, 8, 2>(p, w, s); break;
-    }
+    const int up1 = p.Umax + 1;
+    int force = 0;
+    if (const char* e = getenv("RNNT_K2_CELLS")) force = atoi(e);
+    if (up1 <= 32 && force != 2)
+        launch_c<kVariant, 1, 16, 32>(p, w, s);
+    else if (up1 <= 64 && force != 1)
+        launch_c<kVariant, 2, 8, 32>(p, w, s);
+    else if (up1 <= 128)
+        launch_c<kVariant, 1, 16, 128>(p, w, s);
+    else if (up1 <= 256 && force != 2)
+        launch_c<kVariant, 1, 16, 256>(p, w, s);
+    else if (up1 <= 512 && force != 2)
+        launch_c<kVariant, 1, 8, 512>(p, w, s);
+    else
+        launch_c<kVariant, 2, 4, 512>(p, w, s);
 }
 
 }  // namespace
