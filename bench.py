@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--dtype", default="f32", choices=["f32", "bf16", "f16"],
                     help="storage type of logits/grads (arithmetic is fp32/fp64 either way); the BASELINE "
                          "metric is quoted on f32")
+    ap.add_argument("--mode", default="loss_grad", choices=["loss_grad", "loss", "viterbi"],
+                    help="loss_grad: the BASELINE metric; loss: losses only (K1+K2); viterbi: forced alignment "
+                         "(K1+K4) -- SURVEY 8(f) NEXT-2")
     ap.add_argument("--inplace", action="store_true",
                     help="write grads over the logits (automatic when two copies do not fit in HBM, e.g. c5)")
     return ap.parse_args()
@@ -156,6 +159,16 @@ def oracle_sample(cfg, variant, nthreads, b_ids, pb=None):
     return time.perf_counter() - t0
 
 
+def launches_per_step(mode, B, cfg):
+    """Our kernels per step: K1/K2/K3 once per utterance chunk (<= 4 chunks when the call has >= 2^24
+    elements, see rnnt_api.cu overlap_chunks) + the loss sum; viterbi = K1 + K4."""
+    if mode == "viterbi":
+        return 2
+    elems = B * cfg.Tmax * (cfg.Umax + 1) * cfg.V
+    nch = min(B, 4) if (B >= 2 and elems >= (1 << 24)) else 1
+    return nch * (3 if mode == "loss_grad" else 2) + 1
+
+
 def host_cores():
     return len(os.sched_getaffinity(0))
 
@@ -257,8 +270,11 @@ def main():
     torch.cuda.synchronize()
 
     def step(events=None):
-        rb.rnnt_loss_timed(z, targets, T_b, U_b, gcfg.blank, variant, events=events, grads=grads,
-                           losses=losses, workspace=workspace)
+        if args.mode == "viterbi":
+            rb.rnnt_viterbi(z, targets, T_b, U_b, gcfg.blank, variant, workspace=workspace)
+            return
+        rb.rnnt_loss_timed(z, targets, T_b, U_b, gcfg.blank, variant, events=events,
+                           grads=grads if args.mode == "loss_grad" else False, losses=losses, workspace=workspace)
         rb.rnnt_loss_sum(losses, out=loss_sum)
         rdist.allreduce_loss_sum(loss_sum)
 
@@ -294,8 +310,23 @@ def main():
     k3_bytes = 2 * esize * valid_elems + esize * (all_elems - valid_elems)  # read+write valid, zero-write pad
     k1_bytes = esize * valid_elems
     peak, peak_src = measured_peaks()
-    k3_gbs = k3_bytes / (k_ms["k3_grad"] / 1e3) / 1e9
-    k1_gbs = k1_bytes / (k_ms["k1_lse_gather"] / 1e3) / 1e9
+    if args.mode != "loss_grad":  # no K3 (and, for viterbi, no per-kernel events): report K1 / the step
+        k_ms["k3_grad"] = 0.0
+        if args.mode == "viterbi":
+            k_ms = {"step(k1_lse_gather+k4_viterbi)": ms_step}
+    k3_gbs = k3_bytes / (k_ms["k3_grad"] / 1e3) / 1e9 if k_ms.get("k3_grad") else None
+    k1_ms = k_ms.get("k1_lse_gather", ms_step)
+    k1_gbs = k1_bytes / (k1_ms / 1e3) / 1e9
+    peak, peak_src = measured_peaks()
+    if args.mode == "loss_grad":
+        roof = {"bound": "hbm", "kernel": "k3_grad", "achieved": k3_gbs, "peak": peak, "unit": "GB/s",
+                "frac": k3_gbs / peak, "traffic": ncu_traffic("k3_grad", args.config),
+                "algorithmic_bytes_per_launch": k3_bytes, "peak_source": peak_src}
+    else:
+        roof = {"bound": "hbm", "kernel": "k1_lse_gather" if args.mode == "loss" else "step (k1 + k4)",
+                "achieved": k1_gbs, "peak": peak, "unit": "GB/s", "frac": k1_gbs / peak,
+                "traffic": ncu_traffic("k1_lse_gather", args.config) if args.mode == "loss" else None,
+                "algorithmic_bytes_per_launch": k1_bytes, "peak_source": peak_src}
 
     # sanity: finite losses and the all-reduced sum
     loss_total = float(loss_sum.item())
@@ -304,24 +335,23 @@ def main():
     if rank == 0:
         clk = clocks.summary()
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+            "metric": METRIC if args.mode == "loss_grad" else f"utterances/s {args.mode} (not the BASELINE metric)",
+            "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
             "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": args.dtype, "data": "synthetic",
             "config": {"workload": workload_desc(base, variant), "variant": variant, "B_per_gpu": B,
                        "global_batch": B * world, "parallelism": f"dp{world} (batch shards, NCCL all-reduce of "
                        f"the fp64 loss sum)", "l2": f"inputs {z.numel() * esize / 1e9:.2f} GB/GPU > 126 MB L2: no flush",
                        "grads": "in place" if inplace else "out of place"},
-            "roofline": {"bound": "hbm", "kernel": "k3_grad", "achieved": k3_gbs, "peak": peak, "unit": "GB/s",
-                         "frac": k3_gbs / peak, "traffic": ncu_traffic("k3_grad", args.config),
-                         "algorithmic_bytes_per_launch": k3_bytes, "peak_source": peak_src},
+            "roofline": roof,
             "kernels_ms": k_ms,
             "kernel_gbs": {"k1_lse_gather": k1_gbs, "k3_grad": k3_gbs},
             "note": None if args.dtype == "f32" else "16-bit storage run (SURVEY §8(f) NEXT-1); the BASELINE "
                     "metric itself is fp32",
-            "kernel_frac_of_peak": {"k1_lse_gather": k1_gbs / peak, "k3_grad": k3_gbs / peak},
+            "kernel_frac_of_peak": {"k1_lse_gather": k1_gbs / peak, "k3_grad": k3_gbs and k3_gbs / peak},
             "step_frac_of_3pass_roofline": (3 * esize * valid_elems / (ms_step / 1e3) / 1e9) / peak,
             "clocks": clk,
-            "gpu_launches": 4 * K,
+            "gpu_launches": launches_per_step(args.mode, B, gcfg) * K,
             "loss_sum_last_step": loss_total,
         }
 

@@ -111,6 +111,20 @@ rnnt_status rnnt_loss_ex(const void* logits, rnnt_dtype dtype, const int32_t* ta
                          int V, int blank, int variant, float* losses, void* grads, const float* grad_scale,
                          void* workspace, size_t workspace_bytes, void* stream, void* const* events);
 
+/* Viterbi forced alignment (§2.1 P:80 "forced alignment tasks"): the single
+ * best path through the same lattice (max-plus instead of log-sum-exp), ties broken blank arc > label arc >
+ * skip arc, earliest frame among final skips (reading R21).  Outputs (device):
+ *   best_logp [B]        fp32 log-probability of the best alignment (NaN: invalid utterance; -inf: no path)
+ *   frames    [B][Umax]  frame at which unit u is emitted on the best path (u < U_b; -1 elsewhere)
+ *   span      [B][2]     (first, last) frame covered by scored arcs: > 0 / < T_b-1 when the W skips are taken;
+ *                        may be NULL.
+ * variant: -1 = plain RNN-T, else a wrnnt_variant.  Same inputs, workspace and stream conventions as
+ * rnnt_loss_ex; Umax + 1 <= 1024. */
+rnnt_status rnnt_viterbi(const void* logits, rnnt_dtype dtype, const int32_t* targets,
+                         const int32_t* logit_lens, const int32_t* target_lens, int B, int Tmax, int Umax,
+                         int V, int blank, int variant, float* best_logp, int32_t* frames, int32_t* span,
+                         void* workspace, size_t workspace_bytes, void* stream);
+
 /* Deterministic fp64 sum of losses[0..B) into *loss_sum (device), fixed summation order for a given B.
  * This is the per-rank operand of the cross-GPU all-reduce of the loss sum (BASELINE.json north_star (5)). */
 rnnt_status rnnt_loss_sum(const float* losses, int B, double* loss_sum, void* stream);

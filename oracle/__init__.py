@@ -52,6 +52,8 @@ def _load():
             lib.rnnt_oracle_utterance.restype = i
             lib.rnnt_oracle_batch.argtypes = [P, P, P, P, i, i, i, i, i, i, P, P, i]
             lib.rnnt_oracle_batch.restype = i
+            lib.rnnt_oracle_viterbi.argtypes = [P, i, i, i, i, i, P, i, i, P, P, P]
+            lib.rnnt_oracle_viterbi.restype = i
             lib.rnnt_oracle_max_threads.argtypes = []
             lib.rnnt_oracle_max_threads.restype = i
             _lib = lib
@@ -105,6 +107,25 @@ def batch(z, y, T_b, U_b, blank=0, variant="rnnt", grad=True, nthreads=1):
     lib.rnnt_oracle_batch(_ptr(z), _ptr(y), _ptr(T_b), _ptr(U_b), B, Tmax, Umax, V, int(blank),
                           VARIANTS[variant], _ptr(losses), _ptr(g), int(nthreads))
     return losses, g
+
+
+def viterbi(z, T, U, y, blank=0, variant="rnnt"):
+    """Best alignment of one utterance (max-plus over the same lattice; reading R21 tie-break).
+
+    Returns (best log-score, frames int32 [U] = emission frame of each unit, span (first, last frame)).
+    """
+    lib = _load()
+    z = np.ascontiguousarray(z, dtype=np.float32)
+    Tmax, Up1max, V = z.shape
+    y = np.ascontiguousarray(np.asarray(y, dtype=np.int32).reshape(-1))
+    if y.size == 0:
+        y = np.zeros(1, np.int32)
+    best = np.zeros(1, np.float64)
+    frames = np.full(max(Up1max - 1, 1), -1, np.int32)
+    span = np.full(2, -1, np.int32)
+    lib.rnnt_oracle_viterbi(_ptr(z), Tmax, Up1max - 1, V, int(T), int(U), _ptr(y), int(blank),
+                            VARIANTS[variant], _ptr(best), _ptr(frames), _ptr(span))
+    return float(best[0]), frames[:U].copy(), (int(span[0]), int(span[1]))
 
 
 def max_threads() -> int:

@@ -25,7 +25,8 @@ FINAL = "F"
 
 
 def lattice_arcs(T, U, variant="rnnt"):
-    """Explicit arc list: tuples (src, dst, label) with label ('blank', t, u) | ('label', t, u) | ('skip',)."""
+    """Explicit arc list: tuples (src, dst, label) with label ('blank', t, u) | ('label', t, u) |
+    ('skip', 'initial', t_dst) | ('skip', 'final', t_src)."""
     arcs = []
     for t in range(T):
         for u in range(U + 1):
@@ -36,12 +37,12 @@ def lattice_arcs(T, U, variant="rnnt"):
     arcs.append(((T - 1, U), FINAL, ("blank", T - 1, U)))
     if variant != "rnnt":
         for t in range(1, T):
-            arcs.append(((0, 0), (t, 0), ("skip",)))
+            arcs.append(((0, 0), (t, 0), ("skip", "initial", t)))
         for t in range(0, T - 1):
             if variant == "force_final":
-                arcs.append(((t, U), (T - 1, U), ("skip",)))
+                arcs.append(((t, U), (T - 1, U), ("skip", "final", t)))
             elif variant == "allow_ignore":
-                arcs.append(((t, U), FINAL, ("skip",)))
+                arcs.append(((t, U), FINAL, ("skip", "final", t)))
             else:
                 raise ValueError(variant)
     return arcs
@@ -142,3 +143,34 @@ def loss_and_grad(z, y, T, U, blank=0, variant="rnnt"):
             for j in range(V):
                 g[j] -= r * ((1.0 if j == k else 0.0) - pr[j])
     return -math.log(P), grad, occ_b, occ_y, len(paths)
+
+
+def best_path(z, y, T, U, blank=0, variant="rnnt"):
+    """Viterbi by enumeration: the complete path with the largest sum of arc log-probabilities (float64).
+
+    Returns (best score, frames [U] (emission frame of each unit), span (first, last covered frame),
+    gap to the second-best path score).  The span starts at t0 if the path enters column 0 through the
+    initial skip (0,0)->(t0,0) and ends at t* if it leaves row U through a final skip from (t*,U).
+    """
+    p = softmax_rows(z, T, U)
+    scored = []
+    for path in enumerate_paths(T, U, variant):
+        s = 0.0
+        for lab in path:
+            if lab[0] != "skip":
+                pr = p[lab[1]][lab[2]][_arc_vocab_index(lab, y, blank)]
+                s += math.log(pr) if pr > 0 else -math.inf
+        scored.append((s, path))
+    scored.sort(key=lambda x: -x[0])
+    s0, path = scored[0]
+    gap = s0 - scored[1][0] if len(scored) > 1 else math.inf
+    frames = [-1] * U
+    start, end = 0, T - 1
+    for lab in path:
+        if lab[0] == "label":
+            frames[lab[2]] = lab[1]
+        elif lab[0] == "skip" and lab[1] == "initial":
+            start = lab[2]
+        elif lab[0] == "skip" and lab[1] == "final":
+            end = lab[2]
+    return s0, frames, (start, end), gap

@@ -231,3 +231,149 @@ int rnnt_oracle_max_threads(void) {
     return 1;
 #endif
 }
+
+/*
+ * Viterbi forced alignment over the same lattice (§2.1: the lattice serves "model training
+ * and forced alignment tasks").  Max-plus instead of log-sum-exp:
+ *   delta(0,0) = 0;  delta(t,u) = max over incoming arcs of (delta(src) + w(arc))      (same arc set as above)
+ * Ties are broken in a fixed order (reading R21): blank (time) arc, then label arc, then skip arc;
+ * among final skips the earliest source frame.  Outputs (each may be NULL):
+ *   best        max over complete paths of the summed log-weights
+ *   frames[u]   frame t at which unit u (0-based) is emitted on the best path, u < U
+ *   span[0..1]  first and last frame the best path covers with scored arcs: the frame it enters column 0
+ *               (after an initial skip, else 0) and the frame it leaves row U (before a final skip, else T-1)
+ * Returns 0, or 1 for invalid arguments (best = NaN).  A lattice with no finite path gives best = -inf and
+ * frames / span = -1.
+ */
+enum { BP_BLANK = 0, BP_LABEL = 1, BP_SKIP = 2 };
+
+int rnnt_oracle_viterbi(const float *z, int Tmax, int Umax, int V, int T, int U, const int32_t *y, int blank,
+                        int variant, double *best, int32_t *frames, int32_t *span) {
+    const int64_t Up1max = (int64_t)Umax + 1;
+    int bad = (T < 1 || T > Tmax || U < 0 || U > Umax || V < 2 || blank < 0 || blank >= V ||
+               variant < 0 || variant > 2);
+    for (int u = 0; !bad && u < U; ++u)
+        if (y[u] < 0 || y[u] >= V || y[u] == blank) bad = 1;
+    if (frames)
+        for (int u = 0; u < U && u < Umax; ++u) frames[u] = -1;
+    if (span) span[0] = span[1] = -1;
+    if (bad) {
+        if (best) *best = NAN;
+        return 1;
+    }
+    const int W = (variant != ORACLE_RNNT);
+    const int Up1 = U + 1;
+#define CELL(t, u) ((size_t)(t) * (size_t)Up1 + (size_t)(u))
+#define ZROW(t, u) (z + ((int64_t)(t) * Up1max + (u)) * (int64_t)V)
+    double *lpb = malloc(sizeof(double) * (size_t)T * Up1);
+    double *lpy = malloc(sizeof(double) * (size_t)T * Up1);
+    double *delta = malloc(sizeof(double) * (size_t)T * Up1);
+    unsigned char *bp = malloc((size_t)T * Up1);
+
+    /* log-softmax + Populate, exactly as in rnnt_oracle_utterance */
+    for (int t = 0; t < T; ++t)
+        for (int u = 0; u <= U; ++u) {
+            const float *row = ZROW(t, u);
+            double m = -INFINITY;
+            for (int v = 0; v < V; ++v)
+                if ((double)row[v] > m) m = (double)row[v];
+            double l = -INFINITY;
+            if (m != -INFINITY) {
+                double s = 0.0;
+                for (int v = 0; v < V; ++v) s += exp((double)row[v] - m);
+                l = m + log(s);
+            }
+            lpb[CELL(t, u)] = (l == -INFINITY) ? -INFINITY : (double)row[blank] - l;
+            lpy[CELL(t, u)] = (u < U && l != -INFINITY) ? (double)row[y[u]] - l : -INFINITY;
+        }
+
+    /* max-plus forward pass, t-major; candidate order = tie-break order (strict '>' keeps the first) */
+    for (int t = 0; t < T; ++t)
+        for (int u = 0; u <= U; ++u) {
+            if (t == 0 && u == 0) {
+                delta[CELL(0, 0)] = 0.0;
+                bp[CELL(0, 0)] = BP_BLANK;
+                continue;
+            }
+            double d = -INFINITY;
+            unsigned char from = BP_BLANK;
+            if (t >= 1) {
+                d = delta[CELL(t - 1, u)] + lpb[CELL(t - 1, u)];
+                from = BP_BLANK;
+            }
+            if (u >= 1) {
+                const double c = delta[CELL(t, u - 1)] + lpy[CELL(t, u - 1)];
+                if (c > d || (d == -INFINITY && t < 1)) {
+                    d = c;
+                    from = BP_LABEL;
+                }
+            }
+            if (W && u == 0 && t >= 1) {
+                const double c = delta[CELL(0, 0)] + 0.0; /* initial skip (0,0)->(t,0) */
+                if (c > d) {
+                    d = c;
+                    from = BP_SKIP;
+                }
+            }
+            delta[CELL(t, u)] = d;
+            bp[CELL(t, u)] = from;
+        }
+
+    /* final arcs: terminating blank from (T-1,U); force-final skips into (T-1,U); allow-ignore skips to F */
+    int end_t = T - 1, final_skip_from = -1;
+    double score;
+    {
+        double dm = -INFINITY;
+        int tm = -1;
+        if (W)
+            for (int tp = 0; tp <= T - 2; ++tp)
+                if (delta[CELL(tp, U)] > dm) {
+                    dm = delta[CELL(tp, U)];
+                    tm = tp;
+                }
+        if (variant == ORACLE_W_FORCE_FINAL) {
+            double into = delta[CELL(T - 1, U)];
+            if (dm > into) { /* force-final skip (t*,U)->(T-1,U) */
+                into = dm;
+                final_skip_from = tm;
+            }
+            score = into + lpb[CELL(T - 1, U)];
+        } else if (variant == ORACLE_W_ALLOW_IGNORE) {
+            score = delta[CELL(T - 1, U)] + lpb[CELL(T - 1, U)];
+            if (dm > score) { /* allow-ignore skip (t*,U)->F */
+                score = dm;
+                final_skip_from = tm;
+            }
+        } else {
+            score = delta[CELL(T - 1, U)] + lpb[CELL(T - 1, U)];
+        }
+        if (final_skip_from >= 0) end_t = final_skip_from;
+    }
+    if (best) *best = score;
+    if (score == -INFINITY) {
+        free(lpb); free(lpy); free(delta); free(bp);
+        return 0;
+    }
+    /* back-trace */
+    int t = end_t, u = U, start_t = 0;
+    while (!(t == 0 && u == 0)) {
+        const unsigned char f = bp[CELL(t, u)];
+        if (f == BP_BLANK) {
+            t -= 1;
+        } else if (f == BP_LABEL) {
+            if (frames) frames[u - 1] = t;
+            u -= 1;
+        } else { /* initial skip into (t,0) */
+            start_t = t;
+            t = 0;
+        }
+    }
+    if (span) {
+        span[0] = start_t;
+        span[1] = end_t;
+    }
+    free(lpb); free(lpy); free(delta); free(bp);
+#undef CELL
+#undef ZROW
+    return 0;
+}

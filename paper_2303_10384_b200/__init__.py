@@ -21,7 +21,8 @@ RNNT_OK = 0
 VARIANTS = {"rnnt": -1, "force_final": 0, "allow_ignore": 1}
 
 # Every symbol include/rnnt_b200.h declares.
-EXPORTS = ("rnnt_workspace_bytes", "rnnt_loss", "wrnnt_loss", "rnnt_loss_timed", "rnnt_loss_ex", "rnnt_loss_sum",
+EXPORTS = ("rnnt_workspace_bytes", "rnnt_loss", "wrnnt_loss", "rnnt_loss_timed", "rnnt_loss_ex", "rnnt_viterbi",
+           "rnnt_loss_sum",
            "rnnt_host_buffer_bytes", "rnnt_loss_host", "rnnt_status_string", "rnnt_version")
 DTYPES = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2}
 
@@ -47,6 +48,8 @@ def _load():
     lib.rnnt_loss_timed.restype = I
     lib.rnnt_loss_ex.argtypes = [P, I, P, P, P, I, I, I, I, I, I, P, P, P, P, S, P, P]
     lib.rnnt_loss_ex.restype = I
+    lib.rnnt_viterbi.argtypes = [P, I, P, P, P, I, I, I, I, I, I, P, P, P, P, S, P]
+    lib.rnnt_viterbi.restype = I
     lib.rnnt_loss_sum.argtypes = [P, I, P, P]
     lib.rnnt_loss_sum.restype = I
     lib.rnnt_host_buffer_bytes.argtypes = [I, I, I, I]
@@ -170,6 +173,29 @@ def rnnt_loss_timed(logits, targets, logit_lens, target_lens, blank=0, variant="
     (see include/rnnt_b200.h; the events must be recorded once beforehand so that their handles exist)."""
     return _call(VARIANTS[variant], logits, targets, logit_lens, target_lens, blank, grads, grad_scale, losses,
                  workspace, stream, events)
+
+
+def rnnt_viterbi(logits, targets, logit_lens, target_lens, blank=0, variant="rnnt", workspace=None, stream=None):
+    """Viterbi forced alignment (best path, ties blank > label > skip).  Returns (best_logp fp32 [B],
+    frames int32 [B, Umax] (emission frame of each unit, -1 past U_b), span int32 [B, 2])."""
+    if not (isinstance(logits, torch.Tensor) and logits.is_cuda and logits.dtype in DTYPES):
+        raise TypeError("logits must be a CUDA float32 / float16 / bfloat16 tensor (no CPU fallback)")
+    B, Tmax, Up1, V = logits.shape
+    Umax = Up1 - 1
+    dev = logits.device
+    targets = _as_i32(targets, dev).reshape(B, Umax) if Umax > 0 else None
+    logit_lens = _as_i32(logit_lens, dev)
+    target_lens = _as_i32(target_lens, dev)
+    best = torch.empty(B, dtype=torch.float32, device=dev)
+    frames = torch.empty((B, Umax), dtype=torch.int32, device=dev)
+    span = torch.empty((B, 2), dtype=torch.int32, device=dev)
+    if workspace is None:
+        workspace = torch.empty(max(rnnt_workspace_bytes(B, Tmax, Umax), 1), dtype=torch.uint8, device=dev)
+    _check(library.rnnt_viterbi(_ptr(logits.contiguous()), DTYPES[logits.dtype], _ptr(targets), _ptr(logit_lens),
+                                _ptr(target_lens), B, Tmax, Umax, V, int(blank), VARIANTS[variant], _ptr(best),
+                                _ptr(frames) if Umax > 0 else None, _ptr(span), _ptr(workspace), workspace.numel(),
+                                _stream(stream)))
+    return best, frames, span
 
 
 def rnnt_loss_sum(losses, out=None, stream=None):

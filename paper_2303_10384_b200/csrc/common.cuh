@@ -224,5 +224,7 @@ int lanes_per_row(int nvec);  // K1 / K3 row-group width for a row of nvec 128-b
 cudaError_t launch_k2_alpha_beta(const Problem& p, const Workspace& w, cudaStream_t s);
 cudaError_t launch_k3_grad(const Problem& p, const Workspace& w, cudaStream_t s);
 cudaError_t launch_loss_sum(const float* losses, int B, double* out, cudaStream_t s);
+cudaError_t launch_k4_viterbi(const Problem& p, const Workspace& w, float* best, int32_t* frames, int32_t* span,
+                              cudaStream_t s);
 
 }  // namespace rnnt

@@ -221,6 +221,27 @@ rnnt_status rnnt_loss_ex(const void* logits, rnnt_dtype dtype, const int32_t* ta
                grads, grad_scale, workspace, workspace_bytes, stream, variant_kind(variant), events);
 }
 
+rnnt_status rnnt_viterbi(const void* logits, rnnt_dtype dtype, const int32_t* targets, const int32_t* logit_lens,
+                         const int32_t* target_lens, int B, int Tmax, int Umax, int V, int blank, int variant,
+                         float* best_logp, int32_t* frames, int32_t* span, void* workspace, size_t workspace_bytes,
+                         void* stream) {
+    rnnt_status st = check_sizes(B, Tmax, Umax, V, blank);
+    if (st != RNNT_OK) return st;
+    if (variant < -1 || variant > 1) return RNNT_ERR_INVALID_ARG;
+    if (dtype != RNNT_F32 && dtype != RNNT_F16 && dtype != RNNT_BF16) return RNNT_ERR_INVALID_ARG;
+    if (B == 0) return RNNT_OK;
+    if (!logits || !logit_lens || !target_lens || !best_logp || !workspace) return RNNT_ERR_INVALID_ARG;
+    if (Umax > 0 && (!targets || !frames)) return RNNT_ERR_INVALID_ARG;
+    if (workspace_bytes < rnnt::workspace_bytes(B, Tmax, Umax)) return RNNT_ERR_WORKSPACE_TOO_SMALL;
+    Problem p{logits, targets, logit_lens, target_lens, B, Tmax, Umax, V, blank, variant_kind(variant), nullptr,
+              nullptr, nullptr, static_cast<int>(dtype)};
+    const Workspace w = rnnt::carve(workspace, B, Tmax, Umax);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (rnnt::launch_k1_lse_gather(p, w, s) != cudaSuccess) return RNNT_ERR_CUDA;
+    if (rnnt::launch_k4_viterbi(p, w, best_logp, frames, span, s) != cudaSuccess) return RNNT_ERR_CUDA;
+    return RNNT_OK;
+}
+
 rnnt_status rnnt_loss_sum(const float* losses, int B, double* loss_sum, void* stream) {
     if (B < 0 || !loss_sum || (B > 0 && !losses)) return RNNT_ERR_INVALID_ARG;
     if (rnnt::launch_loss_sum(losses, B, loss_sum, static_cast<cudaStream_t>(stream)) != cudaSuccess)

@@ -279,3 +279,49 @@ def test_padding_is_never_read():
         l1, g1 = oracle.batch(z, y, T_b, U_b, 0, variant)
         l2, g2 = oracle.batch(zn, y, T_b, U_b, 0, variant, nthreads=2)
         assert np.array_equal(l1, l2) and np.array_equal(g1, g2)
+
+
+# ------------------------------------------------------------------------------------------- Viterbi
+def test_viterbi_matches_enumeration():
+    """Max-plus DP + back-trace == the best of all enumerated paths (score, emission frames, span), on random
+    instances whose best path is unique (gap > 1e-9), all variants (NEXT-2; "forced alignment")."""
+    rng = np.random.default_rng(31)
+    n = 0
+    for it in range(200):
+        T, U, V = int(rng.integers(1, 6)), int(rng.integers(0, 4)), int(rng.integers(2, 6))
+        z, y, blank = _rand_instance(rng, T, U, V, scale=2.0)
+        for variant in VARIANTS:
+            s, f, sp = oracle.viterbi(z, T, U, y, blank, variant)
+            s2, f2, sp2, gap = brute.best_path(z, y, T, U, blank, variant)
+            if gap < 1e-9:
+                continue
+            n += 1
+            assert abs(s - s2) <= 1e-12 * max(1.0, abs(s2))
+            assert list(f) == f2 and tuple(sp) == sp2
+    assert n > 300
+
+
+def test_viterbi_bounds_closed_forms_and_ties():
+    """best <= log P (a max is below the log-sum-exp) and best >= log P - log(#paths); single-path lattices
+    give the path's score; all-equal logits (every path ties) resolve by the blank-first rule to emitting
+    every unit at frame 0 (reading R21)."""
+    rng = np.random.default_rng(32)
+    for _ in range(40):
+        T, U, V = int(rng.integers(1, 7)), int(rng.integers(0, 5)), int(rng.integers(2, 7))
+        z, y, blank = _rand_instance(rng, T, U, V, scale=2.0)
+        for variant in VARIANTS:
+            s, _, _ = oracle.viterbi(z, T, U, y, blank, variant)
+            logP = -oracle.utterance(z, T, U, y, blank, variant, grad=False)["loss"]
+            npaths = len(brute.enumerate_paths(T, U, variant))
+            assert s <= logP + 1e-12 and s >= logP - math.log(npaths) - 1e-12
+    z, _, blank = _rand_instance(rng, 5, 0, 4, scale=2.0)
+    s, _, sp = oracle.viterbi(z, 5, 0, [], blank, "rnnt")
+    assert abs(s - sum(_log_softmax(z[t, 0])[blank] for t in range(5))) < 1e-12 and sp == (0, 4)
+    z, y, blank = _rand_instance(rng, 1, 3, 6, scale=2.0)
+    s, f, _ = oracle.viterbi(z, 1, 3, y, blank, "force_final")
+    assert list(f) == [0, 0, 0]
+    assert abs(s - (sum(_log_softmax(z[0, u])[y[u]] for u in range(3)) + _log_softmax(z[0, 3])[blank])) < 1e-12
+    for T, U in ((4, 2), (6, 3), (3, 1)):
+        s, f, sp = oracle.viterbi(np.zeros((T, U + 1, 5), np.float32), T, U, list(range(1, U + 1)), 0, "rnnt")
+        assert list(f) == [0] * U and sp == (0, T - 1)
+        assert abs(s - (T + U) * math.log(1 / 5)) < 1e-12
