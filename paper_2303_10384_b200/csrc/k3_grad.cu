@@ -58,6 +58,19 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32)
         return;
     }
 
+    constexpr int kU = kPerLane / E;
+    const uint64_t pol = l2_evict_first();
+    const uint4* z4 = reinterpret_cast<const uint4*>(zrow);
+    const int nvec = V / E;
+    uint4 raw[kU];
+    if constexpr (kVec) {  // issue the row's first chunk before the per-row scalars: both latencies overlap
+#pragma unroll
+        for (int j = 0; j < kU; ++j) {
+            const int i = j * 32 + lane;
+            if (i < nvec) raw[j] = ldv(z4 + i, pol);
+        }
+    }
+
     // Per-row scalars: occupancies of the two scored arcs leaving (t,u).
     const int64_t dcell = (static_cast<int64_t>(b) * (Tmax + Umax) + (t + u)) * Up1 + u;  // diagonal t+u, slot u
     const float lse = lse_in[row];
@@ -79,20 +92,17 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32)
     const float lsel = (lse == -INFINITY) ? INFINITY : lse * kLog2e;  // all -inf row -> p = 0
 
     if constexpr (kVec) {
-        constexpr int kU = kPerLane / E;
-        const uint64_t pol = l2_evict_first();
-        const uint4* z4 = reinterpret_cast<const uint4*>(zrow);
         uint4* g4 = reinterpret_cast<uint4*>(grow);
-        const int nvec = V / E;
         const int bq = blank / E, yq = (yv < 0) ? -1 : (yv / E);
         const int bk = blank % E, yk = (yv < 0) ? 0 : (yv % E);
         const f32x2 l2e = pk(kLog2e, kLog2e), nl = pk(-lsel, -lsel), g2 = pk(gam, gam);
         for (int base = 0; base < nvec; base += 32 * kU) {
-            uint4 raw[kU];
+            if (base > 0) {
 #pragma unroll
-            for (int j = 0; j < kU; ++j) {
-                const int i = base + j * 32 + lane;
-                if (i < nvec) raw[j] = ldv(z4 + i, pol);
+                for (int j = 0; j < kU; ++j) {
+                    const int i = base + j * 32 + lane;
+                    if (i < nvec) raw[j] = ldv(z4 + i, pol);
+                }
             }
 #pragma unroll
             for (int j = 0; j < kU; ++j) {
@@ -176,6 +186,13 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32)
         return;
     }
 
+    uint4 raw[kU];
+#pragma unroll
+    for (int j = 0; j < kU; ++j) {  // the row's first chunk, issued before the per-row scalars
+        const int i = j * G + sl;
+        if (i < nvec) raw[j] = ldv(z4 + i, pol);
+    }
+
     // Per-row scalars: occupancies of the two scored arcs leaving (t,u).
     const int64_t dcell = (static_cast<int64_t>(b) * (Tmax + Umax) + (t + u)) * Up1 + u;  // diagonal t+u, slot u
     const float lse = lse_in[row];
@@ -200,11 +217,12 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32)
     const int bk = blank % E, yk = (yv < 0) ? 0 : (yv % E);
     const f32x2 l2e = pk(kLog2e, kLog2e), nl = pk(-lsel, -lsel), g2 = pk(gam, gam);
     for (int base = 0; base < nvec; base += G * kU) {
-        uint4 raw[kU];
+        if (base > 0) {
 #pragma unroll
-        for (int j = 0; j < kU; ++j) {
-            const int i = base + j * G + sl;
-            if (i < nvec) raw[j] = ldv(z4 + i, pol);
+            for (int j = 0; j < kU; ++j) {
+                const int i = base + j * G + sl;
+                if (i < nvec) raw[j] = ldv(z4 + i, pol);
+            }
         }
 #pragma unroll
         for (int j = 0; j < kU; ++j) {
