@@ -51,9 +51,10 @@ def parse():
     ap.add_argument("--dtype", default="f32", choices=["f32", "bf16", "f16"],
                     help="storage type of logits/grads (arithmetic is fp32/fp64 either way); the BASELINE "
                          "metric is quoted on f32")
-    ap.add_argument("--mode", default="loss_grad", choices=["loss_grad", "loss", "viterbi"],
+    ap.add_argument("--mode", default="loss_grad", choices=["loss_grad", "loss", "viterbi", "lattice"],
                     help="loss_grad: the BASELINE metric; loss: losses only (K1+K2); viterbi: forced alignment "
-                         "(K1+K4) -- SURVEY 8(f) NEXT-2")
+                         "(K1+K4) -- SURVEY 8(f) NEXT-2; lattice: the same loss+grad through the generic "
+                         "acyclic-lattice engine on explicit Grid/W lattices -- NEXT-3")
     ap.add_argument("--inplace", action="store_true",
                     help="write grads over the logits (automatic when two copies do not fit in HBM, e.g. c5)")
     return ap.parse_args()
@@ -164,6 +165,8 @@ def launches_per_step(mode, B, cfg):
     elements, see rnnt_api.cu overlap_chunks) + the loss sum; viterbi = K1 + K4."""
     if mode == "viterbi":
         return 2
+    if mode == "lattice":
+        return 6 + 1  # K1, L2, L3, L4, L5, L6 + loss sum (plus one memset)
     elems = B * cfg.Tmax * (cfg.Umax + 1) * cfg.V
     nch = min(B, 4) if (B >= 2 and elems >= (1 << 24)) else 1
     return nch * (3 if mode == "loss_grad" else 2) + 1
@@ -269,7 +272,18 @@ def main():
             e.record()  # create the CUDA handles
     torch.cuda.synchronize()
 
+    dlat = None
+    if args.mode == "lattice":
+        from paper_2303_10384_b200 import lattice as rlat
+        dlat = rb.lattice_to_device(rlat.grid_lattices(pb["logit_lens"], pb["target_lens"], pb["targets"],
+                                                       gcfg.blank, variant), dev)
+
     def step(events=None):
+        if args.mode == "lattice":
+            rb.rnnt_lattice_loss(z, dlat, T_b, U_b, grads=grads, losses=losses)
+            rb.rnnt_loss_sum(losses, out=loss_sum)
+            rdist.allreduce_loss_sum(loss_sum)
+            return
         if args.mode == "viterbi":
             rb.rnnt_viterbi(z, targets, T_b, U_b, gcfg.blank, variant, workspace=workspace)
             return
@@ -312,8 +326,8 @@ def main():
     peak, peak_src = measured_peaks()
     if args.mode != "loss_grad":  # no K3 (and, for viterbi, no per-kernel events): report K1 / the step
         k_ms["k3_grad"] = 0.0
-        if args.mode == "viterbi":
-            k_ms = {"step(k1_lse_gather+k4_viterbi)": ms_step}
+        if args.mode in ("viterbi", "lattice"):
+            k_ms = {f"step({args.mode})": ms_step}
     k3_gbs = k3_bytes / (k_ms["k3_grad"] / 1e3) / 1e9 if k_ms.get("k3_grad") else None
     k1_ms = k_ms.get("k1_lse_gather", ms_step)
     k1_gbs = k1_bytes / (k1_ms / 1e3) / 1e9
@@ -323,10 +337,12 @@ def main():
                 "frac": k3_gbs / peak, "traffic": ncu_traffic("k3_grad", args.config),
                 "algorithmic_bytes_per_launch": k3_bytes, "peak_source": peak_src}
     else:
-        roof = {"bound": "hbm", "kernel": "k1_lse_gather" if args.mode == "loss" else "step (k1 + k4)",
-                "achieved": k1_gbs, "peak": peak, "unit": "GB/s", "frac": k1_gbs / peak,
+        nbytes = k1_bytes + (k3_bytes if args.mode == "lattice" else 0)  # lattice: the whole loss+grad step
+        gbs = nbytes / ((k1_ms if args.mode == "loss" else ms_step) / 1e3) / 1e9
+        roof = {"bound": "hbm", "kernel": "k1_lse_gather" if args.mode == "loss" else f"step ({args.mode})",
+                "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
                 "traffic": ncu_traffic("k1_lse_gather", args.config) if args.mode == "loss" else None,
-                "algorithmic_bytes_per_launch": k1_bytes, "peak_source": peak_src}
+                "algorithmic_bytes_per_launch": nbytes, "peak_source": peak_src}
 
     # sanity: finite losses and the all-reduced sum
     loss_total = float(loss_sum.item())

@@ -125,6 +125,31 @@ rnnt_status rnnt_viterbi(const void* logits, rnnt_dtype dtype, const int32_t* ta
                          int V, int blank, int variant, float* best_logp, int32_t* frames, int32_t* span,
                          void* workspace, size_t workspace_bytes, void* stream);
 
+/* Generic acyclic-lattice loss (§1, §2.2 Eq.(3): new losses are new
+ * graphs populated from the log-probabilities tensor, not new kernels).  A batch of B lattices in arc-list
+ * form (all int32 device arrays; builders in paper_2303_10384_b200/lattice.py):
+ *   state_off [B+1]  states of lattice b: [state_off[b], state_off[b+1]); its first state is the start
+ *   lvl_off   [B+1]  levels of lattice b: [lvl_off[b], lvl_off[b+1]) into level_off
+ *   level_off [L+1]  states of level k: [level_off[k], level_off[k+1]); every arc goes to a higher level
+ *   in_off    [S+1]  arcs are sorted by destination: the arcs into s are [in_off[s], in_off[s+1])
+ *   out_off   [S+1], out_arc [A]: out_arc[out_off[s] .. out_off[s+1]) are the arcs leaving s
+ *   arc_src / arc_dst [A] (global state ids), arc_t / arc_u / arc_v [A]: arc weight X[b, t, u, v] =
+ *                    logits[b,t,u,v] - logsumexp_v logits[b,t,u,:], or 0 when arc_v < 0 (structural arc)
+ *   final_w   [S]    fp32 log final weight (-inf: not final)
+ * Rows (t,u) with t < logit_lens[b], u <= target_lens[b] are live; every arc must bind a live row.
+ * losses[b] = -log sum over start->final paths of exp(sum of arc weights + final weight) (Eq.(1)); grads
+ * (fp32, may equal logits, or NULL) = d losses[b] / d logits, zero on non-live rows.  fp32 only; float
+ * atomics make grads order-dependent where > 2 arcs share a row or > 1 arc shares a (t,u,v). */
+size_t rnnt_lattice_workspace_bytes(int B, int Tmax, int Umax, int num_states, int num_arcs);
+rnnt_status rnnt_lattice_loss(const float* logits, const int32_t* logit_lens, const int32_t* target_lens,
+                              int B, int Tmax, int Umax, int V, const int32_t* state_off,
+                              const int32_t* lvl_off, const int32_t* level_off, const int32_t* in_off,
+                              const int32_t* out_off, const int32_t* out_arc, const int32_t* arc_src,
+                              const int32_t* arc_dst, const int32_t* arc_t, const int32_t* arc_u,
+                              const int32_t* arc_v, const float* final_w, int num_states, int num_arcs,
+                              float* losses, float* grads, void* workspace, size_t workspace_bytes,
+                              void* stream);
+
 /* Deterministic fp64 sum of losses[0..B) into *loss_sum (device), fixed summation order for a given B.
  * This is the per-rank operand of the cross-GPU all-reduce of the loss sum (BASELINE.json north_star (5)). */
 rnnt_status rnnt_loss_sum(const float* losses, int B, double* loss_sum, void* stream);

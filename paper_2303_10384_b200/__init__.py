@@ -22,7 +22,7 @@ VARIANTS = {"rnnt": -1, "force_final": 0, "allow_ignore": 1}
 
 # Every symbol include/rnnt_b200.h declares.
 EXPORTS = ("rnnt_workspace_bytes", "rnnt_loss", "wrnnt_loss", "rnnt_loss_timed", "rnnt_loss_ex", "rnnt_viterbi",
-           "rnnt_loss_sum",
+           "rnnt_loss_sum", "rnnt_lattice_workspace_bytes", "rnnt_lattice_loss",
            "rnnt_host_buffer_bytes", "rnnt_loss_host", "rnnt_status_string", "rnnt_version")
 DTYPES = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2}
 
@@ -37,29 +37,26 @@ def _load():
                           f"g.build()'` (nvcc, sm_100a). There is no CPU fallback.")
     lib = ctypes.CDLL(LIB_PATH)
     P, I, S = ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t
-    lib.rnnt_workspace_bytes.argtypes = [I, I, I]
-    lib.rnnt_workspace_bytes.restype = S
     common = [P, P, P, P, I, I, I, I, I, P, P, P, P, S, P]
-    lib.rnnt_loss.argtypes = common
-    lib.rnnt_loss.restype = I
-    lib.wrnnt_loss.argtypes = common + [I]
-    lib.wrnnt_loss.restype = I
-    lib.rnnt_loss_timed.argtypes = common + [I, P]
-    lib.rnnt_loss_timed.restype = I
-    lib.rnnt_loss_ex.argtypes = [P, I, P, P, P, I, I, I, I, I, I, P, P, P, P, S, P, P]
-    lib.rnnt_loss_ex.restype = I
-    lib.rnnt_viterbi.argtypes = [P, I, P, P, P, I, I, I, I, I, I, P, P, P, P, S, P]
-    lib.rnnt_viterbi.restype = I
-    lib.rnnt_loss_sum.argtypes = [P, I, P, P]
-    lib.rnnt_loss_sum.restype = I
-    lib.rnnt_host_buffer_bytes.argtypes = [I, I, I, I]
-    lib.rnnt_host_buffer_bytes.restype = S
-    lib.rnnt_loss_host.argtypes = [P, P, P, P, I, I, I, I, I, I, P, P, P, S, P]
-    lib.rnnt_loss_host.restype = I
-    lib.rnnt_status_string.argtypes = [I]
-    lib.rnnt_status_string.restype = ctypes.c_char_p
-    lib.rnnt_version.argtypes = []
-    lib.rnnt_version.restype = ctypes.c_char_p
+    sigs = {
+        "rnnt_workspace_bytes": ([I, I, I], S),
+        "rnnt_loss": (common, I),
+        "wrnnt_loss": (common + [I], I),
+        "rnnt_loss_timed": (common + [I, P], I),
+        "rnnt_loss_ex": ([P, I, P, P, P, I, I, I, I, I, I, P, P, P, P, S, P, P], I),
+        "rnnt_viterbi": ([P, I, P, P, P, I, I, I, I, I, I, P, P, P, P, S, P], I),
+        "rnnt_lattice_workspace_bytes": ([I, I, I, I, I], S),
+        "rnnt_lattice_loss": ([P, P, P, I, I, I, I] + [P] * 12 + [I, I, P, P, P, S, P], I),
+        "rnnt_loss_sum": ([P, I, P, P], I),
+        "rnnt_host_buffer_bytes": ([I, I, I, I], S),
+        "rnnt_loss_host": ([P, P, P, P, I, I, I, I, I, I, P, P, P, S, P], I),
+        "rnnt_status_string": ([I], ctypes.c_char_p),
+        "rnnt_version": ([], ctypes.c_char_p),
+    }
+    for name, (argtypes, restype) in sigs.items():
+        if hasattr(lib, name):  # every symbol is checked present by build() and tests/test_abi.py; an older
+            fn = getattr(lib, name)  # library loaded through RNNT_B200_LIB for A/B timing may lack new ones
+            fn.argtypes, fn.restype = argtypes, restype
     return lib
 
 
@@ -191,11 +188,50 @@ def rnnt_viterbi(logits, targets, logit_lens, target_lens, blank=0, variant="rnn
     span = torch.empty((B, 2), dtype=torch.int32, device=dev)
     if workspace is None:
         workspace = torch.empty(max(rnnt_workspace_bytes(B, Tmax, Umax), 1), dtype=torch.uint8, device=dev)
-    _check(library.rnnt_viterbi(_ptr(logits.contiguous()), DTYPES[logits.dtype], _ptr(targets), _ptr(logit_lens),
+    logits = logits.contiguous()  # a named reference keeps any copy alive across the call
+    _check(library.rnnt_viterbi(_ptr(logits), DTYPES[logits.dtype], _ptr(targets), _ptr(logit_lens),
                                 _ptr(target_lens), B, Tmax, Umax, V, int(blank), VARIANTS[variant], _ptr(best),
                                 _ptr(frames) if Umax > 0 else None, _ptr(span), _ptr(workspace), workspace.numel(),
                                 _stream(stream)))
     return best, frames, span
+
+
+def rnnt_lattice_loss(logits, lattices, logit_lens, target_lens, grads=True, losses=None, stream=None):
+    """Generic acyclic-lattice loss + logits-gradient (NEXT-3).  ``lattices``: a lattice.LatticeBatch (host
+    numpy arrays, copied to the device here) or the dict ``lattice_to_device`` returns.  fp32 logits.
+    Returns (losses [B], grads or None)."""
+    if not (isinstance(logits, torch.Tensor) and logits.is_cuda and logits.dtype == torch.float32):
+        raise TypeError("logits must be a CUDA float32 tensor (no CPU fallback)")
+    B, Tmax, Up1, V = logits.shape
+    dev = logits.device
+    dv = lattices if isinstance(lattices, dict) else lattice_to_device(lattices, dev)
+    if losses is None:
+        losses = torch.empty(B, dtype=torch.float32, device=dev)
+    if isinstance(grads, str) and grads == "inplace":
+        grads = logits
+    elif grads is True:
+        grads = torch.empty_like(logits)
+    elif grads is False:
+        grads = None
+    need = int(library.rnnt_lattice_workspace_bytes(B, Tmax, Up1 - 1, dv["num_states"], dv["num_arcs"]))
+    ws = torch.empty(max(need, 1), dtype=torch.uint8, device=dev)
+    logit_lens = _as_i32(logit_lens, dev)    # keep the device copies alive across the call
+    target_lens = _as_i32(target_lens, dev)
+    _check(library.rnnt_lattice_loss(
+        _ptr(logits), _ptr(logit_lens), _ptr(target_lens), B, Tmax, Up1 - 1, V,
+        *[_ptr(dv[k]) for k in ("state_off", "lvl_off", "level_off", "in_off", "out_off", "out_arc", "arc_src",
+                                "arc_dst", "arc_t", "arc_u", "arc_v", "final_w")],
+        dv["num_states"], dv["num_arcs"], _ptr(losses), _ptr(grads), _ptr(ws), ws.numel(), _stream(stream)))
+    return losses, grads
+
+
+def lattice_to_device(L, device="cuda"):
+    """Upload a lattice.LatticeBatch once (the dict rnnt_lattice_loss accepts)."""
+    dv = {k: torch.from_numpy(getattr(L, k)).to(device) for k in (
+        "state_off", "lvl_off", "level_off", "in_off", "out_off", "out_arc", "arc_src", "arc_dst", "arc_t", "arc_u",
+        "arc_v", "final_w")}
+    dv["num_states"], dv["num_arcs"] = L.num_states, L.num_arcs
+    return dv
 
 
 def rnnt_loss_sum(losses, out=None, stream=None):

@@ -219,6 +219,7 @@ struct Problem {
     int dtype;
 };
 
+// K1; with w.lp == nullptr (and p.targets == nullptr) it writes the normalizer lse only (generic lattices).
 cudaError_t launch_k1_lse_gather(const Problem& p, const Workspace& w, cudaStream_t s);
 int lanes_per_row(int nvec);  // K1 / K3 row-group width for a row of nvec 128-bit vectors
 cudaError_t launch_k2_alpha_beta(const Problem& p, const Workspace& w, cudaStream_t s);

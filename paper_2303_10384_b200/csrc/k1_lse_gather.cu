@@ -58,8 +58,8 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32, 4)
     }
 
     int yv = -1;
-    if (u < U) yv = targets[static_cast<int64_t>(b) * Umax + u];
-    const bool ybad = (u < U) && (yv < 0 || yv >= V || yv == blank);
+    if (u < U && targets) yv = targets[static_cast<int64_t>(b) * Umax + u];
+    const bool ybad = targets && (u < U) && (yv < 0 || yv >= V || yv == blank);
     if (ybad) yv = -1;
     // Populate gather: lanes 0 / 1 fetch z[blank] / z[y] with scalar loads issued alongside the row's
     // loads (same sectors, merged in L2: no extra DRAM traffic, no register indexing).
@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32, 4)
             xy = (u < U) ? (ybad ? __int_as_float(0x7fc00000) : zy - lse) : -INFINITY;
         }
         const int64_t diag = static_cast<int64_t>(b) * (Tmax + Umax) + (t + u);
-        lp_out[diag * Up1 + u] = make_double2(xb, xy);
+        if (lp_out) lp_out[diag * Up1 + u] = make_double2(xb, xy);
     }
 }
 
@@ -171,8 +171,8 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32)
     if (__all_sync(0xffffffffu, !live)) return;
 
     int yv = -1;
-    if (live && u < U) yv = targets[static_cast<int64_t>(b) * Umax + u];
-    const bool ybad = (u < U) && (yv < 0 || yv >= V || yv == blank);
+    if (live && u < U && targets) yv = targets[static_cast<int64_t>(b) * Umax + u];
+    const bool ybad = targets && (u < U) && (yv < 0 || yv >= V || yv == blank);
     if (ybad) yv = -1;
 
     const int64_t row = static_cast<int64_t>(b) * Tmax * Up1 + r;
@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32)
             xy = (u < U) ? (ybad ? __int_as_float(0x7fc00000) : zy - lse) : -INFINITY;
         }
         const int64_t diag = static_cast<int64_t>(b) * (Tmax + Umax) + (t + u);
-        lp_out[diag * Up1 + u] = make_double2(xb, xy);
+        if (lp_out) lp_out[diag * Up1 + u] = make_double2(xb, xy);
     }
 }
 
