@@ -1,0 +1,27 @@
+"""Small cases for compute-sanitizer: every entry point, all variants, fp32/bf16, scalar + vector paths."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+import paper_2303_10384_b200 as rb
+from paper_2303_10384_b200 import lattice as rlat
+import workloads
+
+for shape in [(3, 9, 4, 8, 0), (2, 33, 40, 130, 129), (2, 20, 70, 256, 3), (2, 12, 5, 1024, 7)]:
+    B, T, U, V, blank = shape
+    for variant in ("rnnt", "force_final", "allow_ignore"):
+        cfg = workloads.random_config(B, T, U, V, seed=sum(shape), blank=blank, variant=variant)
+        pb = workloads.problem(cfg)
+        z = pb["logits"].cuda()
+        rb.loss(z, pb["targets"], pb["logit_lens"], pb["target_lens"], blank, variant)
+        rb.loss(z.to(torch.bfloat16), pb["targets"], pb["logit_lens"], pb["target_lens"], blank, variant,
+                grads="inplace")
+        rb.rnnt_viterbi(z, pb["targets"], pb["logit_lens"], pb["target_lens"], blank, variant)
+        L = rlat.grid_lattices(pb["logit_lens"], pb["target_lens"], pb["targets"], blank, variant)
+        rb.rnnt_lattice_loss(z, L, pb["logit_lens"], pb["target_lens"])
+# the chunked / overlapped path (>= 2^24 elements)
+cfg = workloads.random_config(4, 120, 40, 1024, seed=15, variable=True)
+pb = workloads.problem(cfg)
+rb.rnnt_loss(pb["logits"].cuda(), pb["targets"], pb["logit_lens"], pb["target_lens"], 0)
+torch.cuda.synchronize()
+print("sanitize cases done")
