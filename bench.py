@@ -375,7 +375,7 @@ def main():
     e2e = None
     if not args.no_e2e and args.dtype != "f32":
         e2e = {"value": None, "unit": UNIT, "reason": "the host-buffer entry point takes fp32 only"}
-    elif not args.no_e2e and 2.2 * z.numel() * 4 > host_avail_bytes():
+    elif not args.no_e2e and 2.2 * z.numel() * 4 * int(os.environ.get("LOCAL_WORLD_SIZE", world)) > host_avail_bytes():
         e2e = {"value": None, "unit": UNIT, "reason": "pinned host copies of logits + grads exceed host RAM"}
     elif not args.no_e2e:
         zh = z.cpu().pin_memory()
