@@ -55,6 +55,9 @@ def parse():
                     help="loss_grad: the BASELINE metric; loss: losses only (K1+K2); viterbi: forced alignment "
                          "(K1+K4) -- SURVEY 8(f) NEXT-2; lattice: the same loss+grad through the generic "
                          "acyclic-lattice engine on explicit Grid/W lattices -- NEXT-3")
+    ap.add_argument("--eager", action="store_true",
+                    help="launch the K timed steps one by one from Python instead of replaying them as one CUDA graph "
+                         "(the default at N=1 for --mode loss_grad / loss: no host launch overhead between kernels)")
     ap.add_argument("--inplace", action="store_true",
                     help="write grads over the logits (automatic when two copies do not fit in HBM, e.g. c5)")
     return ap.parse_args()
@@ -299,12 +302,37 @@ def main():
         torch.distributed.barrier()
     torch.cuda.synchronize()
 
+    graph = graph_ev = None
+    if not args.eager and world == 1 and args.mode in ("loss_grad", "loss"):
+        # All K timed steps captured as one CUDA graph (replayed once below): every kernel of every step runs,
+        # only the host launch overhead goes.  The C-ABI call forks its K2 chunks onto internal streams and
+        # joins them back, so it is capturable (its internal streams were created by the warm-up calls).
+        # Timing events inside a graph become external event nodes, which cost a few microseconds each, so
+        # the per-kernel split comes from a second graph of the same K steps with the events, replayed right
+        # after the timed one.
+        graph, graph_ev = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            for i in range(K):
+                step(None)
+        with torch.cuda.graph(graph_ev):
+            for i in range(K):
+                step(evs[i])
+        graph.replay()  # one untimed replay each: a graph's first launch uploads it
+        graph_ev.replay()
+        torch.cuda.synchronize()
+
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
         start.record()
-        for i in range(K):
-            step(evs[i])
+        if graph is not None:
+            graph.replay()
+        else:
+            for i in range(K):
+                step(evs[i])
         end.record()
+        torch.cuda.synchronize()
+    if graph_ev is not None:
+        graph_ev.replay()
         torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
@@ -315,7 +343,7 @@ def main():
 
     # per-kernel device durations inside the timed region (events: K1 start/end, K3 start/end, K2 start/end)
     def span(a, b_):
-        return statistics.mean(evs[i][a].elapsed_time(evs[i][b_]) for i in range(K))
+        return statistics.mean(r[a].elapsed_time(r[b_]) for r in evs)
     k_ms = {"k1_lse_gather": span(0, 1), "k2_alpha_beta": span(4, 5), "k3_grad": span(2, 3),
             "k2_exposed_wait": span(1, 2)}
     T_np, U_np = pb["logit_lens"], pb["target_lens"]
@@ -358,7 +386,9 @@ def main():
             "config": {"workload": workload_desc(base, variant), "variant": variant, "B_per_gpu": B,
                        "global_batch": B * world, "parallelism": f"dp{world} (batch shards, NCCL all-reduce of "
                        f"the fp64 loss sum)", "l2": f"inputs {z.numel() * esize / 1e9:.2f} GB/GPU > 126 MB L2: no flush",
-                       "grads": "in place" if inplace else "out of place"},
+                       "grads": "in place" if inplace else "out of place",
+                       "launch": (f"one CUDA graph of the {K} steps (kernel split: a second graph of the same "
+                                  f"{K} steps with timing events, replayed next)") if graph is not None else "eager"},
             "roofline": roof,
             "kernels_ms": k_ms,
             "kernel_gbs": {"k1_lse_gather": k1_gbs, "k3_grad": k3_gbs},

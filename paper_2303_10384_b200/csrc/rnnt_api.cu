@@ -28,6 +28,15 @@ rnnt_status check_sizes(int B, int Tmax, int Umax, int V, int blank) {
 rnnt_status launch_path(const rnnt::Problem& p, const rnnt::Workspace& w, cudaStream_t s,
                         void* const* events);
 
+// A timing event: while the stream is being captured into a CUDA graph it becomes an external event-record
+// node, which (unlike a plain captured record) is timed on every replay.
+cudaError_t record_timing(cudaEvent_t e, cudaStream_t s) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &st) != cudaSuccess) return cudaErrorUnknown;
+    return st == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal)
+                                               : cudaEventRecord(e, s);
+}
+
 rnnt_status run(const void* logits, int dtype, const int32_t* targets, const int32_t* logit_lens,
                 const int32_t* target_lens, int B, int Tmax, int Umax, int V, int blank, float* losses,
                 void* grads, const float* grad_scale, void* workspace, size_t workspace_bytes, void* stream,
@@ -123,15 +132,15 @@ rnnt_status launch_path(const Problem& p, const Workspace& w, cudaStream_t s, vo
     const int nch = overlap_chunks(p);
     AuxPool* pool = (nch > 1) ? aux_pool() : nullptr;
     if (nch == 1 || pool == nullptr) {
-        if (events && cudaEventRecord(ev(0), s) != cudaSuccess) return RNNT_ERR_CUDA;
+        if (events && record_timing(ev(0), s) != cudaSuccess) return RNNT_ERR_CUDA;
         if (rnnt::launch_k1_lse_gather(p, w, s) != cudaSuccess) return RNNT_ERR_CUDA;
-        if (events && (cudaEventRecord(ev(1), s) != cudaSuccess || cudaEventRecord(ev(4), s) != cudaSuccess))
+        if (events && (record_timing(ev(1), s) != cudaSuccess || record_timing(ev(4), s) != cudaSuccess))
             return RNNT_ERR_CUDA;
         if (rnnt::launch_k2_alpha_beta(p, w, s) != cudaSuccess) return RNNT_ERR_CUDA;
-        if (events && (cudaEventRecord(ev(5), s) != cudaSuccess || cudaEventRecord(ev(2), s) != cudaSuccess))
+        if (events && (record_timing(ev(5), s) != cudaSuccess || record_timing(ev(2), s) != cudaSuccess))
             return RNNT_ERR_CUDA;
         if (p.grads && rnnt::launch_k3_grad(p, w, s) != cudaSuccess) return RNNT_ERR_CUDA;
-        if (events && cudaEventRecord(ev(3), s) != cudaSuccess) return RNNT_ERR_CUDA;
+        if (events && record_timing(ev(3), s) != cudaSuccess) return RNNT_ERR_CUDA;
         return RNNT_OK;
     }
     Problem pc[kMaxChunks];
@@ -142,24 +151,26 @@ rnnt_status launch_path(const Problem& p, const Workspace& w, cudaStream_t s, vo
         b0 += nb;
     }
     auto ok = [](cudaError_t e) { return e == cudaSuccess; };
-    if (events && !ok(cudaEventRecord(ev(0), s))) return RNNT_ERR_CUDA;
+    if (events && !ok(record_timing(ev(0), s))) return RNNT_ERR_CUDA;
     for (int c = 0; c < nch; ++c) {
         cudaStream_t a = pool->aux[c];
         if (!ok(rnnt::launch_k1_lse_gather(pc[c], wc[c], s)) || !ok(cudaEventRecord(pool->k1_done[c], s)) ||
             !ok(cudaStreamWaitEvent(a, pool->k1_done[c], 0)))
             return RNNT_ERR_CUDA;
-        if (c == 0 && events && !ok(cudaEventRecord(ev(4), a))) return RNNT_ERR_CUDA;
-        if (!ok(rnnt::launch_k2_alpha_beta(pc[c], wc[c], a)) || !ok(cudaEventRecord(pool->k2_done[c], a)))
-            return RNNT_ERR_CUDA;
-        if (c == 0 && events && !ok(cudaEventRecord(ev(5), a))) return RNNT_ERR_CUDA;
+        if (c == 0 && events && !ok(record_timing(ev(4), a))) return RNNT_ERR_CUDA;
+        if (!ok(rnnt::launch_k2_alpha_beta(pc[c], wc[c], a))) return RNNT_ERR_CUDA;
+        // ev(5) before k2_done: everything on aux is then joined back into s by the wait on k2_done (a graph
+        // capture of this call must not leave work on aux unjoined).
+        if (c == 0 && events && !ok(record_timing(ev(5), a))) return RNNT_ERR_CUDA;
+        if (!ok(cudaEventRecord(pool->k2_done[c], a))) return RNNT_ERR_CUDA;
     }
-    if (events && !ok(cudaEventRecord(ev(1), s))) return RNNT_ERR_CUDA;
+    if (events && !ok(record_timing(ev(1), s))) return RNNT_ERR_CUDA;
     for (int c = 0; c < nch; ++c) {
         if (!ok(cudaStreamWaitEvent(s, pool->k2_done[c], 0))) return RNNT_ERR_CUDA;
-        if (c == 0 && events && !ok(cudaEventRecord(ev(2), s))) return RNNT_ERR_CUDA;
+        if (c == 0 && events && !ok(record_timing(ev(2), s))) return RNNT_ERR_CUDA;
         if (p.grads && !ok(rnnt::launch_k3_grad(pc[c], wc[c], s))) return RNNT_ERR_CUDA;
     }
-    if (events && !ok(cudaEventRecord(ev(3), s))) return RNNT_ERR_CUDA;
+    if (events && !ok(record_timing(ev(3), s))) return RNNT_ERR_CUDA;
     return RNNT_OK;
 }
 
