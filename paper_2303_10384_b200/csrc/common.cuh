@@ -78,43 +78,6 @@ __device__ __forceinline__ float lg2(float x) {
     return y;
 }
 
-// Streaming loads/stores.  ld.global.nc.L1::no_allocate: read-only path, no L1 allocation (K1 only:
-// logits are read-only there).  ld.global.cs / st.global.cs: evict-first streaming (K3, which may be in
-// place, so it avoids the non-coherent path).
-__device__ __forceinline__ float4 ld_stream_ro(const float4* p) {
-    float4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                 : "l"(p));
-    return v;
-}
-__device__ __forceinline__ float ld_stream_ro(const float* p) {
-    float v;
-    asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
-    return v;
-}
-__device__ __forceinline__ float4 ld_stream(const float4* p) {
-    float4 v;
-    asm volatile("ld.global.cs.v4.f32 {%0,%1,%2,%3}, [%4];"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                 : "l"(p)
-                 : "memory");
-    return v;
-}
-__device__ __forceinline__ float ld_stream(const float* p) {
-    float v;
-    asm volatile("ld.global.cs.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_stream(float4* p, float4 v) {
-    asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
-                 "f"(v.w)
-                 : "memory");
-}
-__device__ __forceinline__ void st_stream(float* p, float v) {
-    asm volatile("st.global.cs.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
-}
-
 // Packed fp32x2 arithmetic (sm_100: FFMA2 / FADD2 / FMUL2 -- two lanes of work per issue slot).
 typedef unsigned long long f32x2;
 __device__ __forceinline__ f32x2 pk(float lo, float hi) {
@@ -161,49 +124,6 @@ __device__ __forceinline__ uint64_t l2_evict_first() {
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
-__device__ __forceinline__ float4 ld_stream_ro(const float4* p, uint64_t pol) {
-    float4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                 : "l"(p), "l"(pol));
-    return v;
-}
-__device__ __forceinline__ float4 ld_stream(const float4* p, uint64_t pol) {
-    float4 v;
-    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                 : "l"(p), "l"(pol)
-                 : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_stream(float4* p, float4 v, uint64_t pol) {
-    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "f"(v.x),
-                 "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
-                 : "memory");
-}
-
-__device__ __forceinline__ float pick4(const float4& v, int k) {
-    return k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
-}
-
-// n / d for 0 <= n < 2^31 and d >= 1 with one IMAD.HI + shift (round-up reciprocal, 31 + ceil(log2 d) bits).
-struct FastDiv {
-    uint32_t d, m;
-    int s;
-    __device__ __forceinline__ uint32_t div(uint32_t n) const { return d == 1 ? n : (__umulhi(n, m) >> s); }
-};
-inline FastDiv make_fastdiv(uint32_t d) {
-    FastDiv f{d, 0u, 0};
-    if (d > 1) {
-        int l = 0;
-        while ((1ull << l) < d) ++l;  // ceil(log2 d)
-        const int p = 31 + l;
-        f.m = static_cast<uint32_t>(((1ull << p) + d - 1) / d);
-        f.s = p - 32;
-    }
-    return f;
-}
-
 // ---------------------------------------------------------------------------------------------------
 // Kernel launchers (defined in k1_lse_gather.cu, k2_alpha_beta.cu, k3_grad.cu).
 // ---------------------------------------------------------------------------------------------------
