@@ -8,7 +8,8 @@
 //          blank; allow-ignore: max of the terminating blank and the skips (t',U) -> F).
 // Ties are broken in a fixed order (reading R21): blank arc, then label arc, then skip arc; among
 // final skips the earliest source frame.  One CTA per utterance, thread u owns column u (one anti-diagonal
-// per step: shuffle + one named barrier when the row spans several warps).  Back-pointers (1 byte per cell)
+// per step: shuffle + one named barrier when the row spans several warps); operands are staged in registers
+// a group of kPf steps ahead, as in K2.  Back-pointers (1 byte per cell)
 // live in shared memory when Tmax x (Umax+1) fits (<= 200 KB), else in the workspace; delta is kept in the
 // workspace (anti-diagonal major) for the final-skip reductions.  Thread 0 back-traces.
 #include "common.cuh"
@@ -23,8 +24,8 @@ __device__ __forceinline__ void named_barrier_v(int nthreads) {
     asm volatile("bar.sync 2, %0;" ::"r"(nthreads) : "memory");
 }
 
-template <int kVariant>
-__global__ void __launch_bounds__(1024)
+template <int kVariant, int kPf, int kMaxThreads>
+__global__ void __launch_bounds__(kMaxThreads)
     k4_viterbi(const double2* __restrict__ lp, const int32_t* __restrict__ targets,
                const int32_t* __restrict__ T_b, const int32_t* __restrict__ U_b, int Tmax, int Umax, int V,
                int blank, double* __restrict__ delta_ws, uint8_t* __restrict__ bp_ws, int bp_in_smem,
@@ -62,33 +63,63 @@ __global__ void __launch_bounds__(1024)
 
     if (warp < nwarps) {
         const unsigned full = 0xffffffffu;
+        const int Teff = (u <= U) ? T : 0;
+        // Operand staging as in K2: two register groups of kPf wavefront steps, group g+1 loading while
+        // group g is consumed.  Loads past the last diagonal stay inside the padded lp array (kLpPad >= kPf).
+        const double2* ld_ptr = lpb + u;
+        double* st_ptr = dlt + u;
+        double2 ga[kPf], gb[kPf];
+        auto load_group = [&](double2 (&g)[kPf]) {
+#pragma unroll
+            for (int s = 0; s < kPf; ++s) {
+                g[s] = ld_ptr[0];
+                ld_ptr += Up1;
+            }
+        };
+        load_group(ga);
         double self = (u == 0) ? 0.0 : -INFINITY;  // delta(t-1,u) + X_b(t-1,u); (0,0) = max(0, -inf) = 0
         double pub = -INFINITY;                     // delta(t,u) + X_y(t,u) for column u+1
-        double2 xn = (u <= U) ? lpb[u] : make_double2(0.0, 0.0);  // operands of step 0 (cell (0-u, u))
-        for (int d = 0; d < D; ++d) {
-            const double2 x = xn;
-            if (d + 1 < D && u <= U) xn = lpb[static_cast<int64_t>(d + 1) * Up1 + u];  // one step ahead
+        auto step_fn = [&](int d, const double2& x) {
             double left = __shfl_up_sync(full, pub, 1);
-            if (lane == 0) left = (warp > 0 && d > 0) ? xfer[(d - 1) & 1][warp - 1] : -INFINITY;
+            if (nwarps > 1 && lane == 0) left = (warp > 0 && d > 0) ? xfer[(d - 1) & 1][warp - 1] : -INFINITY;
             const int t = d - u;
-            const bool valid = (u <= U) && (t >= 0) && (t < T);
-            double nb = left;
-            if (u == 0) nb = (kW && t >= 1) ? 0.0 : -INFINITY;  // initial skip (0,0)->(t,0)
-            double cur = self;
-            int from = kBpBlank;
-            if (nb > cur) {  // strict: ties keep the blank arc
-                cur = nb;
-                from = (u == 0) ? kBpSkip : kBpLabel;
-            }
+            const bool valid = static_cast<unsigned>(t) < static_cast<unsigned>(Teff);
+            double nb = (u == 0) ? ((kW && t >= 1) ? 0.0 : -INFINITY) : left;  // initial skip (0,0)->(t,0)
+            const bool take = nb > self;  // strict: ties keep the blank arc
+            const double cur = take ? nb : self;
             if (valid) {
-                dlt[static_cast<int64_t>(d) * Up1 + u] = cur;
-                bp[static_cast<int64_t>(t) * Up1 + u] = static_cast<uint8_t>(from);
+                *st_ptr = cur;
+                bp[static_cast<int64_t>(t) * Up1 + u] =
+                    static_cast<uint8_t>(take ? ((u == 0) ? kBpSkip : kBpLabel) : kBpBlank);
             }
+            st_ptr += Up1;
             self = valid ? cur + x.x : -INFINITY;
             pub = valid ? cur + x.y : -INFINITY;
             if (nwarps > 1) {
                 if (lane == 31) xfer[d & 1][warp] = pub;
                 named_barrier_v(nthr);
+            }
+        };
+        for (int i0 = 0; i0 < D; i0 += 2 * kPf) {
+            if (i0 + kPf < D) load_group(gb);
+            if (i0 + kPf <= D) {
+#pragma unroll
+                for (int s = 0; s < kPf; ++s) step_fn(i0 + s, ga[s]);
+            } else {
+#pragma unroll
+                for (int s = 0; s < kPf; ++s)
+                    if (i0 + s < D) step_fn(i0 + s, ga[s]);
+            }
+            const int i1 = i0 + kPf;
+            if (i1 >= D) break;
+            if (i1 + kPf < D) load_group(ga);
+            if (i1 + kPf <= D) {
+#pragma unroll
+                for (int s = 0; s < kPf; ++s) step_fn(i1 + s, gb[s]);
+            } else {
+#pragma unroll
+                for (int s = 0; s < kPf; ++s)
+                    if (i1 + s < D) step_fn(i1 + s, gb[s]);
             }
         }
         // Final arcs, by the warp owning column U.
@@ -171,22 +202,33 @@ __global__ void __launch_bounds__(1024)
     }
 }
 
-template <int kVariant>
-cudaError_t launch_v(const Problem& p, const Workspace& w, float* best, int32_t* frames, int32_t* span,
+template <int kVariant, int kPf, int kMaxThreads>
+cudaError_t launch_t(const Problem& p, const Workspace& w, float* best, int32_t* frames, int32_t* span,
                      cudaStream_t s) {
     const int threads = ((p.Umax + 1 + 31) / 32) * 32;
     const int64_t bp_bytes = static_cast<int64_t>(p.Tmax) * (p.Umax + 1);
     const bool in_smem = bp_bytes <= kSmemBpLimit;
     const size_t smem = in_smem ? static_cast<size_t>(bp_bytes) : 0;
+    auto kern = k4_viterbi<kVariant, kPf, kMaxThreads>;
     if (in_smem) {
-        const cudaError_t e =
-            cudaFuncSetAttribute(k4_viterbi<kVariant>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBpLimit);
+        const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBpLimit);
         if (e != cudaSuccess) return e;
     }
-    k4_viterbi<kVariant><<<p.B, threads, smem, s>>>(w.lp, p.targets, p.T_b, p.U_b, p.Tmax, p.Umax, p.V, p.blank,
-                                                    w.alpha, reinterpret_cast<uint8_t*>(w.beta), in_smem ? 1 : 0,
-                                                    best, frames, span);
+    kern<<<p.B, threads, smem, s>>>(w.lp, p.targets, p.T_b, p.U_b, p.Tmax, p.Umax, p.V, p.blank, w.alpha,
+                                    reinterpret_cast<uint8_t*>(w.beta), in_smem ? 1 : 0, best, frames, span);
     return cudaGetLastError();
+}
+
+// Thread bound by Umax + 1 (one column per thread); the staging depth shrinks with the register budget.
+template <int kVariant>
+cudaError_t launch_v(const Problem& p, const Workspace& w, float* best, int32_t* frames, int32_t* span,
+                     cudaStream_t s) {
+    const int up1 = p.Umax + 1;
+    if (up1 <= 32) return launch_t<kVariant, 16, 32>(p, w, best, frames, span, s);
+    if (up1 <= 128) return launch_t<kVariant, 16, 128>(p, w, best, frames, span, s);
+    if (up1 <= 256) return launch_t<kVariant, 16, 256>(p, w, best, frames, span, s);
+    if (up1 <= 512) return launch_t<kVariant, 8, 512>(p, w, best, frames, span, s);
+    return launch_t<kVariant, 4, 1024>(p, w, best, frames, span, s);
 }
 
 }  // namespace
