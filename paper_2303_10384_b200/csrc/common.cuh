@@ -117,6 +117,24 @@ __device__ __forceinline__ float max3(float a, float b, float c) {
     return d;
 }
 
+// log(e^a + e^b).  fp64 difference and max, fp32 MUFU correction.  -inf operands need no branch: if one
+// side is -inf the correction is exactly 0; if both are, diff is NaN, fminf(NaN, 0) = 0 and the result is
+// -inf + ln 2 = -inf.
+__device__ __forceinline__ double lse2f(double a, double b) {
+    const double diff = a - b;
+    const double m = (diff > 0.0) ? a : b;
+    const float x = fminf(-fabsf(static_cast<float>(diff)) * kLog2e, 0.f);
+    const float c = lg2(1.f + ex2(x)) * kLn2;
+    return m + static_cast<double>(c);
+}
+
+// LSE over the 32 lanes of a warp; every lane ends with the same value (lse2f is symmetric).
+__device__ __forceinline__ double warp_lse(double v) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v = lse2f(v, __shfl_xor_sync(0xffffffffu, v, off));
+    return v;
+}
+
 // L2 eviction policy for the once-read joint tensor: evict-first, so the streamed logits do not push the
 // (reused) workspace out of L2.
 __device__ __forceinline__ uint64_t l2_evict_first() {
@@ -147,5 +165,17 @@ cudaError_t launch_k3_grad(const Problem& p, const Workspace& w, cudaStream_t s)
 cudaError_t launch_loss_sum(const float* losses, int B, double* out, cudaStream_t s);
 cudaError_t launch_k4_viterbi(const Problem& p, const Workspace& w, float* best, int32_t* frames, int32_t* span,
                               cudaStream_t s);
+
+// Internal streams / events of the chunk-overlapped launch schedules (rnnt_api.cu): per host thread and
+// device, created once; nullptr if they cannot be created (callers then run sequentially).
+constexpr int kMaxChunks = 4;
+struct AuxPool {
+    bool ready = false;
+    cudaStream_t aux[kMaxChunks] = {};
+    cudaEvent_t k1_done[kMaxChunks] = {}, k2_done[kMaxChunks] = {};
+};
+AuxPool* aux_pool();
+// Number of utterance chunks for a call of B utterances and `elems` joint-tensor elements (1 = sequential).
+int overlap_chunks(int64_t B, int64_t elems);
 
 }  // namespace rnnt

@@ -34,24 +34,6 @@ __device__ __forceinline__ void named_barrier(int nthreads) {
     asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
 }
 
-// log(e^a + e^b).  fp64 difference and max, fp32 MUFU correction.  -inf operands need no branch: if one
-// side is -inf the correction is exactly 0; if both are, diff is NaN, fminf(NaN, 0) = 0 and the result is
-// -inf + ln 2 = -inf.
-__device__ __forceinline__ double lse2f(double a, double b) {
-    const double diff = a - b;
-    const double m = (diff > 0.0) ? a : b;
-    const float x = fminf(-fabsf(static_cast<float>(diff)) * kLog2e, 0.f);
-    const float c = lg2(1.f + ex2(x)) * kLn2;
-    return m + static_cast<double>(c);
-}
-
-// LSE over the 32 lanes of a warp; every lane ends with the same value (lse2f is symmetric).
-__device__ __forceinline__ double warp_lse(double v) {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v = lse2f(v, __shfl_xor_sync(0xffffffffu, v, off));
-    return v;
-}
-
 template <int kVariant, int kC, int kPf, int kMaxThreads>
 __global__ void __launch_bounds__(kMaxThreads)
     k2_alpha_beta(const double2* __restrict__ lp, const int32_t* __restrict__ targets,

@@ -87,40 +87,12 @@ void slice(const Problem& p, const Workspace& w, int b0, int nb, Problem& pc, Wo
 // Number of utterance chunks the call is split into so that K2 (latency-bound, 2 CTAs per utterance) of one
 // chunk runs concurrently with K1 / K3 (bandwidth-bound, the whole GPU) of the others.  Small calls (where
 // the split buys nothing) stay sequential.
-constexpr int kMaxChunks = 4;
 int overlap_chunks(const Problem& p) {
-    const int64_t elems = static_cast<int64_t>(p.B) * p.Tmax * (p.Umax + 1) * p.V;
-    if (p.B < 2 || elems < (int64_t(1) << 24)) return 1;
-    return std::min(p.B, kMaxChunks);
+    return rnnt::overlap_chunks(p.B, static_cast<int64_t>(p.B) * p.Tmax * (p.Umax + 1) * p.V);
 }
-
-// Per-host-thread, per-device cache of the internal streams / events of the overlapped path (creating
-// them per call would cost tens of microseconds of host time, comparable to a small call's device time).
-// Thread-local, so concurrent callers on different threads never share an event.
-struct AuxPool {
-    bool ready = false;
-    cudaStream_t aux[kMaxChunks] = {};
-    cudaEvent_t k1_done[kMaxChunks] = {}, k2_done[kMaxChunks] = {};
-};
-constexpr int kMaxDevices = 64;
-thread_local AuxPool t_pools[kMaxDevices];
-
-AuxPool* aux_pool() {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return nullptr;
-    AuxPool& pool = t_pools[dev];
-    if (pool.ready) return &pool;
-    int lo = 0, hi = 0;
-    if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) return nullptr;
-    for (int c = 0; c < kMaxChunks; ++c) {
-        if (cudaStreamCreateWithPriority(&pool.aux[c], cudaStreamNonBlocking, hi) != cudaSuccess ||
-            cudaEventCreateWithFlags(&pool.k1_done[c], cudaEventDisableTiming) != cudaSuccess ||
-            cudaEventCreateWithFlags(&pool.k2_done[c], cudaEventDisableTiming) != cudaSuccess)
-            return nullptr;
-    }
-    pool.ready = true;
-    return &pool;
-}
+using rnnt::AuxPool;
+using rnnt::aux_pool;
+using rnnt::kMaxChunks;
 
 // K1 -> K2 -> K3 for one call.  With chunks c = 0..n-1 the order is
 //   stream s:       K1(0) K1(1) .. K1(n-1)  [wait K2(0)] K3(0)  [wait K2(1)] K3(1) ..
@@ -175,6 +147,40 @@ rnnt_status launch_path(const Problem& p, const Workspace& w, cudaStream_t s, vo
 }
 
 }  // namespace
+
+namespace rnnt {
+
+int overlap_chunks(int64_t B, int64_t elems) {
+    if (B < 2 || elems < (int64_t(1) << 24)) return 1;
+    return static_cast<int>(std::min<int64_t>(B, kMaxChunks));
+}
+
+// Per-host-thread, per-device cache of the internal streams / events of the overlapped path (creating
+// them per call would cost tens of microseconds of host time, comparable to a small call's device time).
+// Thread-local, so concurrent callers on different threads never share an event.
+namespace {
+constexpr int kMaxDevices = 64;
+thread_local AuxPool t_pools[kMaxDevices];
+}  // namespace
+
+AuxPool* aux_pool() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return nullptr;
+    AuxPool& pool = t_pools[dev];
+    if (pool.ready) return &pool;
+    int lo = 0, hi = 0;
+    if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) return nullptr;
+    for (int c = 0; c < kMaxChunks; ++c) {
+        if (cudaStreamCreateWithPriority(&pool.aux[c], cudaStreamNonBlocking, hi) != cudaSuccess ||
+            cudaEventCreateWithFlags(&pool.k1_done[c], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&pool.k2_done[c], cudaEventDisableTiming) != cudaSuccess)
+            return nullptr;
+    }
+    pool.ready = true;
+    return &pool;
+}
+
+}  // namespace rnnt
 
 namespace {
 

@@ -81,3 +81,21 @@ def test_generic_engine_agrees_with_grid_kernels_in_place(rb, lat):
     torch.cuda.synchronize()
     assert torch.allclose(l_gen, l_grid, rtol=1e-5, atol=0)
     assert (g_gen - g_grid).abs().max().item() < 1e-4
+
+
+@pytest.mark.parametrize("variant", ("force_final", "allow_ignore"))
+@pytest.mark.parametrize("shape", [(3, 300, 64, 512), (2, 40, 600, 16), (1, 8200, 2, 8)],
+                         ids=["ring_overflow_chunked", "wide_levels", "uncached_levels"])
+def test_engine_schedule_paths(rb, lat, shape, variant):
+    """L3's less common paths: neighbours older than the shared-memory ring (W skips across > 16384 states)
+    with the chunk-overlapped schedule (>= 2^24 elements), levels wider than a CTA (strided), and more levels
+    than the cached level table; the W skip states also take the warp-cooperative (> 2 arcs) branch."""
+    B, T, U, V = shape
+    cfg = workloads.random_config(B, T, U, V, seed=T + U + 5, variant=variant, variable=False)
+    pb = workloads.problem(cfg)
+    L = lat.grid_lattices(pb["logit_lens"], pb["target_lens"], pb["targets"], 0, variant)
+    losses, grads = rb.rnnt_lattice_loss(pb["logits"].cuda(), L, pb["logit_lens"], pb["target_lens"])
+    torch.cuda.synchronize()
+    ref_l, ref_g = oracle.batch(pb["logits"].numpy(), pb["targets"], pb["logit_lens"], pb["target_lens"], 0,
+                                variant)
+    _close(losses.cpu().numpy().astype(np.float64), grads.cpu().numpy(), ref_l, ref_g)
