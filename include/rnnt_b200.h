@@ -167,6 +167,25 @@ rnnt_status rnnt_loss_host(const float* logits_host, const int32_t* targets_host
                            float* losses_host, float* grads_host,
                            void* device_buffer, size_t device_buffer_bytes, void* stream);
 
+/* Fused joint network + loss (§4.1: the benchmark's joint over Encoder
+ * and Predictor embeddings of size 512; X comes from the joint network).  The logits
+ *   z[b,t,u,v] = bias[v] + sum_k bf16(tanh(enc[b,t,k] + pred[b,u,k])) * weight[v,k]      (R22)
+ * are computed tile by tile on the tensor cores (tcgen05, fp32 accumulation) and reduced on chip to the
+ * log-softmax normalizer and the Populate gathers -- the [B,Tmax,Umax+1,V] tensor is never written -- and
+ * the losses follow as for rnnt_loss / wrnnt_loss of z (variant: -1 = RNN-T, else a wrnnt_variant).
+ *   enc    [B][Tmax][H] bf16, pred [B][Umax+1][H] bf16, weight [V][H] bf16 (16-byte aligned), bias [V] fp32
+ *          or NULL (= 0); targets / lens / losses / workspace as for rnnt_loss (rnnt_workspace_bytes).
+ * Forward only (losses).  Requires H % 128 == 0, H <= 512, V % 128 == 0 (else RNNT_ERR_UNSUPPORTED). */
+rnnt_status rnnt_joint_loss(const void* enc, const void* pred, const void* weight, const float* bias,
+                            const int32_t* targets, const int32_t* logit_lens, const int32_t* target_lens,
+                            int B, int Tmax, int Umax, int H, int V, int blank, int variant, float* losses,
+                            void* workspace, size_t workspace_bytes, void* stream);
+/* As rnnt_joint_loss; events (NULL or 4 cudaEvent_t): K6 start / end, K2 start / end. */
+rnnt_status rnnt_joint_loss_ex(const void* enc, const void* pred, const void* weight, const float* bias,
+                               const int32_t* targets, const int32_t* logit_lens, const int32_t* target_lens,
+                               int B, int Tmax, int Umax, int H, int V, int blank, int variant, float* losses,
+                               void* workspace, size_t workspace_bytes, void* stream, void* const* events);
+
 const char* rnnt_status_string(rnnt_status status);
 
 /* Library version, e.g. "rnnt_b200 0.1 sm_100a". */

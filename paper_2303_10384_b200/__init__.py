@@ -23,7 +23,8 @@ VARIANTS = {"rnnt": -1, "force_final": 0, "allow_ignore": 1}
 # Every symbol include/rnnt_b200.h declares.
 EXPORTS = ("rnnt_workspace_bytes", "rnnt_loss", "wrnnt_loss", "rnnt_loss_timed", "rnnt_loss_ex", "rnnt_viterbi",
            "rnnt_loss_sum", "rnnt_lattice_workspace_bytes", "rnnt_lattice_loss",
-           "rnnt_host_buffer_bytes", "rnnt_loss_host", "rnnt_status_string", "rnnt_version")
+           "rnnt_host_buffer_bytes", "rnnt_loss_host", "rnnt_joint_loss", "rnnt_joint_loss_ex",
+           "rnnt_status_string", "rnnt_version")
 DTYPES = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2}
 
 
@@ -50,6 +51,8 @@ def _load():
         "rnnt_loss_sum": ([P, I, P, P], I),
         "rnnt_host_buffer_bytes": ([I, I, I, I], S),
         "rnnt_loss_host": ([P, P, P, P, I, I, I, I, I, I, P, P, P, S, P], I),
+        "rnnt_joint_loss": ([P, P, P, P, P, P, P, I, I, I, I, I, I, I, P, P, S, P], I),
+        "rnnt_joint_loss_ex": ([P, P, P, P, P, P, P, I, I, I, I, I, I, I, P, P, S, P, P], I),
         "rnnt_status_string": ([I], ctypes.c_char_p),
         "rnnt_version": ([], ctypes.c_char_p),
     }
@@ -194,6 +197,44 @@ def rnnt_viterbi(logits, targets, logit_lens, target_lens, blank=0, variant="rnn
                                 _ptr(frames) if Umax > 0 else None, _ptr(span), _ptr(workspace), workspace.numel(),
                                 _stream(stream)))
     return best, frames, span
+
+
+def rnnt_joint_loss(enc, pred, weight, bias, targets, logit_lens, target_lens, blank=0, variant="rnnt",
+                    losses=None, workspace=None, stream=None, events=None):
+    """Fused joint network + loss (NEXT-4): z = bf16(tanh(enc[:, :, None] + pred[:, None])) @ weight.T + bias
+    is reduced on chip (tcgen05 GEMM + log-softmax / Populate epilogue) and never materialised; returns the
+    per-utterance losses [B].  enc [B, Tmax, H], pred [B, Umax+1, H], weight [V, H]: CUDA bfloat16; bias [V]
+    float32 or None.  events: None or 4 recorded torch.cuda.Events (K6 start / end, K2 start / end)."""
+    for name, x in (("enc", enc), ("pred", pred), ("weight", weight)):
+        if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.bfloat16 and x.is_contiguous()):
+            raise TypeError(f"{name} must be a contiguous CUDA bfloat16 tensor (no CPU fallback)")
+    B, Tmax, H = enc.shape
+    Up1 = pred.shape[1]
+    Umax = Up1 - 1
+    V = weight.shape[0]
+    if pred.shape != (B, Up1, H) or weight.shape != (V, H):
+        raise ValueError("shapes: enc [B, Tmax, H], pred [B, Umax+1, H], weight [V, H]")
+    dev = enc.device
+    if bias is not None:
+        bias = bias.to(device=dev, dtype=torch.float32).contiguous()
+    targets = _as_i32(targets, dev).reshape(B, Umax) if Umax > 0 else None
+    logit_lens = _as_i32(logit_lens, dev)
+    target_lens = _as_i32(target_lens, dev)
+    if losses is None:
+        losses = torch.empty(B, dtype=torch.float32, device=dev)
+    if workspace is None:
+        workspace = torch.empty(max(rnnt_workspace_bytes(B, Tmax, Umax), 1), dtype=torch.uint8, device=dev)
+    ev = None
+    if events is not None:
+        handles = [e.cuda_event for e in events]
+        if len(handles) != 4 or not all(handles):
+            raise ValueError("need 4 recorded torch.cuda.Events")
+        ev = ctypes.cast((ctypes.c_void_p * 4)(*handles), ctypes.c_void_p)
+    _check(library.rnnt_joint_loss_ex(_ptr(enc), _ptr(pred), _ptr(weight), _ptr(bias), _ptr(targets),
+                                      _ptr(logit_lens), _ptr(target_lens), B, Tmax, Umax, H, V, int(blank),
+                                      VARIANTS[variant], _ptr(losses), _ptr(workspace), workspace.numel(),
+                                      _stream(stream), ev))
+    return losses
 
 
 def rnnt_lattice_loss(logits, lattices, logit_lens, target_lens, grads=True, losses=None, stream=None):

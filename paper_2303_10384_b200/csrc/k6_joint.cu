@@ -1,0 +1,512 @@
+// k6_joint.cu -- K6: the joint network fused with K1: the logits tensor is never
+// materialised.
+//
+// PAPER.md §4.1: the benchmark pipeline feeds the loss from a joint network over Encoder and Predictor
+// embeddings of size 512; the log-probabilities tensor X comes from that network.  The joint here
+// is the standard transducer joiner (reading R22):
+//   h(b,t,u,:) = bf16( tanh( f(b,t,:) + g(b,u,:) ) )            f: [B,Tmax,H], g: [B,Umax+1,H] bf16
+//   z(b,t,u,v) = sum_k h(b,t,u,k) W(v,k) + bias(v)                W: [V,H] bf16, bias fp32, fp32 accumulate
+// and K6 produces exactly what K1 produces from z -- lse(t,u) and the Populate gathers X_b, X_y (§2.2 Eq.(3)
+// P:88) in K2's anti-diagonal layout -- so K2 then yields the losses unchanged.
+//
+// One persistent CTA per SM (16 warps), rows = the (b,t,u) cells in tiles of 128:
+//   warp 0       TMA producer: W tiles [128 v x 64 k] (SWIZZLE_128B) into a ring of kStages smem stages
+//   warp 1       TMEM owner + MMA issuer: tcgen05.mma.kind::f16, A = h tile from TMEM (128 lanes x H/2 cols),
+//                B = W stage (smem descriptor), D = fp32 accumulator 128 x 128 in TMEM (two buffers)
+//   warps 4-7    epilogue: tcgen05.ld of the accumulator (thread = row), + bias, online max / sum of
+//                exp over V, gathers z[blank] and z[y_u]; writes lse and (X_b, X_y) like K1
+//   warps 8-15   A builders: tanh(f + g) of the NEXT tile into a shared-memory staging buffer while the
+//                MMAs of the current tile run; once those complete, one tcgen05.st pass moves it into TMEM
+// TMEM: A [0, 256) columns, accumulators [256, 384) and [384, 512).  mbarriers link the roles.
+// Constraints: H % 128 == 0, H <= 512; V % 128 == 0.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "elem.cuh"
+#include "rnnt_b200.h"
+
+namespace rnnt {
+namespace {
+
+constexpr int kRowsPerTile = 128;
+constexpr int kNTile = 128;      // accumulator columns per MMA
+constexpr int kKBlock = 64;      // K per W stage (128 B of bf16: one SWIZZLE_128B row)
+constexpr int kStageBytes = kNTile * kKBlock * 2;
+constexpr int kThreads = 512;
+constexpr int kMaxStages = 8;
+constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kAccCol0 = 256;
+
+// ---- PTX wrappers -------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "W%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra W%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+        "[%4];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+// D[tmem] (+)= A[tmem] . B[smem]^T, M = 128, N = kNTile, K = 16, bf16 in, fp32 accumulate.
+__device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                       uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, {%5, %6, %7, %8}, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(0), "r"(0), "r"(0), "r"(0)
+        : "memory");
+}
+// Instruction descriptor: fp32 D (bits 4-5 = 1), bf16 A (7-9 = 1) and B (10-12 = 1), both K-major,
+// N >> 3 at bits 17-22, M >> 4 at bits 24-28.
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(kNTile >> 3) << 17) | (uint32_t(128 >> 4) << 24);
+// Shared-memory matrix descriptor of a K-major SWIZZLE_128B tile (rows of 128 B, 8-row atoms of 1024 B):
+// start >> 4, LBO 16 B (unused for swizzled K-major), SBO 1024 B, version 1, layout SWIZZLE_128B (2).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+    return static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4) | (static_cast<uint64_t>(1) << 16) |
+           (static_cast<uint64_t>(1024 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) | (static_cast<uint64_t>(2) << 61);
+}
+
+#define TMEM_LD32(taddr, r)                                                                                     \
+    asm volatile(                                                                                               \
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18," \
+        "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                                         \
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),       \
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), \
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]),            \
+          "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),            \
+          "=r"(r[30]), "=r"(r[31])                                                                              \
+        : "r"(taddr))
+#define TMEM_ST32(taddr, r)                                                                                     \
+    asm volatile(                                                                                               \
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17," \
+        "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),                          \
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),      \
+        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),         \
+        "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),        \
+        "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])                     \
+        : "memory")
+
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+// tanh in fp32 to ~1e-7 relative, mostly on the FMA pipe (MUFU is the epilogue's): |x| >= 1/8:
+// 1 - 2 / (1 + 2^(2|x| log2 e)) with 2^y = 2^round(y) * poly(frac) (degree-6 Taylor on [-1/2, 1/2]);
+// |x| < 1/8: the odd series to x^9.
+__device__ __forceinline__ float tanh_f(float x) {
+    const float a = fabsf(x);
+    const float y = fminf(a * 2.8853900817779268f, 126.f);
+    const float j = rintf(y);
+    const float f = y - j;
+    float p = 1.5403530393381606e-4f;
+    p = fmaf(p, f, 1.3333558146428443e-3f);
+    p = fmaf(p, f, 9.6181291076284772e-3f);
+    p = fmaf(p, f, 5.5504108664821580e-2f);
+    p = fmaf(p, f, 2.4022650695910071e-1f);
+    p = fmaf(p, f, 6.9314718055994531e-1f);
+    p = fmaf(p, f, 1.0f);
+    const float e = __int_as_float(__float_as_int(p) + (static_cast<int>(j) << 23));
+    const float big = fmaf(-2.f, rcp_approx(1.f + e), 1.f);
+    const float a2 = a * a;
+    float s = fmaf(a2, 0.021869488536155203f, -0.053968253968253971f);
+    s = fmaf(s, a2, 0.13333333333333333f);
+    s = fmaf(s, a2, -0.33333333333333333f);
+    const float small = fmaf(s * a2, a, a);
+    return copysignf(a < 0.125f ? small : big, x);
+}
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+    const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<const uint32_t*>(&v);
+}
+__device__ __forceinline__ float2 unpack_bf16x2(uint32_t w) {
+    return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
+}
+
+struct JointArgs {
+    const __nv_bfloat16* f;
+    const __nv_bfloat16* g;
+    const float* bias;
+    const int32_t* targets;
+    const int32_t* T_b;
+    const int32_t* U_b;
+    int B, Tmax, Umax, H, V, blank;
+    int64_t rows;  // B * Tmax * (Umax + 1)
+    int stages;
+    float* lse_out;
+    double2* lp_out;
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k6_joint_lse(const __grid_constant__ CUtensorMap w_map, const JointArgs a) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // carve: [W stages (1024-aligned)] [A staging 128 x H bf16] [bias V fp32] [barriers] [tmem slot]
+    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* wst = base;
+    uint8_t* stage_a = wst + static_cast<size_t>(a.stages) * kStageBytes;
+    float* sbias = reinterpret_cast<float*>(stage_a + static_cast<size_t>(kRowsPerTile) * a.H * 2);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sbias + a.V);
+    uint64_t* b_full = bars;                   // [stages]
+    uint64_t* b_empty = bars + kMaxStages;     // [stages]
+    uint64_t* a_full = bars + 2 * kMaxStages;
+    uint64_t* a_empty = a_full + 1;
+    uint64_t* acc_full = a_full + 2;           // [2]
+    uint64_t* acc_empty = a_full + 4;          // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_full + 6);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int H = a.H, V = a.V;
+    const int KB = H / kKBlock, NT = V / kNTile;
+    const int64_t ntiles = (a.rows + kRowsPerTile - 1) / kRowsPerTile;
+
+    for (int i = threadIdx.x; i < V; i += blockDim.x) sbias[i] = a.bias ? a.bias[i] : 0.f;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < a.stages; ++s) {
+            mbar_init(&b_full[s], 1);
+            mbar_init(&b_empty[s], 1);
+        }
+        mbar_init(a_full, 256);
+        mbar_init(a_empty, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&acc_full[i], 1);
+            mbar_init(&acc_empty[i], 128);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&w_map)) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ===== TMA producer =====
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
+                for (int n = 0; n < NT; ++n)
+                    for (int kb = 0; kb < KB; ++kb) {
+                        mbar_wait(&b_empty[s], ph ^ 1);
+                        mbar_expect_tx(&b_full[s], kStageBytes);
+                        tma_load_2d(wst + static_cast<size_t>(s) * kStageBytes, &w_map, &b_full[s], kb * kKBlock,
+                                    n * kNTile);
+                        if (++s == a.stages) {
+                            s = 0;
+                            ph ^= 1;
+                        }
+                    }
+        }
+    } else if (warp == 1) {
+        // ===== MMA issuer =====
+        int s = 0;
+        uint32_t ph = 0;
+        uint32_t it = 0;  // accumulator use counter
+        uint32_t tl = 0;  // local tile counter
+        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tl) {
+            mbar_wait(a_full, tl & 1);
+            tc_fence_after();
+            for (int n = 0; n < NT; ++n, ++it) {
+                const uint32_t acc = it & 1;
+                mbar_wait(&acc_empty[acc], ((it >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem + kAccCol0 + acc * kNTile;
+                for (int kb = 0; kb < KB; ++kb) {
+                    mbar_wait(&b_full[s], ph);
+                    tc_fence_after();
+                    if (lane == 0) {
+                        const uint64_t bdesc = sw128_desc(smem_u32(wst + static_cast<size_t>(s) * kStageBytes));
+#pragma unroll
+                        for (int k = 0; k < kKBlock / 16; ++k)
+                            mma_ts(d_tmem, tmem + kb * (kKBlock / 2) + k * 8, bdesc + static_cast<uint64_t>(k * 2),
+                                   kIdesc, (kb | k) ? 1u : 0u);
+                        tc_commit(&b_empty[s]);  // frees the W stage when these MMAs complete
+                    }
+                    __syncwarp();
+                    if (++s == a.stages) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+                if (lane == 0) tc_commit(&acc_full[acc]);
+                __syncwarp();
+            }
+            if (lane == 0) tc_commit(a_empty);  // the A tile in TMEM may be overwritten
+            __syncwarp();
+        }
+    } else if (warp >= 4 && warp < 8) {
+        // ===== epilogue: thread = row =====
+        const int q = warp & 3;
+        const int rl = q * 32 + lane;
+        const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16);
+        uint32_t it = 0;
+        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            const int64_t row = tile * kRowsPerTile + rl;
+            const bool in = row < a.rows;
+            const int64_t cells = static_cast<int64_t>(a.Tmax) * (a.Umax + 1);
+            const int b = in ? static_cast<int>(row / cells) : 0;
+            const int rem = in ? static_cast<int>(row - static_cast<int64_t>(b) * cells) : 0;
+            const int t = rem / (a.Umax + 1), u = rem - t * (a.Umax + 1);
+            const int T = in ? min(a.T_b[b], a.Tmax) : 0, U = in ? min(a.U_b[b], a.Umax) : 0;
+            const bool live = in && t < T && u <= U;
+            const int yv = (live && u < U) ? a.targets[static_cast<int64_t>(b) * a.Umax + u] : -1;
+            float m = -INFINITY, ssum = 0.f, zb = 0.f, zy = 0.f;
+            for (int n = 0; n < NT; ++n, ++it) {
+                const uint32_t acc = it & 1;
+                mbar_wait(&acc_full[acc], (it >> 1) & 1);
+                tc_fence_after();
+#pragma unroll 1
+                for (int c = 0; c < kNTile / 32; ++c) {
+                    uint32_t r[32];
+                    TMEM_LD32(lane_base + kAccCol0 + acc * kNTile + c * 32, r);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    const int v0 = n * kNTile + c * 32;
+                    float z[32];
+                    float cm = -INFINITY;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        z[j] = __uint_as_float(r[j]) + sbias[v0 + j];
+                        cm = fmaxf(cm, z[j]);
+                    }
+                    const float mn = fmaxf(m, cm);
+                    const float mnl = mn * kLog2e;
+                    float part = 0.f;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) part += ex2(fmaf(z[j], kLog2e, -mnl));
+                    ssum = fmaf(ssum, ex2((m - mn) * kLog2e), part);
+                    m = mn;
+                    if (static_cast<unsigned>(a.blank - v0) < 32u) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (v0 + j == a.blank) zb = z[j];
+                    }
+                    if (static_cast<unsigned>(yv - v0) < 32u) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (v0 + j == yv) zy = z[j];
+                    }
+                }
+                tc_fence_before();
+                mbar_arrive(&acc_empty[acc]);
+            }
+            if (live) {
+                const float lse = m + lg2(ssum) * kLn2;
+                const int64_t urow = static_cast<int64_t>(b) * cells + rem;
+                a.lse_out[urow] = lse;
+                const bool ybad = (u < U) && (yv < 0 || yv >= a.V || yv == a.blank);
+                const float xb = zb - lse;
+                const float xy = (u < U) ? (ybad ? __int_as_float(0x7fc00000) : zy - lse) : -INFINITY;
+                const int64_t diag = static_cast<int64_t>(b) * (a.Tmax + a.Umax) + (t + u);
+                a.lp_out[diag * (a.Umax + 1) + u] = make_double2(xb, xy);
+            }
+        }
+    } else if (warp >= 8) {
+        // ===== A builders: warp -> (row quarter q, K half kh) =====
+        const int q = warp & 3, kh = (warp - 8) >> 2;
+        const int rl = q * 32 + lane;
+        const int nch = H / 16;            // 16-byte chunks per K half
+        const int row_bytes = H * 2;
+        uint8_t* my_row = stage_a + static_cast<size_t>(rl) * row_bytes;
+        const int64_t cells = static_cast<int64_t>(a.Tmax) * (a.Umax + 1);
+        auto build = [&](int64_t tile) {
+            const int64_t row = tile * kRowsPerTile + rl;
+            const bool in = row < a.rows;
+            const int b = in ? static_cast<int>(row / cells) : 0;
+            const int rem = in ? static_cast<int>(row - static_cast<int64_t>(b) * cells) : 0;
+            const int t = rem / (a.Umax + 1), u = rem - t * (a.Umax + 1);
+            const uint4* fr = reinterpret_cast<const uint4*>(a.f + (static_cast<int64_t>(b) * a.Tmax + t) * H) + kh * nch;
+            const uint4* gr = reinterpret_cast<const uint4*>(a.g + (static_cast<int64_t>(b) * (a.Umax + 1) + u) * H) + kh * nch;
+#pragma unroll 4
+            for (int c = 0; c < nch; ++c) {
+                uint4 o = make_uint4(0u, 0u, 0u, 0u);
+                if (in) {
+                    const uint4 fa = __ldg(fr + c), ga = __ldg(gr + c);
+                    const uint32_t fw[4] = {fa.x, fa.y, fa.z, fa.w}, gw[4] = {ga.x, ga.y, ga.z, ga.w};
+                    uint32_t ow[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float2 x = unpack_bf16x2(fw[e]), y = unpack_bf16x2(gw[e]);
+                        ow[e] = pack_bf16x2(tanh_f(x.x + y.x), tanh_f(x.y + y.y));
+                    }
+                    o = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+                }
+                const int cg = kh * nch + c;  // chunk index in the row; XOR swizzle avoids bank conflicts
+                *reinterpret_cast<uint4*>(my_row + ((cg ^ (rl & 7)) << 4)) = o;
+            }
+        };
+        const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16);
+        uint32_t tl = 0;
+        int64_t tile = blockIdx.x;
+        if (tile < ntiles) build(tile);
+        for (; tile < ntiles; tile += gridDim.x, ++tl) {
+            if (tl > 0) mbar_wait(a_empty, (tl - 1) & 1);
+            tc_fence_after();
+            // staging -> TMEM: this thread's row, its K half = nch chunks = nch * 4 columns
+            for (int c0 = 0; c0 < nch; c0 += 8) {
+                uint32_t r[32];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int cg = kh * nch + c0 + i;
+                    const uint4 v = *reinterpret_cast<const uint4*>(my_row + ((cg ^ (rl & 7)) << 4));
+                    r[4 * i + 0] = v.x;
+                    r[4 * i + 1] = v.y;
+                    r[4 * i + 2] = v.z;
+                    r[4 * i + 3] = v.w;
+                }
+                TMEM_ST32(lane_base + static_cast<uint32_t>((kh * nch + c0) * 4), r);
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            tc_fence_before();
+            mbar_arrive(a_full);
+            if (tile + gridDim.x < ntiles) build(tile + gridDim.x);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
+}
+
+size_t joint_smem_bytes(int H, int V, int stages) {
+    return 1024 + static_cast<size_t>(stages) * kStageBytes + static_cast<size_t>(kRowsPerTile) * H * 2 +
+           static_cast<size_t>(V) * 4 + (2 * kMaxStages + 6) * 8 + 16;
+}
+
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiled encode_fn() {
+    static EncodeTiled fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiled>(p);
+    }
+    return fn;
+}
+
+}  // namespace
+}  // namespace rnnt
+
+namespace {
+// A timing event; under stream capture an external event-record node (timed on every replay).
+cudaError_t record_ev(void* const* events, int i, cudaStream_t s) {
+    if (!events) return cudaSuccess;
+    cudaEvent_t e = static_cast<cudaEvent_t>(events[i]);
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &st) != cudaSuccess) return cudaErrorUnknown;
+    return st == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal)
+                                               : cudaEventRecord(e, s);
+}
+}  // namespace
+
+extern "C" rnnt_status rnnt_joint_loss_ex(const void* enc, const void* pred, const void* weight, const float* bias,
+                                          const int32_t* targets, const int32_t* logit_lens,
+                                          const int32_t* target_lens, int B, int Tmax, int Umax, int H, int V,
+                                          int blank, int variant, float* losses, void* workspace,
+                                          size_t workspace_bytes, void* stream, void* const* events) {
+    using namespace rnnt;
+    if (B < 0 || Tmax < 1 || Umax < 0 || V < 2 || blank < 0 || blank >= V || H < 1) return RNNT_ERR_INVALID_ARG;
+    if (variant < -1 || variant > 1) return RNNT_ERR_INVALID_ARG;
+    if (Umax + 1 > kMaxUp1 || H % 128 != 0 || H > 512 || V % kNTile != 0) return RNNT_ERR_UNSUPPORTED;
+    if (B == 0) return RNNT_OK;
+    if (!enc || !pred || !weight || !logit_lens || !target_lens || !losses || !workspace) return RNNT_ERR_INVALID_ARG;
+    if (Umax > 0 && !targets) return RNNT_ERR_INVALID_ARG;
+    if (workspace_bytes < rnnt::workspace_bytes(B, Tmax, Umax)) return RNNT_ERR_WORKSPACE_TOO_SMALL;
+    if ((reinterpret_cast<uintptr_t>(enc) | reinterpret_cast<uintptr_t>(pred) | reinterpret_cast<uintptr_t>(weight)) % 16)
+        return RNNT_ERR_INVALID_ARG;
+    EncodeTiled enc_fn = encode_fn();
+    if (!enc_fn) return RNNT_ERR_CUDA;
+    CUtensorMap map;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(H), static_cast<cuuint64_t>(V)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(H) * 2};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(kKBlock), static_cast<cuuint32_t>(kNTile)};
+    const cuuint32_t estr[2] = {1, 1};
+    if (enc_fn(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(weight), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return RNNT_ERR_CUDA;
+
+    int dev = 0, nsm = 0, smem_max = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
+        return RNNT_ERR_CUDA;
+    int stages = kMaxStages;
+    while (stages > 2 && joint_smem_bytes(H, V, stages) > static_cast<size_t>(smem_max)) --stages;
+    const size_t smem = joint_smem_bytes(H, V, stages);
+    if (smem > static_cast<size_t>(smem_max)) return RNNT_ERR_UNSUPPORTED;
+    if (cudaFuncSetAttribute(k6_joint_lse, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
+        cudaSuccess)
+        return RNNT_ERR_CUDA;
+
+    const Workspace w = carve(workspace, B, Tmax, Umax);
+    JointArgs args{static_cast<const __nv_bfloat16*>(enc), static_cast<const __nv_bfloat16*>(pred), bias, targets,
+                   logit_lens, target_lens, B, Tmax, Umax, H, V, blank,
+                   static_cast<int64_t>(B) * Tmax * (Umax + 1), stages, w.lse, w.lp};
+    const int64_t ntiles = (args.rows + kRowsPerTile - 1) / kRowsPerTile;
+    const int grid = static_cast<int>(std::min<int64_t>(ntiles, nsm));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (record_ev(events, 0, s) != cudaSuccess) return RNNT_ERR_CUDA;
+    k6_joint_lse<<<grid, kThreads, smem, s>>>(map, args);
+    if (cudaGetLastError() != cudaSuccess || record_ev(events, 1, s) != cudaSuccess) return RNNT_ERR_CUDA;
+    const int vk = (variant < 0) ? kRnnt : (variant == WRNNT_FORCE_FINAL ? kForceFinal : kAllowIgnore);
+    Problem p{nullptr, targets, logit_lens, target_lens, B, Tmax, Umax, V, blank, vk, losses, nullptr, nullptr, kF32};
+    if (record_ev(events, 2, s) != cudaSuccess || launch_k2_alpha_beta(p, w, s) != cudaSuccess ||
+        record_ev(events, 3, s) != cudaSuccess)
+        return RNNT_ERR_CUDA;
+    return RNNT_OK;
+}
+
+extern "C" rnnt_status rnnt_joint_loss(const void* enc, const void* pred, const void* weight, const float* bias,
+                                       const int32_t* targets, const int32_t* logit_lens, const int32_t* target_lens,
+                                       int B, int Tmax, int Umax, int H, int V, int blank, int variant,
+                                       float* losses, void* workspace, size_t workspace_bytes, void* stream) {
+    return rnnt_joint_loss_ex(enc, pred, weight, bias, targets, logit_lens, target_lens, B, Tmax, Umax, H, V, blank,
+                              variant, losses, workspace, workspace_bytes, stream, nullptr);
+}

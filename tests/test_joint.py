@@ -1,0 +1,72 @@
+"""GPU parity of the fused joint network + loss (rnnt_joint_loss, NEXT-4: tcgen05 GEMM with the log-softmax /
+Populate epilogue, then K2) vs the oracle (oracle/joint.py, pinned in tests/test_joint_oracle.py).  Bar: loss
+within 1e-5 relative (floor |L| >= 1), the loss path's bar; the GEMM accumulates in fp32 and h is rounded to
+bf16 on both sides (reading R22)."""
+import numpy as np
+import pytest
+import torch
+
+import workloads
+from oracle import joint as oj
+
+pytestmark = pytest.mark.gpu
+VARIANTS = ("rnnt", "force_final", "allow_ignore")
+
+
+@pytest.fixture(scope="module")
+def rb():
+    import paper_2303_10384_b200
+    return paper_2303_10384_b200
+
+
+def _case(rb, B, T, U, H, V, seed, variant, blank=0, variable=True, bias=True):
+    cfg = workloads.random_config(B, T, U, V, seed=seed, blank=blank, variant=variant, variable=variable)
+    T_b, U_b = workloads.lengths(cfg)
+    y = workloads.targets(cfg, U_b)
+    enc, pred, W, b = workloads.joint_inputs(B, T, U, H, V, seed=seed)
+    if not bias:
+        b = None
+    losses = rb.rnnt_joint_loss(enc.cuda(), pred.cuda(), W.cuda(), None if b is None else b.cuda(), y, T_b, U_b,
+                                blank, variant)
+    torch.cuda.synchronize()
+    ref = oj.joint_loss(enc.double().numpy(), pred.double().numpy(), W.double().numpy(),
+                        None if b is None else b.double().numpy(), y, T_b, U_b, blank, variant)
+    l = losses.cpu().numpy().astype(np.float64)
+    rel = np.abs(l - ref) / np.maximum(np.abs(ref), 1.0)
+    assert rel.max() <= 1e-5, (rel.max(), l, ref)
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("shape", [(2, 9, 4, 128, 128), (3, 37, 11, 256, 384), (2, 50, 20, 512, 1024)],
+                         ids=lambda s: "B{}_T{}_U{}_H{}_V{}".format(*s))
+def test_joint_loss_matches_oracle(rb, shape, variant):
+    B, T, U, H, V = shape
+    _case(rb, B, T, U, H, V, seed=sum(shape) % 97 + 3, variant=variant)
+
+
+def test_joint_blank_last_no_bias_many_tiles(rb):
+    # > 148 row tiles (every CTA loops), ragged last tile, blank = V-1, no bias
+    _case(rb, 4, 120, 40, 384, 256, seed=17, variant="rnnt", blank=255, variable=False, bias=False)
+
+
+def test_joint_matches_materialised_loss_path(rb):
+    """Same utterances two ways on the GPU: the fused path, and the oracle-built logits through rnnt_loss."""
+    B, T, U, H, V = 3, 60, 25, 512, 512
+    cfg = workloads.random_config(B, T, U, V, seed=23, variant="allow_ignore")
+    T_b, U_b = workloads.lengths(cfg)
+    y = workloads.targets(cfg, U_b)
+    enc, pred, W, b = workloads.joint_inputs(B, T, U, H, V, seed=23)
+    z = torch.from_numpy(oj.joint_logits(enc.double().numpy(), pred.double().numpy(), W.double().numpy(),
+                                         b.double().numpy()).astype(np.float32)).cuda()
+    l_ref, _ = rb.wrnnt_loss(z, y, T_b, U_b, 0, "allow_ignore", grads=False)
+    l = rb.rnnt_joint_loss(enc.cuda(), pred.cuda(), W.cuda(), b.cuda(), y, T_b, U_b, 0, "allow_ignore")
+    torch.cuda.synchronize()
+    assert torch.allclose(l, l_ref, rtol=1e-5, atol=1e-5)
+
+
+def test_joint_rejects_unsupported_shapes(rb):
+    enc = torch.zeros(1, 4, 96, dtype=torch.bfloat16, device="cuda")
+    pred = torch.zeros(1, 3, 96, dtype=torch.bfloat16, device="cuda")
+    W = torch.zeros(128, 96, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(rb.RnntError):
+        rb.rnnt_joint_loss(enc, pred, W, None, [[1, 2]], [4], [2])

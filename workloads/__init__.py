@@ -149,3 +149,20 @@ def random_config(B, Tmax, Umax, V, seed, blank=0, variant="rnnt", variable=True
     return Config(f"rand_B{B}_T{Tmax}_U{Umax}_V{V}_s{seed}", B=B, Tmax=Tmax, Umax=Umax, V=V, blank=blank,
                   variant=variant, variable_lengths=variable, t_lo=1, u_lo=0, logit_seed=10_000 * seed,
                   len_seed=seed, tgt_seed=77 * seed + 5)
+
+
+def joint_inputs(B, Tmax, Umax, H, V, seed, device="cpu"):
+    """Seeded inputs of the fused joint network (NEXT-4, §4.1: Encoder / Predictor embeddings
+    of size H = 512): enc [B,Tmax,H] and pred [B,Umax+1,H] ~ N(0, 1/2) each (so enc + pred ~ N(0, 1), the
+    pre-activation range of a trained joiner), weight [V,H] ~ N(0, 1/H), all rounded to bf16; bias [V] ~
+    N(0, 0.1^2) fp32.  Per-utterance streams (seed, b) as for the logits, so a shard is a slice."""
+    gen = torch.Generator().manual_seed(7_000_003 * seed + 11)
+    weight = (torch.randn(V, H, generator=gen) / math.sqrt(H)).to(torch.bfloat16)
+    bias = torch.randn(V, generator=gen) * 0.1
+    enc = torch.empty(B, Tmax, H, dtype=torch.bfloat16)
+    pred = torch.empty(B, Umax + 1, H, dtype=torch.bfloat16)
+    for b in range(B):
+        gb = torch.Generator().manual_seed(7_000_003 * seed + 1_000 + b)
+        enc[b] = (torch.randn(Tmax, H, generator=gb) * math.sqrt(0.5)).to(torch.bfloat16)
+        pred[b] = (torch.randn(Umax + 1, H, generator=gb) * math.sqrt(0.5)).to(torch.bfloat16)
+    return enc.to(device), pred.to(device), weight.to(device), bias.to(device)
