@@ -51,10 +51,12 @@ def parse():
     ap.add_argument("--dtype", default="f32", choices=["f32", "bf16", "f16"],
                     help="storage type of logits/grads (arithmetic is fp32/fp64 either way); the BASELINE "
                          "metric is quoted on f32")
-    ap.add_argument("--mode", default="loss_grad", choices=["loss_grad", "loss", "viterbi", "lattice"],
+    ap.add_argument("--mode", default="loss_grad", choices=["loss_grad", "loss", "viterbi", "lattice", "joint"],
                     help="loss_grad: the BASELINE metric; loss: losses only (K1+K2); viterbi: forced alignment "
                          "(K1+K4) -- SURVEY 8(f) NEXT-2; lattice: the same loss+grad through the generic "
-                         "acyclic-lattice engine on explicit Grid/W lattices -- NEXT-3")
+                         "acyclic-lattice engine on explicit Grid/W lattices -- NEXT-3; joint: the fused joint "
+                         "network + loss forward from Encoder/Predictor embeddings (H=--hidden) -- NEXT-4")
+    ap.add_argument("--hidden", type=int, default=512, help="--mode joint: embedding size H (P:124: 512)")
     ap.add_argument("--eager", action="store_true",
                     help="launch the K timed steps one by one from Python instead of replaying them as one CUDA graph "
                          "(the default at N=1 for --mode loss_grad / loss: no host launch overhead between kernels)")
@@ -242,6 +244,8 @@ def main():
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if args.mode == "joint":
+        return main_joint(args, rb, rdist, rank, world, local, dev)
 
     base = workloads.CONFIGS[args.config]
     variant = args.variant or base.variant
@@ -452,6 +456,130 @@ def main():
                                 "host_cores_available": host_cores()}
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
+# ------------------------------------------------------------------------------------------ fused joint (NEXT-4)
+def main_joint(args, rb, rdist, rank, world, local, dev):
+    """utterances/s of the fused joint network + loss forward (rnnt_joint_loss: K6 tcgen05 GEMM with the
+    log-softmax / Populate epilogue, then K2), inputs = Encoder / Predictor embeddings of size H."""
+    base = workloads.CONFIGS[args.config]
+    variant = args.variant or base.variant
+    gcfg = dataclasses.replace(base, B=base.B_per_gpu * world)
+    b_ids = rdist.contiguous_shard(gcfg.B, rank, world)
+    H = args.hidden
+    T_np, U_np = workloads.lengths(gcfg)
+    T_np, U_np = T_np[b_ids], U_np[b_ids]
+    y_np = workloads.targets(gcfg, workloads.lengths(gcfg)[1], b_ids=b_ids)
+    enc, pred, W, bias = workloads.joint_inputs(gcfg.B, gcfg.Tmax, gcfg.Umax, H, gcfg.V, seed=gcfg.logit_seed % 1000 + 1)
+    enc, pred = enc[b_ids[0]:b_ids[-1] + 1].to(dev), pred[b_ids[0]:b_ids[-1] + 1].to(dev)
+    W, bias = W.to(dev), bias.to(dev)
+    B, Tmax, _ = enc.shape
+    Umax, V = gcfg.Umax, gcfg.V
+    targets = torch.from_numpy(y_np).to(dev)
+    T_b = torch.from_numpy(T_np).to(dev)
+    U_b = torch.from_numpy(U_np).to(dev)
+    losses = torch.empty(B, dtype=torch.float32, device=dev)
+    loss_sum = torch.empty((), dtype=torch.float64, device=dev)
+    workspace = torch.empty(rb.rnnt_workspace_bytes(B, Tmax, Umax), dtype=torch.uint8, device=dev)
+    K, Wm = args.steps, args.warmup
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+    for row in evs:
+        for e in row:
+            e.record()
+    torch.cuda.synchronize()
+
+    def step(events=None):
+        rb.rnnt_joint_loss(enc, pred, W, bias, targets, T_b, U_b, gcfg.blank, variant, losses=losses,
+                           workspace=workspace, events=events)
+        rb.rnnt_loss_sum(losses, out=loss_sum)
+        rdist.allreduce_loss_sum(loss_sum)
+
+    for _ in range(Wm):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    graph = graph_ev = None
+    if not args.eager and world == 1:
+        graph, graph_ev = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            for i in range(K):
+                step(None)
+        with torch.cuda.graph(graph_ev):
+            for i in range(K):
+                step(evs[i])
+        graph.replay()
+        graph_ev.replay()
+        torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        start.record()
+        if graph is not None:
+            graph.replay()
+        else:
+            for i in range(K):
+                step(evs[i])
+        end.record()
+        torch.cuda.synchronize()
+    if graph_ev is not None:
+        graph_ev.replay()
+        torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    ms_step = rdist.max_over_ranks(start.elapsed_time(end), dev) / K
+    value = B * world / (ms_step / 1e3)
+    k6_ms = statistics.mean(r[0].elapsed_time(r[1]) for r in evs)
+    k2_ms = statistics.mean(r[2].elapsed_time(r[3]) for r in evs)
+    rows = B * Tmax * (Umax + 1)
+    flops = 2.0 * rows * V * H
+    tf = flops / (k6_ms / 1e3) / 1e12
+    with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+        mp = json.load(f)
+    peak = float(mp["bf16_tflops_sustained"])
+    loss_total = float(loss_sum.item())
+    if rank != 0:
+        if world > 1:
+            torch.distributed.barrier()
+            torch.distributed.destroy_process_group()
+        return
+    line = {
+        "metric": "utterances/s fused joint+loss forward (not the BASELINE metric)", "value": value, "unit": UNIT,
+        "n_gpus": world, "steps": K, "warmup": Wm, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": f"{base.name} shapes through the joint: B={B}/GPU, Tmax={Tmax}, Umax={Umax}, "
+                               f"V={V}, H={H} (enc/pred bf16, W [V,H] bf16, fp32 accumulate), "
+                               f"{'RNN-T' if variant == 'rnnt' else 'W-RNNT ' + variant}",
+                   "variant": variant, "B_per_gpu": B, "global_batch": B * world, "H": H,
+                   "l2": "no flush: the joint's inputs (enc/pred/W, "
+                         f"{(enc.numel() + pred.numel() + W.numel()) * 2 / 1e6:.0f} MB) are meant to be L2/HBM "
+                         "resident; the [B,T,U+1,V] logits are never written",
+                   "launch": "one CUDA graph of the K steps (split from a second graph with events)"
+                             if graph is not None else "eager"},
+        "roofline": {"bound": "tensor", "kernel": "k6_joint_lse", "achieved": tf, "peak": peak, "unit": "TFLOP/s",
+                     "frac": tf / peak, "traffic": None, "algorithmic_flops_per_launch": flops,
+                     "peak_source": "measured (MEASURED_PEAKS.json bf16_tflops_sustained: the kernel runs back "
+                                    "to back inside the timed step)",
+                     "frac_of_burst_peak": tf / float(mp["bf16_tflops"])},
+        "kernels_ms": {"k6_joint_lse": k6_ms, "k2_alpha_beta": k2_ms},
+        "clocks": clocks.summary(),
+        "gpu_launches": 3 * K,
+        "loss_sum_last_step": loss_total,
+        "e2e": None,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        from oracle import joint as oj
+        ids = [0]
+        t0 = time.perf_counter()
+        oj.joint_loss(enc[:1].double().cpu().numpy(), pred[:1].double().cpu().numpy(), W.double().cpu().numpy(),
+                      bias.double().cpu().numpy(), y_np[:1], T_np[:1], U_np[:1], gcfg.blank, variant)
+        secs = time.perf_counter() - t0
+        line["cpu_baseline"] = {"value": len(ids) / secs, "unit": UNIT, "cores": torch.get_num_threads(),
+                                "kind": "oracle", "sample": f"1 utterance through oracle/joint.py (numpy fp64 "
+                                f"joint + C loss oracle), {secs:.1f} s wall"}
+    print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()
