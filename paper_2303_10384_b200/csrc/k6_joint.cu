@@ -126,29 +126,16 @@ __device__ __forceinline__ float rcp_approx(float x) {
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
-// tanh in fp32 to ~1e-7 relative, mostly on the FMA pipe (MUFU is the epilogue's): |x| >= 1/8:
-// 1 - 2 / (1 + 2^(2|x| log2 e)) with 2^y = 2^round(y) * poly(frac) (degree-6 Taylor on [-1/2, 1/2]);
-// |x| < 1/8: the odd series to x^9.
+// tanh in fp32, ~1e-7 absolute: |x| >= 1/16: 1 - 2 / (1 + 2^(2|x| log2 e)) (MUFU ex2 and rcp; inf -> 1);
+// |x| < 1/16: x - x^3/3 + 2x^5/15 (truncation < 1e-9 relative), which avoids the cancellation in 1 - 2r.
 __device__ __forceinline__ float tanh_f(float x) {
     const float a = fabsf(x);
-    const float y = fminf(a * 2.8853900817779268f, 126.f);
-    const float j = rintf(y);
-    const float f = y - j;
-    float p = 1.5403530393381606e-4f;
-    p = fmaf(p, f, 1.3333558146428443e-3f);
-    p = fmaf(p, f, 9.6181291076284772e-3f);
-    p = fmaf(p, f, 5.5504108664821580e-2f);
-    p = fmaf(p, f, 2.4022650695910071e-1f);
-    p = fmaf(p, f, 6.9314718055994531e-1f);
-    p = fmaf(p, f, 1.0f);
-    const float e = __int_as_float(__float_as_int(p) + (static_cast<int>(j) << 23));
+    const float e = ex2(a * 2.8853900817779268f);
     const float big = fmaf(-2.f, rcp_approx(1.f + e), 1.f);
     const float a2 = a * a;
-    float s = fmaf(a2, 0.021869488536155203f, -0.053968253968253971f);
-    s = fmaf(s, a2, 0.13333333333333333f);
-    s = fmaf(s, a2, -0.33333333333333333f);
+    const float s = fmaf(a2, 0.13333333333333333f, -0.33333333333333333f);
     const float small = fmaf(s * a2, a, a);
-    return copysignf(a < 0.125f ? small : big, x);
+    return copysignf(a < 0.0625f ? small : big, x);
 }
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
@@ -302,20 +289,36 @@ __global__ void __launch_bounds__(kThreads, 1)
                     TMEM_LD32(lane_base + kAccCol0 + acc * kNTile + c * 32, r);
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                     const int v0 = n * kNTile + c * 32;
-                    float z[32];
+                    const float4* b4 = reinterpret_cast<const float4*>(sbias + v0);
+                    f32x2 zz[16];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const float4 bb = b4[j];
+                        zz[2 * j] = fadd2(pk(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1])), pk(bb.x, bb.y));
+                        zz[2 * j + 1] =
+                            fadd2(pk(__uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3])), pk(bb.z, bb.w));
+                    }
                     float cm = -INFINITY;
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        z[j] = __uint_as_float(r[j]) + sbias[v0 + j];
-                        cm = fmaxf(cm, z[j]);
+                    for (int j = 0; j < 16; ++j) {
+                        const float2 v = upk(zz[j]);
+                        cm = max3(cm, v.x, v.y);
                     }
                     const float mn = fmaxf(m, cm);
-                    const float mnl = mn * kLog2e;
-                    float part = 0.f;
+                    const f32x2 l2 = pk(kLog2e, kLog2e), nml = pk(-mn * kLog2e, -mn * kLog2e);
+                    f32x2 acc2 = pk(0.f, 0.f);
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) part += ex2(fmaf(z[j], kLog2e, -mnl));
-                    ssum = fmaf(ssum, ex2((m - mn) * kLog2e), part);
+                    for (int j = 0; j < 16; ++j) acc2 = fadd2(acc2, ex2x2(ffma2(zz[j], l2, nml)));
+                    const float2 a2s = upk(acc2);
+                    ssum = fmaf(ssum, ex2((m - mn) * kLog2e), a2s.x + a2s.y);
                     m = mn;
+                    float z[32];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const float2 v = upk(zz[j]);
+                        z[2 * j] = v.x;
+                        z[2 * j + 1] = v.y;
+                    }
                     if (static_cast<unsigned>(a.blank - v0) < 32u) {
 #pragma unroll
                         for (int j = 0; j < 32; ++j)
@@ -343,37 +346,70 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp >= 8) {
         // ===== A builders: warp -> (row quarter q, K half kh) =====
+        // Build: lane = 16-byte K chunk, so each load instruction reads contiguous bytes of one row (coalesced;
+        // consecutive rows mostly share the f row).  Copy to TMEM: thread = row (tcgen05.st lane quarter).
         const int q = warp & 3, kh = (warp - 8) >> 2;
         const int rl = q * 32 + lane;
         const int nch = H / 16;            // 16-byte chunks per K half
         const int row_bytes = H * 2;
         uint8_t* my_row = stage_a + static_cast<size_t>(rl) * row_bytes;
         const int64_t cells = static_cast<int64_t>(a.Tmax) * (a.Umax + 1);
+        const uint4* f4 = reinterpret_cast<const uint4*>(a.f);
+        const uint4* g4 = reinterpret_cast<const uint4*>(a.g);
+        const int items = 32 * nch;        // (row of the quarter, chunk of the half)
         auto build = [&](int64_t tile) {
-            const int64_t row = tile * kRowsPerTile + rl;
-            const bool in = row < a.rows;
-            const int b = in ? static_cast<int>(row / cells) : 0;
-            const int rem = in ? static_cast<int>(row - static_cast<int64_t>(b) * cells) : 0;
-            const int t = rem / (a.Umax + 1), u = rem - t * (a.Umax + 1);
-            const uint4* fr = reinterpret_cast<const uint4*>(a.f + (static_cast<int64_t>(b) * a.Tmax + t) * H) + kh * nch;
-            const uint4* gr = reinterpret_cast<const uint4*>(a.g + (static_cast<int64_t>(b) * (a.Umax + 1) + u) * H) + kh * nch;
-#pragma unroll 4
-            for (int c = 0; c < nch; ++c) {
-                uint4 o = make_uint4(0u, 0u, 0u, 0u);
-                if (in) {
-                    const uint4 fa = __ldg(fr + c), ga = __ldg(gr + c);
-                    const uint32_t fw[4] = {fa.x, fa.y, fa.z, fa.w}, gw[4] = {ga.x, ga.y, ga.z, ga.w};
+            // lane r: chunk offsets (16-byte units) of row q*32 + r's f and g rows, -1 past the end
+            int fo = -1, go = -1;
+            {
+                const int64_t row = tile * kRowsPerTile + rl;
+                if (row < a.rows) {
+                    const int b = static_cast<int>(row / cells);
+                    const int rem = static_cast<int>(row - static_cast<int64_t>(b) * cells);
+                    const int t = rem / (a.Umax + 1), u = rem - t * (a.Umax + 1);
+                    fo = (b * a.Tmax + t) * (H / 8) + kh * nch;
+                    go = (b * (a.Umax + 1) + u) * (H / 8) + kh * nch;
+                }
+            }
+            int rr = lane / nch, c = lane - (lane / nch) * nch;  // this lane's first item
+            const int drr = 32 / nch, dc = 32 - drr * nch;        // item += 32 (nch in {8, 16, 24, 32})
+            for (int i0 = 0; i0 < items; i0 += 4 * 32) {
+                uint4 fa[4], ga[4];
+                int rows_[4], cs[4];
+                bool ok[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    rows_[j] = rr;
+                    cs[j] = c;
+                    const bool in_range = i0 + j * 32 < items;
+                    const int fro = __shfl_sync(0xffffffffu, fo, rr & 31), gro = __shfl_sync(0xffffffffu, go, rr & 31);
+                    ok[j] = in_range && fro >= 0;
+                    fa[j] = ok[j] ? __ldg(f4 + fro + c) : make_uint4(0u, 0u, 0u, 0u);
+                    ga[j] = ok[j] ? __ldg(g4 + gro + c) : make_uint4(0u, 0u, 0u, 0u);
+                    rr += drr;
+                    c += dc;
+                    if (c >= nch) {
+                        c -= nch;
+                        ++rr;
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    if (i0 + j * 32 >= items) break;
+                    const uint32_t fw[4] = {fa[j].x, fa[j].y, fa[j].z, fa[j].w};
+                    const uint32_t gw[4] = {ga[j].x, ga[j].y, ga[j].z, ga[j].w};
                     uint32_t ow[4];
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         const float2 x = unpack_bf16x2(fw[e]), y = unpack_bf16x2(gw[e]);
-                        ow[e] = pack_bf16x2(tanh_f(x.x + y.x), tanh_f(x.y + y.y));
+                        ow[e] = ok[j] ? pack_bf16x2(tanh_f(x.x + y.x), tanh_f(x.y + y.y)) : 0u;
                     }
-                    o = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+                    const int r2 = q * 32 + rows_[j];
+                    const int cg = kh * nch + cs[j];
+                    *reinterpret_cast<uint4*>(stage_a + static_cast<size_t>(r2) * row_bytes + ((cg ^ (r2 & 7)) << 4)) =
+                        make_uint4(ow[0], ow[1], ow[2], ow[3]);
                 }
-                const int cg = kh * nch + c;  // chunk index in the row; XOR swizzle avoids bank conflicts
-                *reinterpret_cast<uint4*>(my_row + ((cg ^ (rl & 7)) << 4)) = o;
             }
+            __syncwarp();  // each thread copies its own row, written by the whole warp
         };
         const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16);
         uint32_t tl = 0;
