@@ -13,17 +13,21 @@
 //   warp 0       TMA producer: W tiles [128 v x 64 k] (SWIZZLE_128B) into a ring of kStages smem stages
 //   warp 1       TMEM owner + MMA issuer: tcgen05.mma.kind::f16, A = h tile from TMEM (128 lanes x H/2 cols),
 //                B = W stage (smem descriptor), D = fp32 accumulator 128 x 128 in TMEM (two buffers)
-//   warps 4-7    epilogue: tcgen05.ld of the accumulator (thread = row), + bias, online max / sum of
-//                exp over V, gathers z[blank] and z[y_u]; writes lse and (X_b, X_y) like K1
-//   warps 8-15   A builders: tanh(f + g) of the NEXT tile into a shared-memory staging buffer while the
+//   warps 4-11   epilogue, two groups of 4 (group g drains accumulator buffer g): tcgen05.ld (thread = row), + bias,
+//                online max / sum of exp over V, gathers z[blank] and z[y_u]; group 0 merges group 1's
+//                partials and writes lse and (X_b, X_y) like K1
+//   warps 12-19  A builders: tanh(f + g) of the NEXT tile into a shared-memory staging buffer while the
 //                MMAs of the current tile run; once those complete, one tcgen05.st pass moves it into TMEM
-// TMEM: A [0, 256) columns, accumulators [256, 384) and [384, 512).  mbarriers link the roles.
+// TMEM: A [0, 256) columns, kAccBufs = 2 accumulators of 128 columns in [256, 512).  (N = 64 with four
+// buffers was measured slower: 2.20 vs 1.77 ms at c3 / H = 512 -- the narrower MMAs lose more than the
+// deeper buffering gains.)  mbarriers link the roles.
 // Constraints: H % 128 == 0, H <= 512; V % 128 == 0.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 
 #include "common.cuh"
 #include "elem.cuh"
@@ -33,11 +37,12 @@ namespace rnnt {
 namespace {
 
 constexpr int kRowsPerTile = 128;
-constexpr int kNTile = 128;      // accumulator columns per MMA
+constexpr int kNTile = 128;      // accumulator columns per MMA (N)
+constexpr int kAccBufs = 2;      // accumulator buffers in TMEM (kAccBufs * kNTile = 256 columns)
 constexpr int kKBlock = 64;      // K per W stage (128 B of bf16: one SWIZZLE_128B row)
 constexpr int kStageBytes = kNTile * kKBlock * 2;
-constexpr int kThreads = 512;
-constexpr int kMaxStages = 8;
+constexpr int kThreads = 640;  // 20 warps: TMA, MMA, 2 spare, 2 x 4 epilogue, 8 builders
+constexpr int kMaxStages = 16;
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kAccCol0 = 256;
 
@@ -66,6 +71,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// mbar_wait that adds the cycles spent to *acc (diagnostics, RNNT_K6_DEBUG & 4)
+__device__ __forceinline__ void mbar_wait_t(uint64_t* bar, uint32_t parity, bool on, unsigned long long& acc) {
+    const long long t0 = on ? clock64() : 0;
+    mbar_wait(bar, parity);
+    if (on) acc += clock64() - t0;
+}
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
@@ -75,20 +86,42 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-                 : "memory");
-}
-// D[tmem] (+)= A[tmem] . B[smem]^T, M = 128, N = kNTile, K = 16, bf16 in, fp32 accumulate.
-__device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
-                                       uint32_t accumulate) {
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {  // by one elected lane of a converged warp
     asm volatile(
         "{\n"
-        ".reg .pred p;\n"
+        ".reg .pred e;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+        "}\n" ::"r"(smem_u32(bar))
+        : "memory");
+}
+// One K block (64 = 4 x K16) of D[tmem] (+)= A[tmem] . B[smem]^T, M = 128, N = kNTile, bf16 in, fp32
+// accumulate: the four MMAs in one asm block so that the operands reach the uniform datapath once (per-MMA
+// asm statements cost ~15 issue slots each in ELECT / R2UR conversions, as much as the MMA itself takes).
+// A advances 8 TMEM columns (16 bf16) and the B descriptor 32 bytes (>> 4 = 2) per K16 step.  Called by the
+// whole converged warp with warp-uniform operands; elect.sync picks the issuing lane.
+__device__ __forceinline__ void mma_kblock(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                           uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p, q, e;\n"
+        ".reg .b32 a1, a2, a3;\n"
+        ".reg .b64 b1, b2, b3;\n"
         "setp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, {%5, %6, %7, %8}, p;\n"
+        "setp.eq.b32 q, %4, %4;\n"
+        "add.u32 a1, %1, 8;\n"
+        "add.u32 a2, %1, 16;\n"
+        "add.u32 a3, %1, 24;\n"
+        "add.u64 b1, %2, 2;\n"
+        "add.u64 b2, %2, 4;\n"
+        "add.u64 b3, %2, 6;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %3, q;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], b2, %3, q;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], b3, %3, q;\n"
         "}\n" ::"r"(d_tmem),
-        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(0), "r"(0), "r"(0), "r"(0)
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
 // Instruction descriptor: fp32 D (bits 4-5 = 1), bf16 A (7-9 = 1) and B (10-12 = 1), both K-major,
@@ -127,8 +160,10 @@ __device__ __forceinline__ float rcp_approx(float x) {
     return y;
 }
 // tanh in fp32, ~1e-7 absolute: |x| >= 1/16: 1 - 2 / (1 + 2^(2|x| log2 e)) (MUFU ex2 and rcp; inf -> 1);
-// |x| < 1/16: x - x^3/3 + 2x^5/15 (truncation < 1e-9 relative), which avoids the cancellation in 1 - 2r.
-__device__ __forceinline__ float tanh_f(float x) {
+// |x| < 1/16: x - x^3/3 + 2x^5/15 (truncation < 1e-9 relative), avoiding the cancellation in 1 - 2r.
+// (An FMA-pipe polynomial for the exponential, leaving MUFU to the epilogue, measured slower: 1.75 vs
+// 1.67 ms -- the builders are issue-bound, not MUFU-bound.)
+__device__ __forceinline__ float tanh_mufu(float x) {
     const float a = fabsf(x);
     const float e = ex2(a * 2.8853900817779268f);
     const float big = fmaf(-2.f, rcp_approx(1.f + e), 1.f);
@@ -155,6 +190,10 @@ struct JointArgs {
     int B, Tmax, Umax, H, V, blank;
     int64_t rows;  // B * Tmax * (Umax + 1)
     int stages;
+    int dbg;  // diagnostics (env RNNT_K6_DEBUG, never set in production): 1 = builders skip tanh,
+              // 2 = epilogue skips its math (both give wrong losses: timing ablations only), 4 = per-role
+              // barrier-wait cycle counters printed to stderr
+    unsigned long long* prof;
     float* lse_out;
     double2* lp_out;
 };
@@ -167,14 +206,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* wst = base;
     uint8_t* stage_a = wst + static_cast<size_t>(a.stages) * kStageBytes;
     float* sbias = reinterpret_cast<float*>(stage_a + static_cast<size_t>(kRowsPerTile) * a.H * 2);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sbias + a.V);
+    float4* xchg = reinterpret_cast<float4*>(sbias + a.V);  // [2][128] epilogue group 1 -> group 0 partials
+    uint64_t* bars = reinterpret_cast<uint64_t*>(xchg + 2 * kRowsPerTile);
     uint64_t* b_full = bars;                   // [stages]
     uint64_t* b_empty = bars + kMaxStages;     // [stages]
     uint64_t* a_full = bars + 2 * kMaxStages;
     uint64_t* a_empty = a_full + 1;
-    uint64_t* acc_full = a_full + 2;           // [2]
-    uint64_t* acc_empty = a_full + 4;          // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_full + 6);
+    uint64_t* acc_full = a_full + 2;                 // [kAccBufs]
+    uint64_t* acc_empty = a_full + 2 + kAccBufs;     // [kAccBufs]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_full + 2 + 2 * kAccBufs);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int H = a.H, V = a.V;
@@ -189,7 +229,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mbar_init(a_full, 256);
         mbar_init(a_empty, 1);
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kAccBufs; ++i) {
             mbar_init(&acc_full[i], 1);
             mbar_init(&acc_empty[i], 128);
         }
@@ -206,6 +246,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    const bool pon = (a.dbg & 4) != 0;
+    unsigned long long w_tma = 0, w_afull = 0, w_accempty = 0, w_bfull = 0, w_accfull = 0, w_aempty = 0;
+    const long long t_start = clock64();
 
     if (warp == 0) {
         // ===== TMA producer =====
@@ -215,7 +258,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
                 for (int n = 0; n < NT; ++n)
                     for (int kb = 0; kb < KB; ++kb) {
-                        mbar_wait(&b_empty[s], ph ^ 1);
+                        mbar_wait_t(&b_empty[s], ph ^ 1, pon, w_tma);
                         mbar_expect_tx(&b_full[s], kStageBytes);
                         tma_load_2d(wst + static_cast<size_t>(s) * kStageBytes, &w_map, &b_full[s], kb * kKBlock,
                                     n * kNTile);
@@ -232,42 +275,36 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t it = 0;  // accumulator use counter
         uint32_t tl = 0;  // local tile counter
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tl) {
-            mbar_wait(a_full, tl & 1);
+            mbar_wait_t(a_full, tl & 1, pon, w_afull);
             tc_fence_after();
             for (int n = 0; n < NT; ++n, ++it) {
-                const uint32_t acc = it & 1;
-                mbar_wait(&acc_empty[acc], ((it >> 1) & 1) ^ 1);
+                const uint32_t acc = it % kAccBufs;
+                mbar_wait_t(&acc_empty[acc], ((it / kAccBufs) & 1) ^ 1, pon, w_accempty);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem + kAccCol0 + acc * kNTile;
                 for (int kb = 0; kb < KB; ++kb) {
-                    mbar_wait(&b_full[s], ph);
+                    mbar_wait_t(&b_full[s], ph, pon, w_bfull);
                     tc_fence_after();
-                    if (lane == 0) {
-                        const uint64_t bdesc = sw128_desc(smem_u32(wst + static_cast<size_t>(s) * kStageBytes));
-#pragma unroll
-                        for (int k = 0; k < kKBlock / 16; ++k)
-                            mma_ts(d_tmem, tmem + kb * (kKBlock / 2) + k * 8, bdesc + static_cast<uint64_t>(k * 2),
-                                   kIdesc, (kb | k) ? 1u : 0u);
-                        tc_commit(&b_empty[s]);  // frees the W stage when these MMAs complete
-                    }
-                    __syncwarp();
+                    const uint64_t bdesc = sw128_desc(smem_u32(wst + static_cast<size_t>(s) * kStageBytes));
+                    mma_kblock(d_tmem, tmem + kb * (kKBlock / 2), bdesc, kIdesc, kb ? 1u : 0u);
+                    tc_commit(&b_empty[s]);  // frees the W stage when these MMAs complete
                     if (++s == a.stages) {
                         s = 0;
                         ph ^= 1;
                     }
                 }
-                if (lane == 0) tc_commit(&acc_full[acc]);
-                __syncwarp();
+                tc_commit(&acc_full[acc]);
             }
-            if (lane == 0) tc_commit(a_empty);  // the A tile in TMEM may be overwritten
-            __syncwarp();
+            tc_commit(a_empty);  // the A tile in TMEM may be overwritten
         }
-    } else if (warp >= 4 && warp < 8) {
-        // ===== epilogue: thread = row =====
-        const int q = warp & 3;
+    } else if (warp >= 4 && warp < 12) {
+        // ===== epilogue: thread = row; group eg = 0 / 1 owns accumulator buffer eg, i.e. every other N tile
+        // (the MMA alternates buffers), so the two groups drain in parallel; per tile, group 1 hands its row
+        // partials (max, sum, z[blank], z[y]) to group 0 through shared memory, which finishes the row =====
+        const int q = warp & 3, eg = (warp - 4) >> 2;
         const int rl = q * 32 + lane;
         const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16);
-        uint32_t it = 0;
+        uint32_t it = 0, tile_local = 0;
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
             const int64_t row = tile * kRowsPerTile + rl;
             const bool in = row < a.rows;
@@ -280,14 +317,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int yv = (live && u < U) ? a.targets[static_cast<int64_t>(b) * a.Umax + u] : -1;
             float m = -INFINITY, ssum = 0.f, zb = 0.f, zy = 0.f;
             for (int n = 0; n < NT; ++n, ++it) {
-                const uint32_t acc = it & 1;
-                mbar_wait(&acc_full[acc], (it >> 1) & 1);
+                const uint32_t acc = it % kAccBufs;
+                if (static_cast<int>(it & 1) != eg) continue;  // group eg: buffers eg, eg + 2
+                mbar_wait_t(&acc_full[acc], (it / kAccBufs) & 1, pon, w_accfull);
                 tc_fence_after();
 #pragma unroll 1
                 for (int c = 0; c < kNTile / 32; ++c) {
                     uint32_t r[32];
                     TMEM_LD32(lane_base + kAccCol0 + acc * kNTile + c * 32, r);
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    if (a.dbg & 2) {
+                        m = fmaxf(m, __uint_as_float(r[0]) + __uint_as_float(r[31]));
+                        continue;
+                    }
                     const int v0 = n * kNTile + c * 32;
                     const float4* b4 = reinterpret_cast<const float4*>(sbias + v0);
                     f32x2 zz[16];
@@ -306,10 +348,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     const float mn = fmaxf(m, cm);
                     const f32x2 l2 = pk(kLog2e, kLog2e), nml = pk(-mn * kLog2e, -mn * kLog2e);
-                    f32x2 acc2 = pk(0.f, 0.f);
+                    f32x2 accs[4] = {pk(0.f, 0.f), pk(0.f, 0.f), pk(0.f, 0.f), pk(0.f, 0.f)};
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) acc2 = fadd2(acc2, ex2x2(ffma2(zz[j], l2, nml)));
-                    const float2 a2s = upk(acc2);
+                    for (int j = 0; j < 16; ++j) accs[j & 3] = fadd2(accs[j & 3], ex2x2(ffma2(zz[j], l2, nml)));
+                    const float2 a2s = upk(fadd2(fadd2(accs[0], accs[1]), fadd2(accs[2], accs[3])));
                     ssum = fmaf(ssum, ex2((m - mn) * kLog2e), a2s.x + a2s.y);
                     m = mn;
                     float z[32];
@@ -333,6 +375,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc_fence_before();
                 mbar_arrive(&acc_empty[acc]);
             }
+            float4* xb_ = xchg + (tile_local & 1) * kRowsPerTile + rl;
+            if (eg == 1) *xb_ = make_float4(m, ssum, zb, zy);
+            asm volatile("bar.sync 3, 256;" ::: "memory");  // the two epilogue groups
+            ++tile_local;
+            if (eg == 1) continue;
+            {
+                const float4 o = *xb_;
+                const float mm = fmaxf(m, o.x);
+                ssum = (mm == -INFINITY) ? 0.f : ssum * ex2((m - mm) * kLog2e) + o.y * ex2((o.x - mm) * kLog2e);
+                m = mm;
+                zb += o.z;  // the column's owner set it; the other group left 0
+                zy += o.w;
+            }
             if (live) {
                 const float lse = m + lg2(ssum) * kLn2;
                 const int64_t urow = static_cast<int64_t>(b) * cells + rem;
@@ -344,11 +399,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 a.lp_out[diag * (a.Umax + 1) + u] = make_double2(xb, xy);
             }
         }
-    } else if (warp >= 8) {
+    } else if (warp >= 12) {
         // ===== A builders: warp -> (row quarter q, K half kh) =====
         // Build: lane = 16-byte K chunk, so each load instruction reads contiguous bytes of one row (coalesced;
         // consecutive rows mostly share the f row).  Copy to TMEM: thread = row (tcgen05.st lane quarter).
-        const int q = warp & 3, kh = (warp - 8) >> 2;
+        const int q = warp & 3, kh = (warp - 12) >> 2;
         const int rl = q * 32 + lane;
         const int nch = H / 16;            // 16-byte chunks per K half
         const int row_bytes = H * 2;
@@ -401,7 +456,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         const float2 x = unpack_bf16x2(fw[e]), y = unpack_bf16x2(gw[e]);
-                        ow[e] = ok[j] ? pack_bf16x2(tanh_f(x.x + y.x), tanh_f(x.y + y.y)) : 0u;
+                        const float2 h = make_float2(tanh_mufu(x.x + y.x), tanh_mufu(x.y + y.y));
+                        ow[e] = !ok[j] ? 0u : (a.dbg & 1) ? (fw[e] ^ gw[e]) : pack_bf16x2(h.x, h.y);
                     }
                     const int r2 = q * 32 + rows_[j];
                     const int cg = kh * nch + cs[j];
@@ -416,7 +472,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         int64_t tile = blockIdx.x;
         if (tile < ntiles) build(tile);
         for (; tile < ntiles; tile += gridDim.x, ++tl) {
-            if (tl > 0) mbar_wait(a_empty, (tl - 1) & 1);
+            if (tl > 0) mbar_wait_t(a_empty, (tl - 1) & 1, pon, w_aempty);
             tc_fence_after();
             // staging -> TMEM: this thread's row, its K half = nch chunks = nch * 4 columns
             for (int c0 = 0; c0 < nch; c0 += 8) {
@@ -438,6 +494,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (tile + gridDim.x < ntiles) build(tile + gridDim.x);
         }
     }
+    if (pon && lane == 0) {
+        unsigned long long* o = a.prof + static_cast<size_t>(blockIdx.x) * 8;
+        const unsigned long long tot = clock64() - t_start;
+        if (warp == 0) { o[0] = tot; o[1] = w_tma; }
+        if (warp == 1) { o[2] = w_afull; o[3] = w_accempty; o[4] = w_bfull; }
+        if (warp == 4) o[5] = w_accfull;
+        if (warp == 8) o[7] = w_accfull;
+        if (warp == 12) o[6] = w_aempty;
+    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -447,7 +512,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 size_t joint_smem_bytes(int H, int V, int stages) {
     return 1024 + static_cast<size_t>(stages) * kStageBytes + static_cast<size_t>(kRowsPerTile) * H * 2 +
-           static_cast<size_t>(V) * 4 + (2 * kMaxStages + 6) * 8 + 16;
+           static_cast<size_t>(V) * 4 + 2 * kRowsPerTile * 16 + (2 * kMaxStages + 2 + 2 * kAccBufs) * 8 + 16;
 }
 
 using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -524,13 +589,27 @@ extern "C" rnnt_status rnnt_joint_loss_ex(const void* enc, const void* pred, con
     const Workspace w = carve(workspace, B, Tmax, Umax);
     JointArgs args{static_cast<const __nv_bfloat16*>(enc), static_cast<const __nv_bfloat16*>(pred), bias, targets,
                    logit_lens, target_lens, B, Tmax, Umax, H, V, blank,
-                   static_cast<int64_t>(B) * Tmax * (Umax + 1), stages, w.lse, w.lp};
+                   static_cast<int64_t>(B) * Tmax * (Umax + 1), stages, 0, nullptr, w.lse, w.lp};
+    if (const char* e = getenv("RNNT_K6_DEBUG")) args.dbg = atoi(e);
+    args.prof = nullptr;
+    if (args.dbg & 4) cudaMalloc(&args.prof, sizeof(unsigned long long) * 8 * nsm);
     const int64_t ntiles = (args.rows + kRowsPerTile - 1) / kRowsPerTile;
     const int grid = static_cast<int>(std::min<int64_t>(ntiles, nsm));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (record_ev(events, 0, s) != cudaSuccess) return RNNT_ERR_CUDA;
     k6_joint_lse<<<grid, kThreads, smem, s>>>(map, args);
     if (cudaGetLastError() != cudaSuccess || record_ev(events, 1, s) != cudaSuccess) return RNNT_ERR_CUDA;
+    if (args.prof) {  // diagnostics: mean per-CTA cycle split (stderr)
+        unsigned long long h[8 * 148] = {};
+        cudaStreamSynchronize(s);
+        cudaMemcpy(h, args.prof, sizeof(unsigned long long) * 8 * std::min(nsm, 148), cudaMemcpyDeviceToHost);
+        double m[8] = {};
+        for (int c = 0; c < grid && c < 148; ++c)
+            for (int k = 0; k < 8; ++k) m[k] += static_cast<double>(h[c * 8 + k]) / grid;
+        fprintf(stderr, "K6 cycles/CTA total %.0f | tma wait b_empty %.0f | mma wait a_full %.0f acc_empty %.0f b_full %.0f"
+                        " | epi wait acc_full %.0f / %.0f | builder wait a_empty %.0f\n", m[0], m[1], m[2], m[3], m[4], m[5], m[7], m[6]);
+        cudaFree(args.prof);
+    }
     const int vk = (variant < 0) ? kRnnt : (variant == WRNNT_FORCE_FINAL ? kForceFinal : kAllowIgnore);
     Problem p{nullptr, targets, logit_lens, target_lens, B, Tmax, Umax, V, blank, vk, losses, nullptr, nullptr, kF32};
     if (record_ev(events, 2, s) != cudaSuccess || launch_k2_alpha_beta(p, w, s) != cudaSuccess ||
