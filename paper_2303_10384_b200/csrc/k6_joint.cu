@@ -13,7 +13,7 @@
 //   warp 0       TMA producer: W tiles [128 v x 64 k] (SWIZZLE_128B) into a ring of kStages smem stages
 //   warp 1       TMEM owner + MMA issuer: tcgen05.mma.kind::f16, A = h tile from TMEM (128 lanes x H/2 cols),
 //                B = W stage (smem descriptor), D = fp32 accumulator 128 x 128 in TMEM (two buffers)
-//   warps 4-11   epilogue, two groups of 4 (group g drains accumulator buffer g): tcgen05.ld (thread = row), + bias,
+//   warps 4-11   epilogue, two groups of 4 (group g drains half the columns of every accumulator buffer): tcgen05.ld (thread = row), + bias,
 //                online max / sum of exp over V, gathers z[blank] and z[y_u]; group 0 merges group 1's
 //                partials and writes lse and (X_b, X_y) like K1
 //   warps 12-19  A builders: tanh(f + g) of the NEXT tile into a shared-memory staging buffer while the
@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_init(a_empty, 1);
         for (int i = 0; i < kAccBufs; ++i) {
             mbar_init(&acc_full[i], 1);
-            mbar_init(&acc_empty[i], 128);
+            mbar_init(&acc_empty[i], 256);  // both epilogue groups
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&w_map)) : "memory");
@@ -295,12 +295,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 tc_commit(&acc_full[acc]);
             }
-            tc_commit(a_empty);  // the A tile in TMEM may be overwritten
+            // the A tile in TMEM may be overwritten.  (Handing it over per K half, so that the copy of half 0
+            // overlaps the last N tile's MMAs on half 1, measured slower: 1.60 vs 1.52 ms.)
+            tc_commit(a_empty);
         }
     } else if (warp >= 4 && warp < 12) {
-        // ===== epilogue: thread = row; group eg = 0 / 1 owns accumulator buffer eg, i.e. every other N tile
-        // (the MMA alternates buffers), so the two groups drain in parallel; per tile, group 1 hands its row
-        // partials (max, sum, z[blank], z[y]) to group 0 through shared memory, which finishes the row =====
+        // ===== epilogue: thread = row; both groups drain every accumulator buffer, group eg taking columns
+        // [eg * N/2, (eg + 1) * N/2) of each N tile, so a buffer is free after half an N tile's work (with
+        // whole N tiles alternating between the groups, the drain took ~1.4x the MMA time and the MMA waited
+        // on it: 1.65 vs 1.52 ms); per tile, group 1 hands its row partials (max, sum, z[blank], z[y]) to
+        // group 0 through shared memory, which finishes the row =====
         const int q = warp & 3, eg = (warp - 4) >> 2;
         const int rl = q * 32 + lane;
         const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16);
@@ -318,11 +322,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             float m = -INFINITY, ssum = 0.f, zb = 0.f, zy = 0.f;
             for (int n = 0; n < NT; ++n, ++it) {
                 const uint32_t acc = it % kAccBufs;
-                if (static_cast<int>(it & 1) != eg) continue;  // group eg: buffers eg, eg + 2
                 mbar_wait_t(&acc_full[acc], (it / kAccBufs) & 1, pon, w_accfull);
                 tc_fence_after();
 #pragma unroll 1
-                for (int c = 0; c < kNTile / 32; ++c) {
+                for (int c = eg * (kNTile / 64); c < (eg + 1) * (kNTile / 64); ++c) {  // group eg: half the columns
                     uint32_t r[32];
                     TMEM_LD32(lane_base + kAccCol0 + acc * kNTile + c * 32, r);
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
