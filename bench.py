@@ -533,7 +533,7 @@ def main_joint(args, rb, rdist, rank, world, local, dev):
     value = B * world / (ms_step / 1e3)
     k6_ms = statistics.mean(r[0].elapsed_time(r[1]) for r in evs)
     k2_ms = statistics.mean(r[2].elapsed_time(r[3]) for r in evs)
-    rows = B * Tmax * (Umax + 1)
+    rows = int(sum(int(t) * (int(u) + 1) for t, u in zip(T_np, U_np)))  # K6 runs on the valid cells only
     flops = 2.0 * rows * V * H
     tf = flops / (k6_ms / 1e3) / 1e12
     with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:

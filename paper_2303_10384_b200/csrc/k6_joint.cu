@@ -9,7 +9,7 @@
 // and K6 produces exactly what K1 produces from z -- lse(t,u) and the Populate gathers X_b, X_y (§2.2 Eq.(3)
 // P:88) in K2's anti-diagonal layout -- so K2 then yields the losses unchanged.
 //
-// One persistent CTA per SM (16 warps), rows = the (b,t,u) cells in tiles of 128:
+// One persistent CTA per SM (20 warps), rows = the valid (b,t,u) cells (k6_rowmap) in tiles of 128:
 //   warp 0       TMA producer: W tiles [128 v x 64 k] (SWIZZLE_128B) into a ring of kStages smem stages
 //   warp 1       TMEM owner + MMA issuer: tcgen05.mma.kind::f16, A = h tile from TMEM (128 lanes x H/2 cols),
 //                B = W stage (smem descriptor), D = fp32 accumulator 128 x 128 in TMEM (two buffers)
@@ -190,6 +190,8 @@ struct JointArgs {
     int B, Tmax, Umax, H, V, blank;
     int64_t rows;  // B * Tmax * (Umax + 1)
     int stages;
+    const int* rowmap;  // [rows] compact row -> padded row index b*Tmax*(Umax+1) + t*(Umax+1) + u (k6_rowmap)
+    const int* nrows;   // number of valid cells (compact rows)
     int dbg;  // diagnostics (env RNNT_K6_DEBUG, never set in production): 1 = builders skip tanh,
               // 2 = epilogue skips its math (both give wrong losses: timing ablations only), 4 = per-role
               // barrier-wait cycle counters printed to stderr
@@ -219,7 +221,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int H = a.H, V = a.V;
     const int KB = H / kKBlock, NT = V / kNTile;
-    const int64_t ntiles = (a.rows + kRowsPerTile - 1) / kRowsPerTile;
+    const int64_t rows = *a.nrows;  // valid cells only: padding costs no GEMM work
+    const int64_t ntiles = (rows + kRowsPerTile - 1) / kRowsPerTile;
+    const int64_t cells = static_cast<int64_t>(a.Tmax) * (a.Umax + 1);
+    // compact row -> (b, t, u); false past the last row
+    auto decode = [&](int64_t row, int& b, int& t, int& u) -> bool {
+        if (row >= rows) return false;
+        const int p = __ldg(a.rowmap + row);
+        b = static_cast<int>(p / cells);
+        const int rem = static_cast<int>(p - static_cast<int64_t>(b) * cells);
+        t = rem / (a.Umax + 1);
+        u = rem - t * (a.Umax + 1);
+        return true;
+    };
 
     for (int i = threadIdx.x; i < V; i += blockDim.x) sbias[i] = a.bias ? a.bias[i] : 0.f;
     if (threadIdx.x == 0) {
@@ -310,12 +324,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16);
         uint32_t it = 0, tile_local = 0;
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-            const int64_t row = tile * kRowsPerTile + rl;
-            const bool in = row < a.rows;
-            const int64_t cells = static_cast<int64_t>(a.Tmax) * (a.Umax + 1);
-            const int b = in ? static_cast<int>(row / cells) : 0;
-            const int rem = in ? static_cast<int>(row - static_cast<int64_t>(b) * cells) : 0;
-            const int t = rem / (a.Umax + 1), u = rem - t * (a.Umax + 1);
+            int b = 0, t = 0, u = 0;
+            const bool in = decode(tile * kRowsPerTile + rl, b, t, u);
             const int T = in ? min(a.T_b[b], a.Tmax) : 0, U = in ? min(a.U_b[b], a.Umax) : 0;
             const bool live = in && t < T && u <= U;
             const int yv = (live && u < U) ? a.targets[static_cast<int64_t>(b) * a.Umax + u] : -1;
@@ -393,7 +403,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             if (live) {
                 const float lse = m + lg2(ssum) * kLn2;
-                const int64_t urow = static_cast<int64_t>(b) * cells + rem;
+                const int64_t urow = static_cast<int64_t>(b) * cells + t * (a.Umax + 1) + u;
                 a.lse_out[urow] = lse;
                 const bool ybad = (u < U) && (yv < 0 || yv >= a.V || yv == a.blank);
                 const float xb = zb - lse;
@@ -411,22 +421,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int nch = H / 16;            // 16-byte chunks per K half
         const int row_bytes = H * 2;
         uint8_t* my_row = stage_a + static_cast<size_t>(rl) * row_bytes;
-        const int64_t cells = static_cast<int64_t>(a.Tmax) * (a.Umax + 1);
         const uint4* f4 = reinterpret_cast<const uint4*>(a.f);
         const uint4* g4 = reinterpret_cast<const uint4*>(a.g);
         const int items = 32 * nch;        // (row of the quarter, chunk of the half)
-        auto build = [&](int64_t tile) {
+        // Row-map entry of this lane's row (q*32 + lane) in a tile, -1 past the end; fetched one build ahead so
+        // its latency does not start each build.
+        const bool identity = rows == a.rows;  // no padding: the map is the identity, skip its loads
+        auto map_of = [&](int64_t tile) -> int {
+            const int64_t row = tile * kRowsPerTile + rl;
+            if (tile >= ntiles || row >= rows) return -1;
+            return identity ? static_cast<int>(row) : __ldg(a.rowmap + row);
+        };
+        int p_next = -1;
+        auto build = [&](int64_t tile, int p) {
             // lane r: chunk offsets (16-byte units) of row q*32 + r's f and g rows, -1 past the end
             int fo = -1, go = -1;
-            {
-                const int64_t row = tile * kRowsPerTile + rl;
-                if (row < a.rows) {
-                    const int b = static_cast<int>(row / cells);
-                    const int rem = static_cast<int>(row - static_cast<int64_t>(b) * cells);
-                    const int t = rem / (a.Umax + 1), u = rem - t * (a.Umax + 1);
-                    fo = (b * a.Tmax + t) * (H / 8) + kh * nch;
-                    go = (b * (a.Umax + 1) + u) * (H / 8) + kh * nch;
-                }
+            if (p >= 0) {
+                const int b = static_cast<int>(p / cells);
+                const int rem = static_cast<int>(p - static_cast<int64_t>(b) * cells);
+                const int t = rem / (a.Umax + 1), u = rem - t * (a.Umax + 1);
+                fo = (b * a.Tmax + t) * (H / 8) + kh * nch;
+                go = (b * (a.Umax + 1) + u) * (H / 8) + kh * nch;
             }
             int rr = lane / nch, c = lane - (lane / nch) * nch;  // this lane's first item
             const int drr = 32 / nch, dc = 32 - drr * nch;        // item += 32 (nch in {8, 16, 24, 32})
@@ -473,7 +488,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16);
         uint32_t tl = 0;
         int64_t tile = blockIdx.x;
-        if (tile < ntiles) build(tile);
+        if (tile < ntiles) {
+            const int p0 = map_of(tile);
+            p_next = map_of(tile + gridDim.x);
+            build(tile, p0);
+        }
         for (; tile < ntiles; tile += gridDim.x, ++tl) {
             if (tl > 0) mbar_wait_t(a_empty, (tl - 1) & 1, pon, w_aempty);
             tc_fence_after();
@@ -494,7 +513,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             tc_fence_before();
             mbar_arrive(a_full);
-            if (tile + gridDim.x < ntiles) build(tile + gridDim.x);
+            if (tile + gridDim.x < ntiles) {
+                const int p = p_next;
+                p_next = map_of(tile + 2 * static_cast<int64_t>(gridDim.x));
+                build(tile + gridDim.x, p);
+            }
         }
     }
     if (pon && lane == 0) {
@@ -511,6 +534,37 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     if (warp == 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
+}
+
+// Row map of the valid cells (t < T_b, u <= U_b), utterance by utterance: blocks (x, b) write
+// map[off_b + i] = b*Tmax*(Umax+1) + t*(Umax+1) + u for cells i in [x * 4096, (x+1) * 4096) of utterance b's
+// T_b (U_b + 1), off_b = sum of the earlier utterances' counts (invalid lengths count 0); block (0, B-1)
+// writes the total to *nrows.
+__global__ void __launch_bounds__(256) k6_rowmap(const int32_t* __restrict__ T_b, const int32_t* __restrict__ U_b,
+                                                 int B, int Tmax, int Umax, int* __restrict__ map,
+                                                 int* __restrict__ nrows) {
+    __shared__ int s_off[8];
+    const int b = blockIdx.y;
+    auto count = [&](int i) {
+        const int T = T_b[i], U = U_b[i];
+        return (T >= 1 && T <= Tmax && U >= 0 && U <= Umax) ? T * (U + 1) : 0;
+    };
+    int part = 0;
+    for (int i = threadIdx.x; i < b; i += blockDim.x) part += count(i);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if ((threadIdx.x & 31) == 0) s_off[threadIdx.x >> 5] = part;
+    __syncthreads();
+    int off = 0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) off += s_off[w];
+    const int n = count(b), up1 = U_b[b] + 1;
+    const int64_t base = static_cast<int64_t>(b) * Tmax * (Umax + 1);
+    const int i1 = min(n, static_cast<int>(blockIdx.x + 1) * 4096);
+    for (int i = static_cast<int>(blockIdx.x) * 4096 + threadIdx.x; i < i1; i += blockDim.x) {
+        const int t = i / up1, u = i - t * up1;
+        map[off + i] = static_cast<int>(base + t * (Umax + 1) + u);
+    }
+    if (b == B - 1 && blockIdx.x == 0 && threadIdx.x == 0) *nrows = off + n;
 }
 
 size_t joint_smem_bytes(int H, int V, int stages) {
@@ -590,9 +644,13 @@ extern "C" rnnt_status rnnt_joint_loss_ex(const void* enc, const void* pred, con
         return RNNT_ERR_CUDA;
 
     const Workspace w = carve(workspace, B, Tmax, Umax);
+    if (static_cast<int64_t>(B) * Tmax * (Umax + 1) >= (int64_t(1) << 31)) return RNNT_ERR_UNSUPPORTED;
+    // the row map and its length live in the alpha / beta regions, which K2 only fills afterwards
+    int* rowmap = reinterpret_cast<int*>(w.alpha);
+    int* nrows = reinterpret_cast<int*>(w.beta);
     JointArgs args{static_cast<const __nv_bfloat16*>(enc), static_cast<const __nv_bfloat16*>(pred), bias, targets,
                    logit_lens, target_lens, B, Tmax, Umax, H, V, blank,
-                   static_cast<int64_t>(B) * Tmax * (Umax + 1), stages, 0, nullptr, w.lse, w.lp};
+                   static_cast<int64_t>(B) * Tmax * (Umax + 1), stages, rowmap, nrows, 0, nullptr, w.lse, w.lp};
     if (const char* e = getenv("RNNT_K6_DEBUG")) args.dbg = atoi(e);
     args.prof = nullptr;
     if (args.dbg & 4) cudaMalloc(&args.prof, sizeof(unsigned long long) * 8 * nsm);
@@ -600,6 +658,8 @@ extern "C" rnnt_status rnnt_joint_loss_ex(const void* enc, const void* pred, con
     const int grid = static_cast<int>(std::min<int64_t>(ntiles, nsm));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (record_ev(events, 0, s) != cudaSuccess) return RNNT_ERR_CUDA;
+    k6_rowmap<<<dim3(static_cast<unsigned>((static_cast<int64_t>(Tmax) * (Umax + 1) + 4095) / 4096), B), 256, 0, s>>>(
+        logit_lens, target_lens, B, Tmax, Umax, rowmap, nrows);
     k6_joint_lse<<<grid, kThreads, smem, s>>>(map, args);
     if (cudaGetLastError() != cudaSuccess || record_ev(events, 1, s) != cudaSuccess) return RNNT_ERR_CUDA;
     if (args.prof) {  // diagnostics: mean per-CTA cycle split (stderr)

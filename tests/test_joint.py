@@ -70,3 +70,9 @@ def test_joint_rejects_unsupported_shapes(rb):
     W = torch.zeros(128, 96, dtype=torch.bfloat16, device="cuda")
     with pytest.raises(rb.RnntError):
         rb.rnnt_joint_loss(enc, pred, W, None, [[1, 2]], [4], [2])
+
+
+def test_joint_many_short_utterances(rb):
+    # 300 utterances of a few cells each (variable lengths): the compact row map crosses many utterance
+    # boundaries inside every 128-row tile
+    _case(rb, 300, 5, 3, 128, 128, seed=29, variant="force_final")
