@@ -185,6 +185,13 @@ rnnt_status rnnt_joint_loss_ex(const void* enc, const void* pred, const void* we
                                const int32_t* targets, const int32_t* logit_lens, const int32_t* target_lens,
                                int B, int Tmax, int Umax, int H, int V, int blank, int variant, float* losses,
                                void* workspace, size_t workspace_bytes, void* stream, void* const* events);
+/* Viterbi forced alignment (as rnnt_viterbi) on the fused joint's logits: K6 then K4, the logits never written.
+ * Outputs as rnnt_viterbi: best_logp [B] fp32, frames [B][Umax] int32, span [B][2] int32 or NULL. */
+rnnt_status rnnt_joint_viterbi(const void* enc, const void* pred, const void* weight, const float* bias,
+                               const int32_t* targets, const int32_t* logit_lens, const int32_t* target_lens,
+                               int B, int Tmax, int Umax, int H, int V, int blank, int variant, float* best_logp,
+                               int32_t* frames, int32_t* span, void* workspace, size_t workspace_bytes,
+                               void* stream);
 
 const char* rnnt_status_string(rnnt_status status);
 

@@ -23,7 +23,7 @@ VARIANTS = {"rnnt": -1, "force_final": 0, "allow_ignore": 1}
 # Every symbol include/rnnt_b200.h declares.
 EXPORTS = ("rnnt_workspace_bytes", "rnnt_loss", "wrnnt_loss", "rnnt_loss_timed", "rnnt_loss_ex", "rnnt_viterbi",
            "rnnt_loss_sum", "rnnt_lattice_workspace_bytes", "rnnt_lattice_loss",
-           "rnnt_host_buffer_bytes", "rnnt_loss_host", "rnnt_joint_loss", "rnnt_joint_loss_ex",
+           "rnnt_host_buffer_bytes", "rnnt_loss_host", "rnnt_joint_loss", "rnnt_joint_loss_ex", "rnnt_joint_viterbi",
            "rnnt_status_string", "rnnt_version")
 DTYPES = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2}
 
@@ -53,6 +53,7 @@ def _load():
         "rnnt_loss_host": ([P, P, P, P, I, I, I, I, I, I, P, P, P, S, P], I),
         "rnnt_joint_loss": ([P, P, P, P, P, P, P, I, I, I, I, I, I, I, P, P, S, P], I),
         "rnnt_joint_loss_ex": ([P, P, P, P, P, P, P, I, I, I, I, I, I, I, P, P, S, P, P], I),
+        "rnnt_joint_viterbi": ([P, P, P, P, P, P, P, I, I, I, I, I, I, I, P, P, P, P, S, P], I),
         "rnnt_status_string": ([I], ctypes.c_char_p),
         "rnnt_version": ([], ctypes.c_char_p),
     }
@@ -235,6 +236,34 @@ def rnnt_joint_loss(enc, pred, weight, bias, targets, logit_lens, target_lens, b
                                       VARIANTS[variant], _ptr(losses), _ptr(workspace), workspace.numel(),
                                       _stream(stream), ev))
     return losses
+
+
+def rnnt_joint_viterbi(enc, pred, weight, bias, targets, logit_lens, target_lens, blank=0, variant="rnnt",
+                       workspace=None, stream=None):
+    """Viterbi forced alignment on the fused joint's logits (K6 + K4; the logits are never written).  Inputs as
+    rnnt_joint_loss; returns (best_logp fp32 [B], frames int32 [B, Umax], span int32 [B, 2]) as rnnt_viterbi."""
+    for name, x in (("enc", enc), ("pred", pred), ("weight", weight)):
+        if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.bfloat16 and x.is_contiguous()):
+            raise TypeError(f"{name} must be a contiguous CUDA bfloat16 tensor (no CPU fallback)")
+    B, Tmax, H = enc.shape
+    Umax = pred.shape[1] - 1
+    V = weight.shape[0]
+    dev = enc.device
+    if bias is not None:
+        bias = bias.to(device=dev, dtype=torch.float32).contiguous()
+    targets = _as_i32(targets, dev).reshape(B, Umax) if Umax > 0 else None
+    logit_lens = _as_i32(logit_lens, dev)
+    target_lens = _as_i32(target_lens, dev)
+    best = torch.empty(B, dtype=torch.float32, device=dev)
+    frames = torch.empty((B, Umax), dtype=torch.int32, device=dev)
+    span = torch.empty((B, 2), dtype=torch.int32, device=dev)
+    if workspace is None:
+        workspace = torch.empty(max(rnnt_workspace_bytes(B, Tmax, Umax), 1), dtype=torch.uint8, device=dev)
+    _check(library.rnnt_joint_viterbi(_ptr(enc), _ptr(pred), _ptr(weight), _ptr(bias), _ptr(targets),
+                                      _ptr(logit_lens), _ptr(target_lens), B, Tmax, Umax, H, V, int(blank),
+                                      VARIANTS[variant], _ptr(best), _ptr(frames) if Umax > 0 else None, _ptr(span),
+                                      _ptr(workspace), workspace.numel(), _stream(stream)))
+    return best, frames, span
 
 
 def rnnt_lattice_loss(logits, lattices, logit_lens, target_lens, grads=True, losses=None, stream=None):

@@ -603,17 +603,18 @@ cudaError_t record_ev(void* const* events, int i, cudaStream_t s) {
 }
 }  // namespace
 
-extern "C" rnnt_status rnnt_joint_loss_ex(const void* enc, const void* pred, const void* weight, const float* bias,
-                                          const int32_t* targets, const int32_t* logit_lens,
-                                          const int32_t* target_lens, int B, int Tmax, int Umax, int H, int V,
-                                          int blank, int variant, float* losses, void* workspace,
-                                          size_t workspace_bytes, void* stream, void* const* events) {
+namespace {
+// Argument checks, W's tensor map, the row map and K6 (-> lse and the Populate gathers in the workspace):
+// the part the loss and the Viterbi entries share.
+rnnt_status joint_front(const void* enc, const void* pred, const void* weight, const float* bias,
+                        const int32_t* targets, const int32_t* logit_lens, const int32_t* target_lens, int B,
+                        int Tmax, int Umax, int H, int V, int blank, void* workspace, size_t workspace_bytes,
+                        cudaStream_t s, void* const* events) {
     using namespace rnnt;
     if (B < 0 || Tmax < 1 || Umax < 0 || V < 2 || blank < 0 || blank >= V || H < 1) return RNNT_ERR_INVALID_ARG;
-    if (variant < -1 || variant > 1) return RNNT_ERR_INVALID_ARG;
     if (Umax + 1 > kMaxUp1 || H % 128 != 0 || H > 512 || V % kNTile != 0) return RNNT_ERR_UNSUPPORTED;
     if (B == 0) return RNNT_OK;
-    if (!enc || !pred || !weight || !logit_lens || !target_lens || !losses || !workspace) return RNNT_ERR_INVALID_ARG;
+    if (!enc || !pred || !weight || !logit_lens || !target_lens || !workspace) return RNNT_ERR_INVALID_ARG;
     if (Umax > 0 && !targets) return RNNT_ERR_INVALID_ARG;
     if (workspace_bytes < rnnt::workspace_bytes(B, Tmax, Umax)) return RNNT_ERR_WORKSPACE_TOO_SMALL;
     if ((reinterpret_cast<uintptr_t>(enc) | reinterpret_cast<uintptr_t>(pred) | reinterpret_cast<uintptr_t>(weight)) % 16)
@@ -656,7 +657,6 @@ extern "C" rnnt_status rnnt_joint_loss_ex(const void* enc, const void* pred, con
     if (args.dbg & 4) cudaMalloc(&args.prof, sizeof(unsigned long long) * 8 * nsm);
     const int64_t ntiles = (args.rows + kRowsPerTile - 1) / kRowsPerTile;
     const int grid = static_cast<int>(std::min<int64_t>(ntiles, nsm));
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (record_ev(events, 0, s) != cudaSuccess) return RNNT_ERR_CUDA;
     k6_rowmap<<<dim3(static_cast<unsigned>((static_cast<int64_t>(Tmax) * (Umax + 1) + 4095) / 4096), B), 256, 0, s>>>(
         logit_lens, target_lens, B, Tmax, Umax, rowmap, nrows);
@@ -673,12 +673,47 @@ extern "C" rnnt_status rnnt_joint_loss_ex(const void* enc, const void* pred, con
                         " | epi wait acc_full %.0f / %.0f | builder wait a_empty %.0f\n", m[0], m[1], m[2], m[3], m[4], m[5], m[7], m[6]);
         cudaFree(args.prof);
     }
+    return RNNT_OK;
+}
+}  // namespace
+
+extern "C" rnnt_status rnnt_joint_loss_ex(const void* enc, const void* pred, const void* weight, const float* bias,
+                                          const int32_t* targets, const int32_t* logit_lens,
+                                          const int32_t* target_lens, int B, int Tmax, int Umax, int H, int V,
+                                          int blank, int variant, float* losses, void* workspace,
+                                          size_t workspace_bytes, void* stream, void* const* events) {
+    using namespace rnnt;
+    if (variant < -1 || variant > 1) return RNNT_ERR_INVALID_ARG;
+    if (B > 0 && !losses) return RNNT_ERR_INVALID_ARG;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const rnnt_status st = joint_front(enc, pred, weight, bias, targets, logit_lens, target_lens, B, Tmax, Umax, H, V,
+                                       blank, workspace, workspace_bytes, s, events);
+    if (st != RNNT_OK || B == 0) return st;
+    const Workspace w = carve(workspace, B, Tmax, Umax);
     const int vk = (variant < 0) ? kRnnt : (variant == WRNNT_FORCE_FINAL ? kForceFinal : kAllowIgnore);
     Problem p{nullptr, targets, logit_lens, target_lens, B, Tmax, Umax, V, blank, vk, losses, nullptr, nullptr, kF32};
     if (record_ev(events, 2, s) != cudaSuccess || launch_k2_alpha_beta(p, w, s) != cudaSuccess ||
         record_ev(events, 3, s) != cudaSuccess)
         return RNNT_ERR_CUDA;
     return RNNT_OK;
+}
+
+extern "C" rnnt_status rnnt_joint_viterbi(const void* enc, const void* pred, const void* weight, const float* bias,
+                                          const int32_t* targets, const int32_t* logit_lens,
+                                          const int32_t* target_lens, int B, int Tmax, int Umax, int H, int V,
+                                          int blank, int variant, float* best_logp, int32_t* frames, int32_t* span,
+                                          void* workspace, size_t workspace_bytes, void* stream) {
+    using namespace rnnt;
+    if (variant < -1 || variant > 1) return RNNT_ERR_INVALID_ARG;
+    if (B > 0 && (!best_logp || (Umax > 0 && !frames))) return RNNT_ERR_INVALID_ARG;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const rnnt_status st = joint_front(enc, pred, weight, bias, targets, logit_lens, target_lens, B, Tmax, Umax, H, V,
+                                       blank, workspace, workspace_bytes, s, nullptr);
+    if (st != RNNT_OK || B == 0) return st;
+    const Workspace w = carve(workspace, B, Tmax, Umax);
+    const int vk = (variant < 0) ? kRnnt : (variant == WRNNT_FORCE_FINAL ? kForceFinal : kAllowIgnore);
+    Problem p{nullptr, targets, logit_lens, target_lens, B, Tmax, Umax, V, blank, vk, nullptr, nullptr, nullptr, kF32};
+    return launch_k4_viterbi(p, w, best_logp, frames, span, s) == cudaSuccess ? RNNT_OK : RNNT_ERR_CUDA;
 }
 
 extern "C" rnnt_status rnnt_joint_loss(const void* enc, const void* pred, const void* weight, const float* bias,

@@ -76,3 +76,30 @@ def test_joint_many_short_utterances(rb):
     # 300 utterances of a few cells each (variable lengths): the compact row map crosses many utterance
     # boundaries inside every 128-row tile
     _case(rb, 300, 5, 3, 128, 128, seed=29, variant="force_final")
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_joint_viterbi_matches_oracle(rb, variant):
+    """rnnt_joint_viterbi (K6 + K4) vs the Viterbi oracle on the oracle-built joint logits: same best score
+    (1e-5 relative) and the same alignment (reading R21 tie-break; random logits have no ties)."""
+    import oracle
+    B, T, U, H, V = 3, 40, 12, 256, 256
+    cfg = workloads.random_config(B, T, U, V, seed=31, variant=variant)
+    T_b, U_b = workloads.lengths(cfg)
+    y = workloads.targets(cfg, U_b)
+    enc, pred, W, b = workloads.joint_inputs(B, T, U, H, V, seed=31)
+    best, frames, span = rb.rnnt_joint_viterbi(enc.cuda(), pred.cuda(), W.cuda(), b.cuda(), y, T_b, U_b, 0, variant)
+    torch.cuda.synchronize()
+    z = oj.joint_logits(enc.double().numpy(), pred.double().numpy(), W.double().numpy(),
+                        b.double().numpy()).astype(np.float32)
+    from tests.test_viterbi import _path_score
+    for i in range(B):
+        T, U = int(T_b[i]), int(U_b[i])
+        ref_best, ref_frames, ref_span = oracle.viterbi(z[i], T, U, y[i][:U], 0, variant)
+        assert abs(best[i].item() - ref_best) <= 1e-5 * max(abs(ref_best), 1.0)
+        f = frames[i, :U].cpu().numpy()
+        sp = tuple(span[i].cpu().numpy().tolist())
+        if f.tolist() != list(ref_frames) or sp != tuple(ref_span):
+            # a near-tie under the GPU's fp32 accumulation: its alignment must score as well, to rounding
+            sg = _path_score(z[i], y[i], T, U, 0, f, sp, variant)
+            assert abs(sg - ref_best) <= 1e-5 * max(abs(ref_best), 1.0)
