@@ -41,7 +41,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--config", default="c3")
+    ap.add_argument("--config", default="c3", help="c1..c5 (BASELINE.json), or p124 (the paper's own benchmark shapes, P:124)")
     ap.add_argument("--variant", default=None)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -205,7 +205,7 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", 0))
     if rank != 0:
         return
-    cfg = workloads.CONFIGS[args.config]
+    cfg = {**workloads.CONFIGS, **workloads.EXTRA_CONFIGS}[args.config]
     variant = args.variant or cfg.variant
     threads = oracle_threads(cfg, args.cpu_threads)
     import oracle
@@ -247,7 +247,7 @@ def main():
     if args.mode == "joint":
         return main_joint(args, rb, rdist, rank, world, local, dev)
 
-    base = workloads.CONFIGS[args.config]
+    base = {**workloads.CONFIGS, **workloads.EXTRA_CONFIGS}[args.config]
     variant = args.variant or base.variant
     gcfg = dataclasses.replace(base, B=base.B_per_gpu * world)   # weak scaling: B per GPU fixed
     b_ids = rdist.contiguous_shard(gcfg.B, rank, world)
@@ -465,7 +465,7 @@ def main():
 def main_joint(args, rb, rdist, rank, world, local, dev):
     """utterances/s of the fused joint network + loss forward (rnnt_joint_loss: K6 tcgen05 GEMM with the
     log-softmax / Populate epilogue, then K2), inputs = Encoder / Predictor embeddings of size H."""
-    base = workloads.CONFIGS[args.config]
+    base = {**workloads.CONFIGS, **workloads.EXTRA_CONFIGS}[args.config]
     variant = args.variant or base.variant
     gcfg = dataclasses.replace(base, B=base.B_per_gpu * world)
     b_ids = rdist.contiguous_shard(gcfg.B, rank, world)

@@ -21,7 +21,7 @@
 // TMEM: A [0, 256) columns, kAccBufs = 2 accumulators of 128 columns in [256, 512).  (N = 64 with four
 // buffers was measured slower: 2.20 vs 1.77 ms at c3 / H = 512 -- the narrower MMAs lose more than the
 // deeper buffering gains.)  mbarriers link the roles.
-// Constraints: H % 128 == 0, H <= 512; V % 128 == 0.
+// Constraints: H % 128 == 0, H <= 512 (any V: the last N tile's missing columns are masked).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -208,7 +208,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* wst = base;
     uint8_t* stage_a = wst + static_cast<size_t>(a.stages) * kStageBytes;
     float* sbias = reinterpret_cast<float*>(stage_a + static_cast<size_t>(kRowsPerTile) * a.H * 2);
-    float4* xchg = reinterpret_cast<float4*>(sbias + a.V);  // [2][128] epilogue group 1 -> group 0 partials
+    const int Vp = (a.V + kNTile - 1) / kNTile * kNTile;  // V rounded up to whole N tiles
+    float4* xchg = reinterpret_cast<float4*>(sbias + Vp);  // [2][128] epilogue group 1 -> group 0 partials
     uint64_t* bars = reinterpret_cast<uint64_t*>(xchg + 2 * kRowsPerTile);
     uint64_t* b_full = bars;                   // [stages]
     uint64_t* b_empty = bars + kMaxStages;     // [stages]
@@ -220,7 +221,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int H = a.H, V = a.V;
-    const int KB = H / kKBlock, NT = V / kNTile;
+    const int KB = H / kKBlock, NT = Vp / kNTile;
     const int64_t rows = *a.nrows;  // valid cells only: padding costs no GEMM work
     const int64_t ntiles = (rows + kRowsPerTile - 1) / kRowsPerTile;
     const int64_t cells = static_cast<int64_t>(a.Tmax) * (a.Umax + 1);
@@ -235,7 +236,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         return true;
     };
 
-    for (int i = threadIdx.x; i < V; i += blockDim.x) sbias[i] = a.bias ? a.bias[i] : 0.f;
+    // Columns past V (the last N tile's tail): TMA zero-fills W's missing rows, and a -inf bias makes those
+    // logits -inf, i.e. absent from the max and the sum (V need not be a multiple of the tile).
+    for (int i = threadIdx.x; i < Vp; i += blockDim.x) sbias[i] = i < V ? (a.bias ? a.bias[i] : 0.f) : -INFINITY;
     if (threadIdx.x == 0) {
         for (int s = 0; s < a.stages; ++s) {
             mbar_init(&b_full[s], 1);
@@ -360,6 +363,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         cm = max3(cm, v.x, v.y);
                     }
                     const float mn = fmaxf(m, cm);
+                    if (mn == -INFINITY) continue;  // nothing finite yet (a chunk of masked tail columns)
                     const f32x2 l2 = pk(kLog2e, kLog2e), nml = pk(-mn * kLog2e, -mn * kLog2e);
                     f32x2 accs[4] = {pk(0.f, 0.f), pk(0.f, 0.f), pk(0.f, 0.f), pk(0.f, 0.f)};
 #pragma unroll
@@ -569,7 +573,8 @@ __global__ void __launch_bounds__(256) k6_rowmap(const int32_t* __restrict__ T_b
 
 size_t joint_smem_bytes(int H, int V, int stages) {
     return 1024 + static_cast<size_t>(stages) * kStageBytes + static_cast<size_t>(kRowsPerTile) * H * 2 +
-           static_cast<size_t>(V) * 4 + 2 * kRowsPerTile * 16 + (2 * kMaxStages + 2 + 2 * kAccBufs) * 8 + 16;
+           static_cast<size_t>((V + kNTile - 1) / kNTile * kNTile) * 4 + 2 * kRowsPerTile * 16 +
+           (2 * kMaxStages + 2 + 2 * kAccBufs) * 8 + 16;
 }
 
 using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -612,7 +617,7 @@ rnnt_status joint_front(const void* enc, const void* pred, const void* weight, c
                         cudaStream_t s, void* const* events) {
     using namespace rnnt;
     if (B < 0 || Tmax < 1 || Umax < 0 || V < 2 || blank < 0 || blank >= V || H < 1) return RNNT_ERR_INVALID_ARG;
-    if (Umax + 1 > kMaxUp1 || H % 128 != 0 || H > 512 || V % kNTile != 0) return RNNT_ERR_UNSUPPORTED;
+    if (Umax + 1 > kMaxUp1 || H % 128 != 0 || H > 512) return RNNT_ERR_UNSUPPORTED;
     if (B == 0) return RNNT_OK;
     if (!enc || !pred || !weight || !logit_lens || !target_lens || !workspace) return RNNT_ERR_INVALID_ARG;
     if (Umax > 0 && !targets) return RNNT_ERR_INVALID_ARG;

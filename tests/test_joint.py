@@ -37,7 +37,8 @@ def _case(rb, B, T, U, H, V, seed, variant, blank=0, variable=True, bias=True):
 
 
 @pytest.mark.parametrize("variant", VARIANTS)
-@pytest.mark.parametrize("shape", [(2, 9, 4, 128, 128), (3, 37, 11, 256, 384), (2, 50, 20, 512, 1024)],
+@pytest.mark.parametrize("shape", [(2, 9, 4, 128, 128), (3, 37, 11, 256, 384), (2, 50, 20, 512, 1024),
+                                   (2, 30, 9, 512, 500), (2, 11, 5, 128, 37)],
                          ids=lambda s: "B{}_T{}_U{}_H{}_V{}".format(*s))
 def test_joint_loss_matches_oracle(rb, shape, variant):
     B, T, U, H, V = shape

@@ -68,6 +68,13 @@ CONFIGS = {
                  variant="force_final", drop=(0.2, 0.5)),
     "c5": Config("B256_T1000_U200_V4096", B=256, Tmax=1000, Umax=200, V=4096, logit_seed=5000, per_gpu=32),
 }
+# Not a BASELINE config: the paper's own loss benchmark (§4.1, read per DESIGN.md c15): batch 30,
+# vocabulary 500, time 101..433 and units 73..92 across the batch; with Encoder/Predictor embeddings of 512 it
+# is the fused joint's natural workload (bench --mode joint --config p124).
+EXTRA_CONFIGS = {
+    "p124": Config("B30_T433_U92_V500_var", B=30, Tmax=433, Umax=92, V=500, variable_lengths=True, t_lo=101,
+                   u_lo=73, logit_seed=1240, len_seed=124),
+}
 
 
 def lengths(cfg: Config):
