@@ -24,6 +24,7 @@ VARIANTS = {"rnnt": -1, "force_final": 0, "allow_ignore": 1}
 EXPORTS = ("rnnt_workspace_bytes", "rnnt_loss", "wrnnt_loss", "rnnt_loss_timed", "rnnt_loss_ex", "rnnt_viterbi",
            "rnnt_loss_sum", "rnnt_lattice_workspace_bytes", "rnnt_lattice_loss",
            "rnnt_host_buffer_bytes", "rnnt_loss_host", "rnnt_joint_loss", "rnnt_joint_loss_ex", "rnnt_joint_viterbi",
+           "rnnt_joint_grad_workspace_bytes", "rnnt_joint_loss_grad",
            "rnnt_status_string", "rnnt_version")
 DTYPES = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2}
 
@@ -54,6 +55,8 @@ def _load():
         "rnnt_joint_loss": ([P, P, P, P, P, P, P, I, I, I, I, I, I, I, P, P, S, P], I),
         "rnnt_joint_loss_ex": ([P, P, P, P, P, P, P, I, I, I, I, I, I, I, P, P, S, P, P], I),
         "rnnt_joint_viterbi": ([P, P, P, P, P, P, P, I, I, I, I, I, I, I, P, P, P, P, S, P], I),
+        "rnnt_joint_grad_workspace_bytes": ([I, I, I, I, I], S),
+        "rnnt_joint_loss_grad": ([P, P, P, P, P, P, P, I, I, I, I, I, I, I, P, P, P, P, P, P, S, P], I),
         "rnnt_status_string": ([I], ctypes.c_char_p),
         "rnnt_version": ([], ctypes.c_char_p),
     }
@@ -236,6 +239,38 @@ def rnnt_joint_loss(enc, pred, weight, bias, targets, logit_lens, target_lens, b
                                       VARIANTS[variant], _ptr(losses), _ptr(workspace), workspace.numel(),
                                       _stream(stream), ev))
     return losses
+
+
+def rnnt_joint_loss_grad(enc, pred, weight, bias, targets, logit_lens, target_lens, blank=0, variant="rnnt",
+                         workspace=None, stream=None):
+    """Training step of the fused joint (NEXT-4 backward): returns (losses [B], d_enc [B, Tmax, H],
+    d_pred [B, Umax+1, H], d_weight [V, H], d_bias [V]), the gradients (fp32) of sum(losses).  Inputs as
+    rnnt_joint_loss; bias may be None (then d_bias is still returned, for a zero bias)."""
+    for name, x in (("enc", enc), ("pred", pred), ("weight", weight)):
+        if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.bfloat16 and x.is_contiguous()):
+            raise TypeError(f"{name} must be a contiguous CUDA bfloat16 tensor (no CPU fallback)")
+    B, Tmax, H = enc.shape
+    Umax = pred.shape[1] - 1
+    V = weight.shape[0]
+    dev = enc.device
+    if bias is not None:
+        bias = bias.to(device=dev, dtype=torch.float32).contiguous()
+    targets = _as_i32(targets, dev).reshape(B, Umax) if Umax > 0 else None
+    logit_lens = _as_i32(logit_lens, dev)
+    target_lens = _as_i32(target_lens, dev)
+    losses = torch.empty(B, dtype=torch.float32, device=dev)
+    d_enc = torch.empty((B, Tmax, H), dtype=torch.float32, device=dev)
+    d_pred = torch.empty((B, Umax + 1, H), dtype=torch.float32, device=dev)
+    d_weight = torch.empty((V, H), dtype=torch.float32, device=dev)
+    d_bias = torch.empty(V, dtype=torch.float32, device=dev)
+    if workspace is None:
+        need = int(library.rnnt_joint_grad_workspace_bytes(B, Tmax, Umax, H, V))
+        workspace = torch.empty(max(need, 1), dtype=torch.uint8, device=dev)
+    _check(library.rnnt_joint_loss_grad(_ptr(enc), _ptr(pred), _ptr(weight), _ptr(bias), _ptr(targets),
+                                        _ptr(logit_lens), _ptr(target_lens), B, Tmax, Umax, H, V, int(blank),
+                                        VARIANTS[variant], _ptr(losses), _ptr(d_enc), _ptr(d_pred), _ptr(d_weight),
+                                        _ptr(d_bias), _ptr(workspace), workspace.numel(), _stream(stream)))
+    return losses, d_enc, d_pred, d_weight, d_bias
 
 
 def rnnt_joint_viterbi(enc, pred, weight, bias, targets, logit_lens, target_lens, blank=0, variant="rnnt",

@@ -1,0 +1,35 @@
+// joint.cuh -- internal interface between the fused joint's forward / first backward pass (k6_joint.cu) and
+// the rest of its backward (k7_joint_grad.cu).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "rnnt_b200.h"
+
+namespace rnnt {
+
+// Backward-pass inputs / outputs of K6<true>: the forward's lse / lp and K2's alpha / beta / logP in; dz
+// ([rows][Vp] bf16, Vp = V rounded up to 128) and h ([rows][H] bf16) out, rows = the compact valid cells.
+struct GradIO {
+    const float* lse;
+    const double2* lp;
+    const double* alpha;
+    const double* beta;
+    const double* logp;
+    __nv_bfloat16* dz;
+    __nv_bfloat16* h;
+};
+
+// Argument checks, W's tensor map, (optionally) the compact row map, and K6: the forward (-> lse and the
+// Populate gathers in the workspace) when g == nullptr, the backward's first pass (-> dz, h) otherwise.
+// rowmap / nrows: where the row map lives (nullptr: the workspace's alpha / beta regions, free until K2).
+rnnt_status joint_front(const void* enc, const void* pred, const void* weight, const float* bias,
+                        const int32_t* targets, const int32_t* logit_lens, const int32_t* target_lens, int B,
+                        int Tmax, int Umax, int H, int V, int blank, void* workspace, size_t workspace_bytes,
+                        cudaStream_t s, void* const* events, int* rowmap = nullptr, int* nrows = nullptr,
+                        bool make_map = true, const GradIO* g = nullptr);
+
+constexpr int kJointVTile = 128;  // K6's N tile: dz rows are padded to a multiple of it
+
+}  // namespace rnnt

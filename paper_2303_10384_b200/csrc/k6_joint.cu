@@ -31,6 +31,7 @@
 
 #include "common.cuh"
 #include "elem.cuh"
+#include "joint.cuh"
 #include "rnnt_b200.h"
 
 namespace rnnt {
@@ -212,8 +213,21 @@ struct JointArgs {
     unsigned long long* prof;
     float* lse_out;
     double2* lp_out;
+    // backward pass (kGrad): the forward's lse / lp and K2's alpha / beta / logP in, dz and h out
+    const float* lse_in;
+    const double2* lp_in;
+    const double* alpha;
+    const double* beta;
+    const double* logp;
+    __nv_bfloat16* dz_out;  // [rows][Vp] row-major, Vp = V rounded up to whole N tiles (tail columns 0)
+    __nv_bfloat16* h_out;   // [rows][H]
 };
 
+// kGrad = false: the forward (lse + gathers).  kGrad = true: the backward's first pass -- the same GEMM
+// recomputes z and the epilogue forms dz = softmax(z) (occ_b + occ_y) - [v = blank] occ_b - [v = y] occ_y
+// (K3's formula, with the forward's lse and K2's alpha / beta), stored in bf16 for the two backward GEMMs;
+// the builders also store h.
+template <bool kGrad>
 __global__ void __launch_bounds__(kThreads, 1)
     k6_joint_lse(const __grid_constant__ CUtensorMap w_map, const JointArgs a) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -346,6 +360,83 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int T = in ? min(a.T_b[b], a.Tmax) : 0, U = in ? min(a.U_b[b], a.Umax) : 0;
             const bool live = in && t < T && u <= U;
             const int yv = (live && u < U) ? a.targets[static_cast<int64_t>(b) * a.Umax + u] : -1;
+            if constexpr (kGrad) {
+                // Per-row occupancies of the two scored arcs leaving (t,u), as K3 (k3_grad.cu): padded rows,
+                // invalid or no-path utterances (logP not finite) get dz = 0.
+                const int64_t crow = tile * kRowsPerTile + rl;  // compact row: dz / h row index
+                const double lP = in ? a.logp[b] : 0.0;
+                const bool gl = live && isfinite(lP);
+                float gam = 0.f, sb = 0.f, sy = 0.f, lsel = INFINITY;
+                int gy = -1;
+                if (gl) {
+                    const int Up1 = a.Umax + 1;
+                    const int64_t dcell = (static_cast<int64_t>(b) * (a.Tmax + a.Umax) + (t + u)) * Up1 + u;
+                    const float lse = a.lse_in[static_cast<int64_t>(b) * cells + t * Up1 + u];
+                    const double2 l = a.lp_in[dcell];
+                    const double al = a.alpha[dcell];
+                    if (t < T - 1)
+                        sb = __expf(static_cast<float>(al + l.x + a.beta[dcell + Up1] - lP));
+                    else if (u == U)
+                        sb = __expf(static_cast<float>(al + l.x - lP));
+                    if (u < U) {
+                        sy = __expf(static_cast<float>(al + l.y + a.beta[dcell + Up1 + 1] - lP));
+                        gy = yv;
+                    }
+                    gam = sb + sy;
+                    lsel = (lse == -INFINITY) ? INFINITY : lse * kLog2e;  // an all -inf row: p = 0
+                }
+                const f32x2 l2 = pk(kLog2e, kLog2e), nl = pk(-lsel, -lsel), g2 = pk(gam, gam);
+                for (int n = 0; n < NT; ++n, ++it) {
+                    const uint32_t acc = it % kAccBufs;
+                    mbar_wait_t(&acc_full[acc], (it / kAccBufs) & 1, pon, w_accfull);
+                    tc_fence_after();
+#pragma unroll 1
+                    for (int c = eg * (kNTile / 64); c < (eg + 1) * (kNTile / 64); ++c) {
+                        uint32_t r[32];
+                        TMEM_LD32(lane_base + kAccCol0 + acc * kNTile + c * 32, r);
+                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                        if (crow >= rows) continue;
+                        const int v0 = n * kNTile + c * 32;
+                        const float4* b4 = reinterpret_cast<const float4*>(sbias + v0);
+                        float g[32];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const float4 bb = b4[j];
+                            const f32x2 z0 = fadd2(pk(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1])), pk(bb.x, bb.y));
+                            const f32x2 z1 = fadd2(pk(__uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3])), pk(bb.z, bb.w));
+                            const float2 p0 = upk(fmul2(ex2x2(ffma2(z0, l2, nl)), g2));
+                            const float2 p1 = upk(fmul2(ex2x2(ffma2(z1, l2, nl)), g2));
+                            g[4 * j] = p0.x;
+                            g[4 * j + 1] = p0.y;
+                            g[4 * j + 2] = p1.x;
+                            g[4 * j + 3] = p1.y;
+                        }
+                        if (static_cast<unsigned>(a.blank - v0) < 32u) {  // the arcs' own logits
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                if (v0 + j == a.blank) g[j] -= sb;
+                        }
+                        if (static_cast<unsigned>(gy - v0) < 32u) {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                if (v0 + j == gy) g[j] -= sy;
+                        }
+                        uint4* dst = reinterpret_cast<uint4*>(a.dz_out + crow * NT * kNTile + v0);
+#pragma unroll
+                        for (int q4 = 0; q4 < 4; ++q4) {
+                            uint4 o;
+                            o.x = gl ? pack_bf16x2(g[8 * q4 + 0], g[8 * q4 + 1]) : 0u;
+                            o.y = gl ? pack_bf16x2(g[8 * q4 + 2], g[8 * q4 + 3]) : 0u;
+                            o.z = gl ? pack_bf16x2(g[8 * q4 + 4], g[8 * q4 + 5]) : 0u;
+                            o.w = gl ? pack_bf16x2(g[8 * q4 + 6], g[8 * q4 + 7]) : 0u;
+                            dst[q4] = o;
+                        }
+                    }
+                    tc_fence_before();
+                    mbar_arrive(&acc_empty[acc]);
+                }
+                continue;
+            }
             float m = -INFINITY, ssum = 0.f, zb = 0.f, zy = 0.f;
             for (int n = 0; n < NT; ++n, ++it) {
                 const uint32_t acc = it % kAccBufs;
@@ -500,6 +591,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int cg = kh * nch + cs[j];
                     *reinterpret_cast<uint4*>(stage_a + static_cast<size_t>(r2) * row_bytes + ((cg ^ (r2 & 7)) << 4)) =
                         make_uint4(ow[0], ow[1], ow[2], ow[3]);
+                    if constexpr (kGrad) {  // h for the dW GEMM, compact rows (coalesced: lane = chunk)
+                        const int64_t crow = tile * kRowsPerTile + r2;
+                        if (ok[j]) reinterpret_cast<uint4*>(a.h_out + crow * H)[cg] = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+                    }
                 }
             }
             __syncwarp();  // each thread copies its own row, written by the whole warp
@@ -623,14 +718,16 @@ cudaError_t record_ev(void* const* events, int i, cudaStream_t s) {
 }
 }  // namespace
 
-namespace {
-// Argument checks, W's tensor map, the row map and K6 (-> lse and the Populate gathers in the workspace):
-// the part the loss and the Viterbi entries share.
+namespace rnnt {
+// Argument checks, W's tensor map, (optionally) the row map, and K6: the forward (-> lse and the Populate
+// gathers in the workspace) when g == nullptr, the backward's first pass (-> dz, h) otherwise.  Shared by
+// the loss, Viterbi and gradient entries.  rowmap / nrows: where the compact row map lives (nullptr: the
+// alpha / beta regions of the workspace, free until K2 runs).
 rnnt_status joint_front(const void* enc, const void* pred, const void* weight, const float* bias,
                         const int32_t* targets, const int32_t* logit_lens, const int32_t* target_lens, int B,
                         int Tmax, int Umax, int H, int V, int blank, void* workspace, size_t workspace_bytes,
-                        cudaStream_t s, void* const* events) {
-    using namespace rnnt;
+                        cudaStream_t s, void* const* events, int* rowmap, int* nrows, bool make_map,
+                        const GradIO* g) {
     if (B < 0 || Tmax < 1 || Umax < 0 || V < 2 || blank < 0 || blank >= V || H < 1) return RNNT_ERR_INVALID_ARG;
     if (Umax + 1 > kMaxUp1 || H % 128 != 0 || H > 512) return RNNT_ERR_UNSUPPORTED;
     if (B == 0) return RNNT_OK;
@@ -660,27 +757,39 @@ rnnt_status joint_front(const void* enc, const void* pred, const void* weight, c
     while (stages > 2 && joint_smem_bytes(H, V, stages) > static_cast<size_t>(smem_max)) --stages;
     const size_t smem = joint_smem_bytes(H, V, stages);
     if (smem > static_cast<size_t>(smem_max)) return RNNT_ERR_UNSUPPORTED;
-    if (cudaFuncSetAttribute(k6_joint_lse, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
-        cudaSuccess)
+    auto kern = g ? k6_joint_lse<true> : k6_joint_lse<false>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
         return RNNT_ERR_CUDA;
 
     const Workspace w = carve(workspace, B, Tmax, Umax);
     if (static_cast<int64_t>(B) * Tmax * (Umax + 1) >= (int64_t(1) << 31)) return RNNT_ERR_UNSUPPORTED;
-    // the row map and its length live in the alpha / beta regions, which K2 only fills afterwards
-    int* rowmap = reinterpret_cast<int*>(w.alpha);
-    int* nrows = reinterpret_cast<int*>(w.beta);
+    if (!rowmap) {  // the row map and its length in the alpha / beta regions, which K2 only fills afterwards
+        rowmap = reinterpret_cast<int*>(w.alpha);
+        nrows = reinterpret_cast<int*>(w.beta);
+    }
     JointArgs args{static_cast<const __nv_bfloat16*>(enc), static_cast<const __nv_bfloat16*>(pred), bias, targets,
                    logit_lens, target_lens, B, Tmax, Umax, H, V, blank,
-                   static_cast<int64_t>(B) * Tmax * (Umax + 1), stages, rowmap, nrows, 0, nullptr, w.lse, w.lp};
+                   static_cast<int64_t>(B) * Tmax * (Umax + 1), stages, rowmap, nrows, 0, nullptr, w.lse, w.lp,
+                   nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    if (g) {
+        args.lse_in = g->lse;
+        args.lp_in = g->lp;
+        args.alpha = g->alpha;
+        args.beta = g->beta;
+        args.logp = g->logp;
+        args.dz_out = g->dz;
+        args.h_out = g->h;
+    }
     if (const char* e = getenv("RNNT_K6_DEBUG")) args.dbg = atoi(e);
     args.prof = nullptr;
     if (args.dbg & 4) cudaMalloc(&args.prof, sizeof(unsigned long long) * 8 * nsm);
     const int64_t ntiles = (args.rows + kRowsPerTile - 1) / kRowsPerTile;
     const int grid = static_cast<int>(std::min<int64_t>(ntiles, nsm));
     if (record_ev(events, 0, s) != cudaSuccess) return RNNT_ERR_CUDA;
-    k6_rowmap<<<dim3(static_cast<unsigned>((static_cast<int64_t>(Tmax) * (Umax + 1) + 4095) / 4096), B), 256, 0, s>>>(
-        logit_lens, target_lens, B, Tmax, Umax, rowmap, nrows);
-    k6_joint_lse<<<grid, kThreads, smem, s>>>(map, args);
+    if (make_map)
+        k6_rowmap<<<dim3(static_cast<unsigned>((static_cast<int64_t>(Tmax) * (Umax + 1) + 4095) / 4096), B), 256, 0,
+                    s>>>(logit_lens, target_lens, B, Tmax, Umax, rowmap, nrows);
+    kern<<<grid, kThreads, smem, s>>>(map, args);
     if (cudaGetLastError() != cudaSuccess || record_ev(events, 1, s) != cudaSuccess) return RNNT_ERR_CUDA;
     if (args.prof) {  // diagnostics: mean per-CTA cycle split (stderr)
         unsigned long long h[8 * 148] = {};
@@ -695,7 +804,7 @@ rnnt_status joint_front(const void* enc, const void* pred, const void* weight, c
     }
     return RNNT_OK;
 }
-}  // namespace
+}  // namespace rnnt
 
 extern "C" rnnt_status rnnt_joint_loss_ex(const void* enc, const void* pred, const void* weight, const float* bias,
                                           const int32_t* targets, const int32_t* logit_lens,

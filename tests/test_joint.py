@@ -104,3 +104,26 @@ def test_joint_viterbi_matches_oracle(rb, variant):
             # a near-tie under the GPU's fp32 accumulation: its alignment must score as well, to rounding
             sg = _path_score(z[i], y[i], T, U, 0, f, sp, variant)
             assert abs(sg - ref_best) <= 1e-5 * max(abs(ref_best), 1.0)
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("shape", [(2, 9, 4, 128, 128), (3, 30, 10, 256, 500), (2, 40, 16, 512, 1024)],
+                         ids=lambda s: "B{}_T{}_U{}_H{}_V{}".format(*s))
+def test_joint_loss_grad_matches_oracle(rb, shape, variant):
+    """rnnt_joint_loss_grad (K6, K2, K6<grad>, cuBLAS, K7) vs the oracle's chain rule under reading R23.
+    Bars: losses 1e-5 relative; each gradient within 2e-3 of its largest entry (bf16 dz: an element whose
+    GPU value sits within ~1e-6 of a bf16 rounding boundary may round the other way; fp32 vs fp64 sums)."""
+    B, T, U, H, V = shape
+    cfg = workloads.random_config(B, T, U, V, seed=sum(shape) % 89 + 7, variant=variant)
+    T_b, U_b = workloads.lengths(cfg)
+    y = workloads.targets(cfg, U_b)
+    enc, pred, W, b = workloads.joint_inputs(B, T, U, H, V, seed=sum(shape) % 89 + 7)
+    out = rb.rnnt_joint_loss_grad(enc.cuda(), pred.cuda(), W.cuda(), b.cuda(), y, T_b, U_b, 0, variant)
+    torch.cuda.synchronize()
+    ref = oj.joint_loss_and_grads(enc.double().numpy(), pred.double().numpy(), W.double().numpy(),
+                                  b.double().numpy(), y, T_b, U_b, 0, variant)
+    l = out[0].cpu().numpy().astype(np.float64)
+    assert (np.abs(l - ref[0]) / np.maximum(np.abs(ref[0]), 1.0)).max() <= 1e-5
+    for name, mine, r in zip(("d_enc", "d_pred", "d_weight", "d_bias"), out[1:], ref[1:]):
+        err = np.abs(mine.cpu().numpy().astype(np.float64) - r).max()
+        assert err <= 2e-3 * np.abs(r).max(), (name, err, np.abs(r).max())
