@@ -51,11 +51,12 @@ def parse():
     ap.add_argument("--dtype", default="f32", choices=["f32", "bf16", "f16"],
                     help="storage type of logits/grads (arithmetic is fp32/fp64 either way); the BASELINE "
                          "metric is quoted on f32")
-    ap.add_argument("--mode", default="loss_grad", choices=["loss_grad", "loss", "viterbi", "lattice", "joint"],
+    ap.add_argument("--mode", default="loss_grad", choices=["loss_grad", "loss", "viterbi", "lattice", "joint", "joint_grad"],
                     help="loss_grad: the BASELINE metric; loss: losses only (K1+K2); viterbi: forced alignment "
                          "(K1+K4) -- SURVEY 8(f) NEXT-2; lattice: the same loss+grad through the generic "
                          "acyclic-lattice engine on explicit Grid/W lattices -- NEXT-3; joint: the fused joint "
-                         "network + loss forward from Encoder/Predictor embeddings (H=--hidden) -- NEXT-4")
+                         "network + loss forward from Encoder/Predictor embeddings (H=--hidden) -- NEXT-4; "
+                         "joint_grad: the fused joint's training step (loss + gradients w.r.t. enc, pred, W, bias)")
     ap.add_argument("--hidden", type=int, default=512, help="--mode joint: embedding size H (P:124: 512)")
     ap.add_argument("--eager", action="store_true",
                     help="launch the K timed steps one by one from Python instead of replaying them as one CUDA graph "
@@ -244,7 +245,7 @@ def main():
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if args.mode == "joint":
+    if args.mode in ("joint", "joint_grad"):
         return main_joint(args, rb, rdist, rank, world, local, dev)
 
     base = {**workloads.CONFIGS, **workloads.EXTRA_CONFIGS}[args.config]
@@ -483,7 +484,15 @@ def main_joint(args, rb, rdist, rank, world, local, dev):
     U_b = torch.from_numpy(U_np).to(dev)
     losses = torch.empty(B, dtype=torch.float32, device=dev)
     loss_sum = torch.empty((), dtype=torch.float64, device=dev)
-    workspace = torch.empty(rb.rnnt_workspace_bytes(B, Tmax, Umax), dtype=torch.uint8, device=dev)
+    grad = args.mode == "joint_grad"
+    if grad:
+        H_ = enc.shape[2]
+        outs = (losses, torch.empty((B, Tmax, H_), device=dev), torch.empty((B, Umax + 1, H_), device=dev),
+                torch.empty((V, H_), device=dev), torch.empty(V, device=dev))
+        workspace = torch.empty(rb.library.rnnt_joint_grad_workspace_bytes(B, Tmax, Umax, H_, V), dtype=torch.uint8,
+                                device=dev)
+    else:
+        workspace = torch.empty(rb.rnnt_workspace_bytes(B, Tmax, Umax), dtype=torch.uint8, device=dev)
     K, Wm = args.steps, args.warmup
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
     for row in evs:
@@ -492,8 +501,12 @@ def main_joint(args, rb, rdist, rank, world, local, dev):
     torch.cuda.synchronize()
 
     def step(events=None):
-        rb.rnnt_joint_loss(enc, pred, W, bias, targets, T_b, U_b, gcfg.blank, variant, losses=losses,
-                           workspace=workspace, events=events)
+        if grad:
+            rb.rnnt_joint_loss_grad(enc, pred, W, bias, targets, T_b, U_b, gcfg.blank, variant, workspace=workspace,
+                                    outputs=outs)
+        else:
+            rb.rnnt_joint_loss(enc, pred, W, bias, targets, T_b, U_b, gcfg.blank, variant, losses=losses,
+                               workspace=workspace, events=events)
         rb.rnnt_loss_sum(losses, out=loss_sum)
         rdist.allreduce_loss_sum(loss_sum)
 
@@ -503,7 +516,7 @@ def main_joint(args, rb, rdist, rank, world, local, dev):
     if world > 1:
         torch.distributed.barrier()
     graph = graph_ev = None
-    if not args.eager and world == 1:
+    if not args.eager and world == 1 and not grad:
         graph, graph_ev = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
             for i in range(K):
@@ -531,11 +544,14 @@ def main_joint(args, rb, rdist, rank, world, local, dev):
         torch.distributed.barrier()
     ms_step = rdist.max_over_ranks(start.elapsed_time(end), dev) / K
     value = B * world / (ms_step / 1e3)
-    k6_ms = statistics.mean(r[0].elapsed_time(r[1]) for r in evs)
-    k2_ms = statistics.mean(r[2].elapsed_time(r[3]) for r in evs)
+    k6_ms = statistics.mean(r[0].elapsed_time(r[1]) for r in evs) if not grad else None
+    k2_ms = statistics.mean(r[2].elapsed_time(r[3]) for r in evs) if not grad else None
     rows = int(sum(int(t) * (int(u) + 1) for t, u in zip(T_np, U_np)))  # K6 runs on the valid cells only
     flops = 2.0 * rows * V * H
-    tf = flops / (k6_ms / 1e3) / 1e12
+    if grad:  # K6 forward + K6<grad> recompute (valid rows) + the two backward GEMMs (all padded rows)
+        rows_p = B * Tmax * (Umax + 1)
+        flops = 2.0 * 2 * rows * V * H + 2.0 * 2 * rows_p * V * H
+    tf = flops / ((ms_step if grad else k6_ms) / 1e3) / 1e12
     with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
         mp = json.load(f)
     peak = float(mp["bf16_tflops_sustained"])
@@ -546,7 +562,9 @@ def main_joint(args, rb, rdist, rank, world, local, dev):
             torch.distributed.destroy_process_group()
         return
     line = {
-        "metric": "utterances/s fused joint+loss forward (not the BASELINE metric)", "value": value, "unit": UNIT,
+        "metric": ("utterances/s fused joint+loss training step (loss + d enc / d pred / dW / dbias; not the "
+                   "BASELINE metric)") if grad else "utterances/s fused joint+loss forward (not the BASELINE metric)",
+        "value": value, "unit": UNIT,
         "n_gpus": world, "steps": K, "warmup": Wm, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": f"{base.name} shapes through the joint: B={B}/GPU, Tmax={Tmax}, Umax={Umax}, "
@@ -558,18 +576,19 @@ def main_joint(args, rb, rdist, rank, world, local, dev):
                          "resident; the [B,T,U+1,V] logits are never written",
                    "launch": "one CUDA graph of the K steps (split from a second graph with events)"
                              if graph is not None else "eager"},
-        "roofline": {"bound": "tensor", "kernel": "k6_joint_lse", "achieved": tf, "peak": peak, "unit": "TFLOP/s",
+        "roofline": {"bound": "tensor", "kernel": "step (joint_grad: 4 GEMM-sized passes)" if grad else "k6_joint_lse",
+                     "achieved": tf, "peak": peak, "unit": "TFLOP/s",
                      "frac": tf / peak, "traffic": None, "algorithmic_flops_per_launch": flops,
                      "peak_source": "measured (MEASURED_PEAKS.json bf16_tflops_sustained: the kernel runs back "
                                     "to back inside the timed step)",
                      "frac_of_burst_peak": tf / float(mp["bf16_tflops"])},
-        "kernels_ms": {"k6_joint_lse": k6_ms, "k2_alpha_beta": k2_ms},
+        "kernels_ms": {"step": ms_step} if grad else {"k6_joint_lse": k6_ms, "k2_alpha_beta": k2_ms},
         "clocks": clocks.summary(),
-        "gpu_launches": 3 * K,
+        "gpu_launches": (9 if grad else 4) * K,  # rowmap, K6, K2, loss sum (+ K6<grad>, zero_tail, ones, K7 x2)
         "loss_sum_last_step": loss_total,
         "e2e": None,
     }
-    if world == 1 and not args.no_cpu_baseline:
+    if world == 1 and not args.no_cpu_baseline and not grad:
         from oracle import joint as oj
         ids = [0]
         t0 = time.perf_counter()

@@ -242,10 +242,11 @@ def rnnt_joint_loss(enc, pred, weight, bias, targets, logit_lens, target_lens, b
 
 
 def rnnt_joint_loss_grad(enc, pred, weight, bias, targets, logit_lens, target_lens, blank=0, variant="rnnt",
-                         workspace=None, stream=None):
+                         workspace=None, stream=None, outputs=None):
     """Training step of the fused joint (NEXT-4 backward): returns (losses [B], d_enc [B, Tmax, H],
     d_pred [B, Umax+1, H], d_weight [V, H], d_bias [V]), the gradients (fp32) of sum(losses).  Inputs as
-    rnnt_joint_loss; bias may be None (then d_bias is still returned, for a zero bias)."""
+    rnnt_joint_loss; bias may be None (then d_bias is still returned, for a zero bias).  outputs: optional
+    preallocated (losses, d_enc, d_pred, d_weight, d_bias) fp32 tensors of those shapes."""
     for name, x in (("enc", enc), ("pred", pred), ("weight", weight)):
         if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.bfloat16 and x.is_contiguous()):
             raise TypeError(f"{name} must be a contiguous CUDA bfloat16 tensor (no CPU fallback)")
@@ -258,11 +259,13 @@ def rnnt_joint_loss_grad(enc, pred, weight, bias, targets, logit_lens, target_le
     targets = _as_i32(targets, dev).reshape(B, Umax) if Umax > 0 else None
     logit_lens = _as_i32(logit_lens, dev)
     target_lens = _as_i32(target_lens, dev)
-    losses = torch.empty(B, dtype=torch.float32, device=dev)
-    d_enc = torch.empty((B, Tmax, H), dtype=torch.float32, device=dev)
-    d_pred = torch.empty((B, Umax + 1, H), dtype=torch.float32, device=dev)
-    d_weight = torch.empty((V, H), dtype=torch.float32, device=dev)
-    d_bias = torch.empty(V, dtype=torch.float32, device=dev)
+    if outputs is None:
+        outputs = (torch.empty(B, dtype=torch.float32, device=dev),
+                   torch.empty((B, Tmax, H), dtype=torch.float32, device=dev),
+                   torch.empty((B, Umax + 1, H), dtype=torch.float32, device=dev),
+                   torch.empty((V, H), dtype=torch.float32, device=dev),
+                   torch.empty(V, dtype=torch.float32, device=dev))
+    losses, d_enc, d_pred, d_weight, d_bias = outputs
     if workspace is None:
         need = int(library.rnnt_joint_grad_workspace_bytes(B, Tmax, Umax, H, V))
         workspace = torch.empty(max(need, 1), dtype=torch.uint8, device=dev)

@@ -10,7 +10,8 @@
 namespace rnnt {
 
 // Backward-pass inputs / outputs of K6<true>: the forward's lse / lp and K2's alpha / beta / logP in; dz
-// ([rows][Vp] bf16, Vp = V rounded up to 128) and h ([rows][H] bf16) out, rows = the compact valid cells.
+// ([rows][Vp] bf16, Vp = V rounded up to 128) and h ([rows][H + kJointHPad] bf16) out, rows = the compact
+// valid cells.
 struct GradIO {
     const float* lse;
     const double2* lp;
@@ -31,5 +32,6 @@ rnnt_status joint_front(const void* enc, const void* pred, const void* weight, c
                         bool make_map = true, const GradIO* g = nullptr);
 
 constexpr int kJointVTile = 128;  // K6's N tile: dz rows are padded to a multiple of it
+constexpr int kJointHPad = 8;     // h rows carry 8 extra bf16 columns: (1, 0, ..., 0), for dbias in the dW GEMM
 
 }  // namespace rnnt

@@ -220,7 +220,7 @@ struct JointArgs {
     const double* beta;
     const double* logp;
     __nv_bfloat16* dz_out;  // [rows][Vp] row-major, Vp = V rounded up to whole N tiles (tail columns 0)
-    __nv_bfloat16* h_out;   // [rows][H]
+    __nv_bfloat16* h_out;   // [rows][H + kJointHPad]: h, then (1, 0, ..., 0)
 };
 
 // kGrad = false: the forward (lse + gathers).  kGrad = true: the backward's first pass -- the same GEMM
@@ -593,7 +593,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                         make_uint4(ow[0], ow[1], ow[2], ow[3]);
                     if constexpr (kGrad) {  // h for the dW GEMM, compact rows (coalesced: lane = chunk)
                         const int64_t crow = tile * kRowsPerTile + r2;
-                        if (ok[j]) reinterpret_cast<uint4*>(a.h_out + crow * H)[cg] = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+                        // rows of H + 8: the extra 16 bytes hold (1, 0, ..., 0), so the dW GEMM's extra output
+                        // column is dbias = sum_rows dz (no separate GEMV over dz)
+                        __nv_bfloat16* hrow = a.h_out + crow * (H + kJointHPad);
+                        if (ok[j]) reinterpret_cast<uint4*>(hrow)[cg] = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+                        if (ok[j] && cg == 0) reinterpret_cast<uint4*>(hrow + H)[0] = make_uint4(0x3f80u, 0u, 0u, 0u);
                     }
                 }
             }

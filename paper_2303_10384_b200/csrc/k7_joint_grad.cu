@@ -8,9 +8,9 @@
 //   d enc(b,t,:) = sum_{u <= U_b} dpre(t,u,:)           d pred(b,u,:) = sum_{t < T_b} dpre(t,u,:)
 // over the valid cells.  Pipeline (all on the caller's stream):
 //   K6 (forward: lse, gathers) -> K2 (alpha, beta, losses) -> K6<grad> (recomputes z on the tensor cores;
-//   its epilogue writes dz in bf16, its builders write h) -> two plain cuBLAS GEMMs (dh = dz W, dW = dz^T h;
-//   bf16 in, fp32 accumulate and out) and one GEMV-shaped GEMM (dbias = dz^T 1) -> K7 (tanh' and the two
-//   reductions).  The [B,T,U+1,V] logits never exist; dz does, in bf16 (half the bytes of fp32 logits),
+//   its epilogue writes dz in bf16, its builders write h with an extra (1, 0, .., 0) column) -> two plain
+//   cuBLAS GEMMs (dh = dz W; [dW | dbias] = dz^T [h | 1], bf16 in, fp32 accumulate and out) -> K7 (tanh' and
+//   the two reductions).  The [B,T,U+1,V] logits never exist; dz does, in bf16 (half the bytes of fp32 logits),
 //   because dW needs it against every row.  Rows are the compact valid cells (K6's row map); the GEMMs run
 //   over the padded row count B*Tmax*(Umax+1) (the host does not know the valid count without a sync) with
 //   the tail rows zeroed.
@@ -28,13 +28,13 @@ namespace {
 
 constexpr int kJointMaxDevices = 64;
 
-// Zero rows [*nrows, R) of dz ([R][Vp]) and h ([R][H]) so the padded-row GEMMs see no stale data.
-__global__ void __launch_bounds__(256) k7_zero_tail(const int* __restrict__ nrows, int64_t R, int Vp, int H,
+// Zero rows [*nrows, R) of dz ([R][Vp]) and h ([R][Hs]) so the padded-row GEMMs see no stale data.
+__global__ void __launch_bounds__(256) k7_zero_tail(const int* __restrict__ nrows, int64_t R, int Vp, int Hs,
                                                     __nv_bfloat16* dz, __nv_bfloat16* h) {
     const int64_t r0 = *nrows;
-    const int64_t nz = (R - r0) * Vp / 8, nh = (R - r0) * H / 8;  // 16-byte units
+    const int64_t nz = (R - r0) * Vp / 8, nh = (R - r0) * Hs / 8;  // 16-byte units
     uint4* z4 = reinterpret_cast<uint4*>(dz + r0 * Vp);
-    uint4* h4 = reinterpret_cast<uint4*>(h + r0 * H);
+    uint4* h4 = reinterpret_cast<uint4*>(h + r0 * Hs);
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nz + nh;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         if (i < nz)
@@ -44,10 +44,18 @@ __global__ void __launch_bounds__(256) k7_zero_tail(const int* __restrict__ nrow
     }
 }
 
-__global__ void __launch_bounds__(256) k7_fill_ones(__nv_bfloat16* x, int64_t n) {
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-        x[i] = __float2bfloat16(1.f);
+// d_weight [V][H] and d_bias [V] out of the augmented dW GEMM's [V][H + kJointHPad] result.
+__global__ void __launch_bounds__(256) k7_split_dw(const float* __restrict__ dwa, int V, int H, float* __restrict__ dw,
+                                                   float* __restrict__ db) {
+    const int Hs = H + kJointHPad;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < static_cast<int64_t>(V) * Hs;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int v = static_cast<int>(i / Hs), c = static_cast<int>(i - static_cast<int64_t>(v) * Hs);
+        if (c < H)
+            dw[static_cast<int64_t>(v) * H + c] = dwa[i];
+        else if (c == H && db)
+            db[v] = dwa[i];
+    }
 }
 
 __device__ __forceinline__ int utt_count(const int32_t* T_b, const int32_t* U_b, int i, int Tmax, int Umax) {
@@ -69,7 +77,8 @@ __device__ int utt_offset(const int32_t* T_b, const int32_t* U_b, int b, int Tma
 }
 
 // K7: block (i, b) reduces dpre = dh * (1 - h^2) over u for frame i (mode 0: d enc[b, i, :]) or over t for
-// unit i (mode 1: d pred[b, i, :]); H <= 512, 128 threads x 4 columns.  Invalid / padded rows: 0.
+// unit i (mode 1: d pred[b, i, :]); H <= 512, 128 threads x 4 columns; padded frames / units get 0.  (One
+// pass computing both with shared-memory partials and atomics measured slower: 2.5 vs 1.4 ms at c3.)
 template <int kMode>
 __global__ void __launch_bounds__(128) k7_reduce(const float* __restrict__ dh, const __nv_bfloat16* __restrict__ h,
                                                  const int32_t* __restrict__ T_b, const int32_t* __restrict__ U_b,
@@ -82,13 +91,15 @@ __global__ void __launch_bounds__(128) k7_reduce(const float* __restrict__ dh, c
     const int len = kMode == 0 ? (i < T ? U + 1 : 0) : (i <= U ? T : 0);
     const int64_t first = off + (kMode == 0 ? static_cast<int64_t>(i) * (U + 1) : i);
     const int64_t stride = kMode == 0 ? 1 : (U + 1);
+    const int Hs = H + kJointHPad;
     float* o = out + (static_cast<int64_t>(b) * (kMode == 0 ? Tmax : Umax + 1) + i) * H;
     for (int c = threadIdx.x * 4; c < H; c += blockDim.x * 4) {
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
         for (int k = 0; k < len; ++k) {
             const int64_t r = first + k * stride;
             const float4 d = *reinterpret_cast<const float4*>(dh + r * H + c);
-            const uint2 hw = *reinterpret_cast<const uint2*>(h + r * H + c);
+            const uint2 hw = *reinterpret_cast<const uint2*>(h + r * Hs + c);
             const float h0 = __uint_as_float(hw.x << 16), h1 = __uint_as_float(hw.x & 0xffff0000u);
             const float h2 = __uint_as_float(hw.y << 16), h3 = __uint_as_float(hw.y & 0xffff0000u);
             acc.x = fmaf(d.x, fmaf(-h0, h0, 1.f), acc.x);
@@ -112,7 +123,7 @@ cublasHandle_t blas_handle() {
 struct GradLayout {
     int64_t R;  // padded rows B * Tmax * (Umax + 1)
     int Vp;
-    size_t base, rowmap, nrows, dz, h, dh, ones, total;
+    size_t base, rowmap, nrows, dz, h, dh, dwa, total;
 };
 
 GradLayout grad_layout(int B, int Tmax, int Umax, int H, int V) {
@@ -128,11 +139,11 @@ GradLayout grad_layout(int B, int Tmax, int Umax, int H, int V) {
     L.dz = off;
     off += align256(sizeof(__nv_bfloat16) * L.R * L.Vp);
     L.h = off;
-    off += align256(sizeof(__nv_bfloat16) * L.R * H);
+    off += align256(sizeof(__nv_bfloat16) * L.R * (H + kJointHPad));
     L.dh = off;
     off += align256(sizeof(float) * L.R * H);
-    L.ones = off;
-    off += align256(sizeof(__nv_bfloat16) * L.R);
+    L.dwa = off;
+    off += align256(sizeof(float) * static_cast<size_t>(V) * (H + kJointHPad));
     L.total = off;
     return L;
 }
@@ -165,7 +176,7 @@ extern "C" rnnt_status rnnt_joint_loss_grad(const void* enc, const void* pred, c
     auto* dz = reinterpret_cast<__nv_bfloat16*>(ws + L.dz);
     auto* hb = reinterpret_cast<__nv_bfloat16*>(ws + L.h);
     auto* dh = reinterpret_cast<float*>(ws + L.dh);
-    auto* ones = reinterpret_cast<__nv_bfloat16*>(ws + L.ones);
+    auto* dwa = reinterpret_cast<float*>(ws + L.dwa);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     cublasHandle_t hd = blas_handle();
     if (!hd) return RNNT_ERR_CUDA;
@@ -183,8 +194,8 @@ extern "C" rnnt_status rnnt_joint_loss_grad(const void* enc, const void* pred, c
     st = joint_front(enc, pred, weight, bias, targets, logit_lens, target_lens, B, Tmax, Umax, H, V, blank,
                      workspace, workspace_bytes, s, nullptr, rowmap, nrows, false, &g);
     if (st != RNNT_OK) return st;
-    k7_zero_tail<<<1184, 256, 0, s>>>(nrows, L.R, L.Vp, H, dz, hb);
-    if (d_bias) k7_fill_ones<<<296, 256, 0, s>>>(ones, L.R);
+    const int Hs = H + kJointHPad;
+    k7_zero_tail<<<1184, 256, 0, s>>>(nrows, L.R, L.Vp, Hs, dz, hb);
     if (cudaGetLastError() != cudaSuccess) return RNNT_ERR_CUDA;
     // the two GEMMs and dbias (column-major views of the row-major arrays; bf16 in, fp32 accumulate / out)
     const float one = 1.f, zero = 0.f;
@@ -194,15 +205,11 @@ extern "C" rnnt_status rnnt_joint_loss_grad(const void* enc, const void* pred, c
     if (cublasGemmEx(hd, CUBLAS_OP_N, CUBLAS_OP_N, H, R, V, &one, weight, CUDA_R_16BF, H, dz, CUDA_R_16BF, L.Vp,
                      &zero, dh, CUDA_R_32F, H, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT) != CUBLAS_STATUS_SUCCESS)
         return RNNT_ERR_CUDA;
-    // dW^T [H x V] = h^T [H x R] . dz [R x V]
-    if (cublasGemmEx(hd, CUBLAS_OP_N, CUBLAS_OP_T, H, V, R, &one, hb, CUDA_R_16BF, H, dz, CUDA_R_16BF, L.Vp, &zero,
-                     d_weight, CUDA_R_32F, H, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT) != CUBLAS_STATUS_SUCCESS)
+    // [dW | dbias]^T [(H + 8) x V] = [h | 1 0..0]^T [(H + 8) x R] . dz [R x V]
+    if (cublasGemmEx(hd, CUBLAS_OP_N, CUBLAS_OP_T, Hs, V, R, &one, hb, CUDA_R_16BF, Hs, dz, CUDA_R_16BF, L.Vp, &zero,
+                     dwa, CUDA_R_32F, Hs, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT) != CUBLAS_STATUS_SUCCESS)
         return RNNT_ERR_CUDA;
-    // dbias [V x 1] = dz^T [V x R] . 1 [R x 1]
-    if (d_bias && cublasGemmEx(hd, CUBLAS_OP_N, CUBLAS_OP_N, V, 1, R, &one, dz, CUDA_R_16BF, L.Vp, ones, CUDA_R_16BF,
-                               R, &zero, d_bias, CUDA_R_32F, V, CUBLAS_COMPUTE_32F,
-                               CUBLAS_GEMM_DEFAULT) != CUBLAS_STATUS_SUCCESS)
-        return RNNT_ERR_CUDA;
+    k7_split_dw<<<296, 256, 0, s>>>(dwa, V, H, d_weight, d_bias);
     // K7: tanh' and the reductions into d enc / d pred
     k7_reduce<0><<<dim3(Tmax, B), 128, 0, s>>>(dh, hb, logit_lens, target_lens, Tmax, Umax, H, d_enc);
     k7_reduce<1><<<dim3(Umax + 1, B), 128, 0, s>>>(dh, hb, logit_lens, target_lens, Tmax, Umax, H, d_pred);
