@@ -516,7 +516,7 @@ def main_joint(args, rb, rdist, rank, world, local, dev):
     if world > 1:
         torch.distributed.barrier()
     graph = graph_ev = None
-    if not args.eager and world == 1 and not grad:
+    if not args.eager and world == 1:
         graph, graph_ev = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
             for i in range(K):
@@ -574,7 +574,7 @@ def main_joint(args, rb, rdist, rank, world, local, dev):
                    "l2": "no flush: the joint's inputs (enc/pred/W, "
                          f"{(enc.numel() + pred.numel() + W.numel()) * 2 / 1e6:.0f} MB) are meant to be L2/HBM "
                          "resident; the [B,T,U+1,V] logits are never written",
-                   "launch": "one CUDA graph of the K steps (split from a second graph with events)"
+                   "launch": ("one CUDA graph of the K steps" + ("" if grad else " (split from a second graph with events)"))
                              if graph is not None else "eager"},
         "roofline": {"bound": "tensor", "kernel": "step (joint_grad: 4 GEMM-sized passes)" if grad else "k6_joint_lse",
                      "achieved": tf, "peak": peak, "unit": "TFLOP/s",
