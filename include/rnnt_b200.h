@@ -197,9 +197,9 @@ rnnt_status rnnt_joint_viterbi(const void* enc, const void* pred, const void* we
  * gradients of sum_b losses[b] with respect to the joint's inputs, fp32 row-major:
  *   d_enc [B][Tmax][H], d_pred [B][Umax+1][H] (zero on padded frames / units), d_weight [V][H], d_bias [V]
  *   (or NULL).  dz = d loss / d z is formed on chip from the recomputed logits (K3's formula) and stored in bf16
- *   for the two backward GEMMs (dh = dz W, dW = dz^T h; cuBLAS, fp32 accumulation); tanh' uses the stored
- *   bf16 h.  workspace: rnnt_joint_grad_workspace_bytes(...) bytes (it holds dz, h and dh of every padded
- *   cell: ~ (2 V + 6 H) bytes per cell).  Same constraints as rnnt_joint_loss. */
+ *   for the two backward GEMMs (dh = dz W stored in bf16, dW = dz^T h; cuBLAS, fp32 accumulation); tanh' uses
+ *   the stored bf16 h.  workspace: rnnt_joint_grad_workspace_bytes(...) bytes (it holds dz, h and dh of every
+ *   padded cell: ~ (2 V + 4 H) bytes per cell).  Same constraints as rnnt_joint_loss. */
 size_t rnnt_joint_grad_workspace_bytes(int B, int Tmax, int Umax, int H, int V);
 rnnt_status rnnt_joint_loss_grad(const void* enc, const void* pred, const void* weight, const float* bias,
                                  const int32_t* targets, const int32_t* logit_lens, const int32_t* target_lens,

@@ -55,9 +55,10 @@ def joint_loss(f, g, W, bias, y, T_b, U_b, blank=0, variant="rnnt"):
 
 def joint_loss_and_grads(f, g, W, bias, y, T_b, U_b, blank=0, variant="rnnt", round_bf16=True):
     """Losses and the gradients of their sum w.r.t. (f, g, W, bias) -- the chain rule of the joint above,
-    line by line (reading R23: the backward uses the stored bf16 h for tanh' = 1 - h^2, and dz is
-    rounded to bf16 before the two backward matrix products, as a bf16 training graph stores it).
-    round_bf16=False drops both roundings (h and dz): the plain real-valued chain rule (for pinning).
+    line by line (reading R23: the backward uses the stored bf16 h for tanh' = 1 - h^2, dz is
+    rounded to bf16 before the two backward matrix products and dh = dz W is stored in bf16, as a bf16
+    training graph stores them).  round_bf16=False drops the roundings (h, dz, dh): the plain real-valued
+    chain rule (for pinning).
 
     Returns (losses [B], d_f [B,Tmax,H], d_g [B,Umax+1,H], d_W [V,H], d_bias [V]), float64."""
     f = np.asarray(f, np.float64)
@@ -70,7 +71,7 @@ def joint_loss_and_grads(f, g, W, bias, y, T_b, U_b, blank=0, variant="rnnt", ro
         z = z + np.asarray(bias, np.float64)
     losses, dz = _loss_batch(z.astype(np.float32), y, T_b, U_b, blank, variant, grad=True)
     dz = rnd(dz)                                                     # d sum(loss) / d z, zero on padding
-    dh = dz @ W                                                      # [B, T, U+1, H]
+    dh = rnd(dz @ W)                                                 # [B, T, U+1, H], stored in bf16
     d_W = np.einsum("btuv,btuh->vh", dz, h)
     d_bias = dz.sum(axis=(0, 1, 2))
     dpre = dh * (1.0 - h * h)                                        # through tanh

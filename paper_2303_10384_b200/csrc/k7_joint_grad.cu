@@ -4,7 +4,7 @@
 //   dz(t,u,v)  = softmax(z)(v) (occ_b + occ_y) - [v = blank] occ_b - [v = y_u] occ_y      (K3's formula)
 //   dh(t,u,:)  = sum_v dz(t,u,v) W(v,:)                  dW(v,:) = sum_{t,u} dz(t,u,v) h(t,u,:)
 //   dbias(v)   = sum_{t,u} dz(t,u,v)
-//   dpre       = dh * (1 - h^2)   (tanh' from the stored bf16 h)
+//   dpre       = dh * (1 - h^2)   (dh stored in bf16, tanh' from the stored bf16 h)
 //   d enc(b,t,:) = sum_{u <= U_b} dpre(t,u,:)           d pred(b,u,:) = sum_{t < T_b} dpre(t,u,:)
 // over the valid cells.  Pipeline (all on the caller's stream):
 //   K6 (forward: lse, gathers) -> K2 (alpha, beta, losses) -> K6<grad> (recomputes z on the tensor cores;
@@ -80,7 +80,7 @@ __device__ int utt_offset(const int32_t* T_b, const int32_t* U_b, int b, int Tma
 // unit i (mode 1: d pred[b, i, :]); H <= 512, 128 threads x 4 columns; padded frames / units get 0.  (One
 // pass computing both with shared-memory partials and atomics measured slower: 2.5 vs 1.4 ms at c3.)
 template <int kMode>
-__global__ void __launch_bounds__(128) k7_reduce(const float* __restrict__ dh, const __nv_bfloat16* __restrict__ h,
+__global__ void __launch_bounds__(128) k7_reduce(const __nv_bfloat16* __restrict__ dh, const __nv_bfloat16* __restrict__ h,
                                                  const int32_t* __restrict__ T_b, const int32_t* __restrict__ U_b,
                                                  int Tmax, int Umax, int H, float* __restrict__ out) {
     __shared__ int s_part[4];
@@ -98,7 +98,9 @@ __global__ void __launch_bounds__(128) k7_reduce(const float* __restrict__ dh, c
 #pragma unroll 4
         for (int k = 0; k < len; ++k) {
             const int64_t r = first + k * stride;
-            const float4 d = *reinterpret_cast<const float4*>(dh + r * H + c);
+            const uint2 dw = *reinterpret_cast<const uint2*>(dh + r * H + c);
+            const float4 d = make_float4(__uint_as_float(dw.x << 16), __uint_as_float(dw.x & 0xffff0000u),
+                                         __uint_as_float(dw.y << 16), __uint_as_float(dw.y & 0xffff0000u));
             const uint2 hw = *reinterpret_cast<const uint2*>(h + r * Hs + c);
             const float h0 = __uint_as_float(hw.x << 16), h1 = __uint_as_float(hw.x & 0xffff0000u);
             const float h2 = __uint_as_float(hw.y << 16), h3 = __uint_as_float(hw.y & 0xffff0000u);
@@ -141,7 +143,7 @@ GradLayout grad_layout(int B, int Tmax, int Umax, int H, int V) {
     L.h = off;
     off += align256(sizeof(__nv_bfloat16) * L.R * (H + kJointHPad));
     L.dh = off;
-    off += align256(sizeof(float) * L.R * H);
+    off += align256(sizeof(__nv_bfloat16) * L.R * H);
     L.dwa = off;
     off += align256(sizeof(float) * static_cast<size_t>(V) * (H + kJointHPad));
     L.total = off;
@@ -175,7 +177,7 @@ extern "C" rnnt_status rnnt_joint_loss_grad(const void* enc, const void* pred, c
     int* nrows = reinterpret_cast<int*>(ws + L.nrows);
     auto* dz = reinterpret_cast<__nv_bfloat16*>(ws + L.dz);
     auto* hb = reinterpret_cast<__nv_bfloat16*>(ws + L.h);
-    auto* dh = reinterpret_cast<float*>(ws + L.dh);
+    auto* dh = reinterpret_cast<__nv_bfloat16*>(ws + L.dh);
     auto* dwa = reinterpret_cast<float*>(ws + L.dwa);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     cublasHandle_t hd = blas_handle();
@@ -203,7 +205,7 @@ extern "C" rnnt_status rnnt_joint_loss_grad(const void* enc, const void* pred, c
     if (cublasSetStream(hd, s) != CUBLAS_STATUS_SUCCESS) return RNNT_ERR_CUDA;
     // dh^T [H x R] = W^T [H x V] . dz^T [V x R]
     if (cublasGemmEx(hd, CUBLAS_OP_N, CUBLAS_OP_N, H, R, V, &one, weight, CUDA_R_16BF, H, dz, CUDA_R_16BF, L.Vp,
-                     &zero, dh, CUDA_R_32F, H, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT) != CUBLAS_STATUS_SUCCESS)
+                     &zero, dh, CUDA_R_16BF, H, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT) != CUBLAS_STATUS_SUCCESS)
         return RNNT_ERR_CUDA;
     // [dW | dbias]^T [(H + 8) x V] = [h | 1 0..0]^T [(H + 8) x R] . dz [R x V]
     if (cublasGemmEx(hd, CUBLAS_OP_N, CUBLAS_OP_T, Hs, V, R, &one, hb, CUDA_R_16BF, Hs, dz, CUDA_R_16BF, L.Vp, &zero,
