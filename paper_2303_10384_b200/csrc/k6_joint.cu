@@ -85,8 +85,37 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
         : "memory");
 }
+// Cluster-multicast variant: the tile lands at the same shared-memory offset of every CTA in cta_mask, each
+// of whose mbarrier at `bar`'s offset receives the complete_tx.
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                               uint16_t cta_mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster "
+        "[%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "h"(cta_mask)
+        : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// commit to the mbarrier at `bar`'s offset in every CTA of cta_mask (one elected lane of a converged warp)
+__device__ __forceinline__ void tc_commit_mc(uint64_t* bar, uint16_t cta_mask) {
+    asm volatile(
+        "{\n"
+        ".reg .pred e;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "h"(cta_mask)
+        : "memory");
+}
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {  // by one elected lane of a converged warp
     asm volatile(
         "{\n"
@@ -227,8 +256,12 @@ struct JointArgs {
 // recomputes z and the epilogue forms dz = softmax(z) (occ_b + occ_y) - [v = blank] occ_b - [v = y] occ_y
 // (K3's formula, with the forward's lse and K2's alpha / beta), stored in bf16 for the two backward GEMMs;
 // the builders also store h.
-template <bool kGrad>
-__global__ void __launch_bounds__(kThreads, 1)
+// kCl = 2: CTA pairs (clusters of 2) share every W stage -- each CTA fetches half of the stage's rows and
+// multicasts it into both CTAs' shared memory (half the W traffic from L2 per SM); the pair walks the same
+// W sequence in lockstep (a stage is refilled once both MMAs released it) and the same number of row tiles
+// (the second CTA's last one may be a dummy past the end).
+template <bool kGrad, int kCl>
+__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
     k6_joint_lse(const __grid_constant__ CUtensorMap w_map, const JointArgs a) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // carve: [W stages (1024-aligned)] [A staging 128 x H bf16] [bias V fp32] [barriers] [tmem slot]
@@ -270,7 +303,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 0) {
         for (int s = 0; s < a.stages; ++s) {
             mbar_init(&b_full[s], 1);
-            mbar_init(&b_empty[s], 1);
+            mbar_init(&b_empty[s], kCl);  // released by the MMAs of every CTA of the cluster
         }
         mbar_init(a_full, 256);
         mbar_init(a_empty, 1);
@@ -288,9 +321,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (kCl > 1)
+        cluster_sync_all();  // barriers initialised cluster-wide before any multicast signals them
+    else
+        __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    // Row tiles: blockIdx.x + k * gridDim.x for k < n_iter, n_iter taken from the cluster's first CTA
+    const int64_t bx = blockIdx.x, cl0 = bx - bx % kCl;
+    const int64_t n_iter = ntiles > cl0 ? (ntiles - cl0 + gridDim.x - 1) / gridDim.x : 0;
+    const uint32_t crank = kCl > 1 ? cluster_rank() : 0;
     const bool pon = (a.dbg & 4) != 0;
     unsigned long long w_tma = 0, w_afull = 0, w_accempty = 0, w_bfull = 0, w_accfull = 0, w_aempty = 0;
     const long long t_start = clock64();
@@ -300,13 +340,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             int s = 0;
             uint32_t ph = 0;
-            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
+            for (int64_t k = 0; k < n_iter; ++k)
                 for (int n = 0; n < NT; ++n)
                     for (int kb = 0; kb < KB; ++kb) {
                         mbar_wait_t(&b_empty[s], ph ^ 1, pon, w_tma);
-                        mbar_expect_tx(&b_full[s], kStageBytes);
-                        tma_load_2d(wst + static_cast<size_t>(s) * kStageBytes, &w_map, &b_full[s], kb * kKBlock,
-                                    n * kNTile);
+                        mbar_expect_tx(&b_full[s], kStageBytes);  // the whole stage lands here (both halves)
+                        if constexpr (kCl > 1)
+                            tma_load_2d_mc(wst + static_cast<size_t>(s) * kStageBytes + crank * (kStageBytes / kCl),
+                                           &w_map, &b_full[s], kb * kKBlock, n * kNTile + crank * (kNTile / kCl),
+                                           static_cast<uint16_t>((1u << kCl) - 1));
+                        else
+                            tma_load_2d(wst + static_cast<size_t>(s) * kStageBytes, &w_map, &b_full[s], kb * kKBlock,
+                                        n * kNTile);
                         if (++s == a.stages) {
                             s = 0;
                             ph ^= 1;
@@ -319,7 +364,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t ph = 0;
         uint32_t it = 0;  // accumulator use counter
         uint32_t tl = 0;  // local tile counter
-        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tl) {
+        for (int64_t k = 0; k < n_iter; ++k, ++tl) {
             mbar_wait_t(a_full, tl & 1, pon, w_afull);
             tc_fence_after();
             for (int n = 0; n < NT; ++n, ++it) {
@@ -332,7 +377,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tc_fence_after();
                     const uint64_t bdesc = sw128_desc(smem_u32(wst + static_cast<size_t>(s) * kStageBytes));
                     mma_kblock(d_tmem, tmem + kb * (kKBlock / 2), bdesc, kIdesc, kb ? 1u : 0u);
-                    tc_commit(&b_empty[s]);  // frees the W stage when these MMAs complete
+                    // frees the W stage (in every CTA of the cluster: its producer refills both) once these MMAs complete
+                    if constexpr (kCl > 1)
+                        tc_commit_mc(&b_empty[s], static_cast<uint16_t>((1u << kCl) - 1));
+                    else
+                        tc_commit(&b_empty[s]);
                     if (++s == a.stages) {
                         s = 0;
                         ph ^= 1;
@@ -354,7 +403,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int rl = q * 32 + lane;
         const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16);
         uint32_t it = 0, tile_local = 0;
-        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        for (int64_t k = 0; k < n_iter; ++k) {
+            const int64_t tile = bx + k * gridDim.x;
             int b = 0, t = 0, u = 0;
             const bool in = decode(tile * kRowsPerTile + rl, b, t, u);
             const int T = in ? min(a.T_b[b], a.Tmax) : 0, U = in ? min(a.U_b[b], a.Umax) : 0;
@@ -605,13 +655,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16);
         uint32_t tl = 0;
-        int64_t tile = blockIdx.x;
-        if (tile < ntiles) {
-            const int p0 = map_of(tile);
-            p_next = map_of(tile + gridDim.x);
-            build(tile, p0);
+        if (n_iter > 0) {
+            const int p0 = map_of(bx);
+            p_next = map_of(bx + gridDim.x);
+            build(bx, p0);
         }
-        for (; tile < ntiles; tile += gridDim.x, ++tl) {
+        for (int64_t k = 0; k < n_iter; ++k, ++tl) {
+            const int64_t tile = bx + k * gridDim.x;
             if (tl > 0) mbar_wait_t(a_empty, (tl - 1) & 1, pon, w_aempty);
             tc_fence_after();
             // staging -> TMEM: this thread's row, its K half = nch chunks = nch * 4 columns
@@ -631,7 +681,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             tc_fence_before();
             mbar_arrive(a_full);
-            if (tile + gridDim.x < ntiles) {
+            if (k + 1 < n_iter) {
                 const int p = p_next;
                 p_next = map_of(tile + 2 * static_cast<int64_t>(gridDim.x));
                 build(tile + gridDim.x, p);
@@ -648,7 +698,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (warp == 12) o[6] = w_aempty;
     }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (kCl > 1)
+        cluster_sync_all();  // no CTA leaves while its partner may still multicast into it
+    else
+        __syncthreads();
     tc_fence_after();
     if (warp == 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
@@ -745,7 +798,9 @@ rnnt_status joint_front(const void* enc, const void* pred, const void* weight, c
     CUtensorMap map;
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(H), static_cast<cuuint64_t>(V)};
     const cuuint64_t strides[1] = {static_cast<cuuint64_t>(H) * 2};
-    const cuuint32_t box[2] = {static_cast<cuuint32_t>(kKBlock), static_cast<cuuint32_t>(kNTile)};
+    int cl = 2;  // CTA-pair W multicast (RNNT_K6_CLUSTER=1: one CTA per W stream, for A/B)
+    if (const char* e = getenv("RNNT_K6_CLUSTER")) cl = atoi(e) == 1 ? 1 : 2;
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(kKBlock), static_cast<cuuint32_t>(kNTile / cl)};
     const cuuint32_t estr[2] = {1, 1};
     if (enc_fn(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(weight), dims, strides, box, estr,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -761,7 +816,8 @@ rnnt_status joint_front(const void* enc, const void* pred, const void* weight, c
     while (stages > 2 && joint_smem_bytes(H, V, stages) > static_cast<size_t>(smem_max)) --stages;
     const size_t smem = joint_smem_bytes(H, V, stages);
     if (smem > static_cast<size_t>(smem_max)) return RNNT_ERR_UNSUPPORTED;
-    auto kern = g ? k6_joint_lse<true> : k6_joint_lse<false>;
+    auto kern = g ? (cl > 1 ? k6_joint_lse<true, 2> : k6_joint_lse<true, 1>)
+                  : (cl > 1 ? k6_joint_lse<false, 2> : k6_joint_lse<false, 1>);
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
         return RNNT_ERR_CUDA;
 
@@ -788,7 +844,8 @@ rnnt_status joint_front(const void* enc, const void* pred, const void* weight, c
     args.prof = nullptr;
     if (args.dbg & 4) cudaMalloc(&args.prof, sizeof(unsigned long long) * 8 * nsm);
     const int64_t ntiles = (args.rows + kRowsPerTile - 1) / kRowsPerTile;
-    const int grid = static_cast<int>(std::min<int64_t>(ntiles, nsm));
+    int grid = static_cast<int>(std::min<int64_t>(ntiles, nsm));
+    grid = std::max(cl, grid - grid % cl);  // whole clusters
     if (record_ev(events, 0, s) != cudaSuccess) return RNNT_ERR_CUDA;
     if (make_map)
         k6_rowmap<<<dim3(static_cast<unsigned>((static_cast<int64_t>(Tmax) * (Umax + 1) + 4095) / 4096), B), 256, 0,
