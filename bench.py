@@ -578,7 +578,7 @@ def main_joint(args, rb, rdist, rank, world, local, dev):
                              if graph is not None else "eager"},
         "roofline": {"bound": "tensor", "kernel": "step (joint_grad: 4 GEMM-sized passes)" if grad else "k6_joint_lse",
                      "achieved": tf, "peak": peak, "unit": "TFLOP/s",
-                     "frac": tf / peak, "traffic": None, "algorithmic_flops_per_launch": flops,
+                     "frac": tf / peak, "traffic": None if grad else ncu_traffic("k6_joint_lse", args.config + "_joint"), "algorithmic_flops_per_launch": flops,
                      "peak_source": "measured (MEASURED_PEAKS.json bf16_tflops_sustained: the kernel runs back "
                                     "to back inside the timed step)",
                      "frac_of_burst_peak": tf / float(mp["bf16_tflops"])},
