@@ -58,6 +58,9 @@ def parse():
                          "network + loss forward from Encoder/Predictor embeddings (H=--hidden) -- NEXT-4; "
                          "joint_grad: the fused joint's training step (loss + gradients w.r.t. enc, pred, W, bias)")
     ap.add_argument("--hidden", type=int, default=512, help="--mode joint: embedding size H (P:124: 512)")
+    ap.add_argument("--lattice", default="grid", choices=["grid", "compose"],
+                    help="--mode lattice: build the lattices directly (Grid-Transducer, P:90-92) or by composing the "
+                         "time and unit schemas (Compose-Transducer, P:82-88; host-side, untimed)")
     ap.add_argument("--eager", action="store_true",
                     help="launch the K timed steps one by one from Python instead of replaying them as one CUDA graph "
                          "(the default at N=1 for --mode loss_grad / loss: no host launch overhead between kernels)")
@@ -283,8 +286,12 @@ def main():
     dlat = None
     if args.mode == "lattice":
         from paper_2303_10384_b200 import lattice as rlat
-        dlat = rb.lattice_to_device(rlat.grid_lattices(pb["logit_lens"], pb["target_lens"], pb["targets"],
-                                                       gcfg.blank, variant), dev)
+        if args.lattice == "compose":
+            from paper_2303_10384_b200 import compose as rcmp
+            hl = rcmp.compose_lattices(pb["logit_lens"], pb["target_lens"], pb["targets"], gcfg.V, gcfg.blank, variant)
+        else:
+            hl = rlat.grid_lattices(pb["logit_lens"], pb["target_lens"], pb["targets"], gcfg.blank, variant)
+        dlat = rb.lattice_to_device(hl, dev)
 
     def step(events=None):
         if args.mode == "lattice":
@@ -392,6 +399,7 @@ def main():
                        "global_batch": B * world, "parallelism": f"dp{world} (batch shards, NCCL all-reduce of "
                        f"the fp64 loss sum)", "l2": f"inputs {z.numel() * esize / 1e9:.2f} GB/GPU > 126 MB L2: no flush",
                        "grads": "in place" if inplace else "out of place",
+                       **({"lattice": args.lattice} if args.mode == "lattice" else {}),
                        "launch": (f"one CUDA graph of the {K} steps (kernel split: a second graph of the same "
                                   f"{K} steps with timing events, replayed next)") if graph is not None else "eager"},
             "roofline": roof,
