@@ -291,7 +291,7 @@ def main():
             hl = rcmp.compose_lattices(pb["logit_lens"], pb["target_lens"], pb["targets"], gcfg.V, gcfg.blank, variant)
         else:
             hl = rlat.grid_lattices(pb["logit_lens"], pb["target_lens"], pb["targets"], gcfg.blank, variant)
-        dlat = rb.lattice_to_device(hl, dev)
+        dlat = rb.lattice_to_device(hl, dev, Tmax, Umax)
 
     def step(events=None):
         if args.mode == "lattice":

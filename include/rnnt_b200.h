@@ -136,17 +136,21 @@ rnnt_status rnnt_viterbi(const void* logits, rnnt_dtype dtype, const int32_t* ta
  *   arc_src / arc_dst [A] (global state ids), arc_t / arc_u / arc_v [A]: arc weight X[b, t, u, v] =
  *                    logits[b,t,u,v] - logsumexp_v logits[b,t,u,:], or 0 when arc_v < 0 (structural arc)
  *   final_w   [S]    fp32 log final weight (-inf: not final)
+ *   row_off [B*Tmax*(Umax+1) + 1], row_arc [#bound arcs] or both NULL: the arcs bound to logits row
+ *                    r = (b*Tmax + t)*(Umax+1) + u are row_arc[row_off[r] .. row_off[r+1]) (lattice.py builds it);
+ *                    with it the gradient is one deterministic row pass, without it two float-atomic passes
  * Rows (t,u) with t < logit_lens[b], u <= target_lens[b] are live; every arc must bind a live row.
  * losses[b] = -log sum over start->final paths of exp(sum of arc weights + final weight) (Eq.(1)); grads
- * (fp32, may equal logits, or NULL) = d losses[b] / d logits, zero on non-live rows.  fp32 only; float
- * atomics make grads order-dependent where > 2 arcs share a row or > 1 arc shares a (t,u,v). */
+ * (fp32, may equal logits, or NULL) = d losses[b] / d logits, zero on non-live rows.  fp32 only; without a
+ * row index, float atomics make grads order-dependent where > 2 arcs share a row or > 1 arc shares a (t,u,v). */
 size_t rnnt_lattice_workspace_bytes(int B, int Tmax, int Umax, int num_states, int num_arcs);
 rnnt_status rnnt_lattice_loss(const float* logits, const int32_t* logit_lens, const int32_t* target_lens,
                               int B, int Tmax, int Umax, int V, const int32_t* state_off,
                               const int32_t* lvl_off, const int32_t* level_off, const int32_t* in_off,
                               const int32_t* out_off, const int32_t* out_arc, const int32_t* arc_src,
                               const int32_t* arc_dst, const int32_t* arc_t, const int32_t* arc_u,
-                              const int32_t* arc_v, const float* final_w, int num_states, int num_arcs,
+                              const int32_t* arc_v, const float* final_w, const int32_t* row_off,
+                              const int32_t* row_arc, int num_states, int num_arcs,
                               float* losses, float* grads, void* workspace, size_t workspace_bytes,
                               void* stream);
 

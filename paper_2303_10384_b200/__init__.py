@@ -10,6 +10,7 @@ from __future__ import annotations
 import ctypes
 import os
 
+import numpy as np
 import torch
 
 from ._build import LIB_PATH
@@ -48,7 +49,7 @@ def _load():
         "rnnt_loss_ex": ([P, I, P, P, P, I, I, I, I, I, I, P, P, P, P, S, P, P], I),
         "rnnt_viterbi": ([P, I, P, P, P, I, I, I, I, I, I, P, P, P, P, S, P], I),
         "rnnt_lattice_workspace_bytes": ([I, I, I, I, I], S),
-        "rnnt_lattice_loss": ([P, P, P, I, I, I, I] + [P] * 12 + [I, I, P, P, P, S, P], I),
+        "rnnt_lattice_loss": ([P, P, P, I, I, I, I] + [P] * 14 + [I, I, P, P, P, S, P], I),
         "rnnt_loss_sum": ([P, I, P, P], I),
         "rnnt_host_buffer_bytes": ([I, I, I, I], S),
         "rnnt_loss_host": ([P, P, P, P, I, I, I, I, I, I, P, P, P, S, P], I),
@@ -312,7 +313,7 @@ def rnnt_lattice_loss(logits, lattices, logit_lens, target_lens, grads=True, los
         raise TypeError("logits must be a CUDA float32 tensor (no CPU fallback)")
     B, Tmax, Up1, V = logits.shape
     dev = logits.device
-    dv = lattices if isinstance(lattices, dict) else lattice_to_device(lattices, dev)
+    dv = lattices if isinstance(lattices, dict) else lattice_to_device(lattices, dev, Tmax, Up1 - 1)
     if losses is None:
         losses = torch.empty(B, dtype=torch.float32, device=dev)
     if isinstance(grads, str) and grads == "inplace":
@@ -329,16 +330,22 @@ def rnnt_lattice_loss(logits, lattices, logit_lens, target_lens, grads=True, los
         _ptr(logits), _ptr(logit_lens), _ptr(target_lens), B, Tmax, Up1 - 1, V,
         *[_ptr(dv[k]) for k in ("state_off", "lvl_off", "level_off", "in_off", "out_off", "out_arc", "arc_src",
                                 "arc_dst", "arc_t", "arc_u", "arc_v", "final_w")],
+        _ptr(dv.get("row_off")), _ptr(dv.get("row_arc")),
         dv["num_states"], dv["num_arcs"], _ptr(losses), _ptr(grads), _ptr(ws), ws.numel(), _stream(stream)))
     return losses, grads
 
 
-def lattice_to_device(L, device="cuda"):
-    """Upload a lattice.LatticeBatch once (the dict rnnt_lattice_loss accepts)."""
+def lattice_to_device(L, device="cuda", Tmax=None, Umax=None):
+    """Upload a lattice.LatticeBatch once (the dict rnnt_lattice_loss accepts).  With the logits' (Tmax, Umax)
+    the row index is uploaded too (one deterministic gradient pass; without it, two float-atomic passes)."""
     dv = {k: torch.from_numpy(getattr(L, k)).to(device) for k in (
         "state_off", "lvl_off", "level_off", "in_off", "out_off", "out_arc", "arc_src", "arc_dst", "arc_t", "arc_u",
         "arc_v", "final_w")}
     dv["num_states"], dv["num_arcs"] = L.num_states, L.num_arcs
+    if Tmax is not None:
+        row_off, row_arc = L.row_index(Tmax, Umax)
+        dv["row_off"] = torch.from_numpy(row_off).to(device)
+        dv["row_arc"] = torch.from_numpy(row_arc if row_arc.size else np.zeros(1, np.int32)).to(device)
     return dv
 
 

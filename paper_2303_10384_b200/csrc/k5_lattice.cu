@@ -320,12 +320,161 @@ __global__ void __launch_bounds__(256) l5_rows(const float* logits, const float*
     }
 }
 
+// With a row index (row_off / row_arc: the arcs bound to each logits row, host-built) the gradient needs no
+// float atomics, so it does not depend on scheduling (deterministic):
+//   L4r  one thread per row: S[row] = sum of its arcs' occupancies, in row_arc order, and the first two arcs'
+//        (v, occ) (rows with more are flagged)
+//   L5r  warp per row: reads S and the (v, occ) pairs (one hop), issues the row's logit loads, stores
+//        softmax * S with each arc's occ subtracted by the lane owning element v (the scatter, L6, is gone);
+//        flagged rows walk their arcs 32 per warp pass.
+__global__ void __launch_bounds__(256) l4_row_sums(Lat L, const float* __restrict__ w, const double* __restrict__ alpha,
+                                                   const double* __restrict__ beta, const double* __restrict__ logp,
+                                                   const int32_t* __restrict__ row_off,
+                                                   const int32_t* __restrict__ row_arc, const int32_t* __restrict__ T_b,
+                                                   const int32_t* __restrict__ U_b, int Tmax, int Umax,
+                                                   float* __restrict__ rowS, float4* __restrict__ rowfix, int b0, int nb) {
+    const int Up1 = Umax + 1;
+    const int64_t cells = static_cast<int64_t>(Tmax) * Up1;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nb * cells;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int b = b0 + static_cast<int>(i / cells);
+        const int r = static_cast<int>(i - (b - b0) * cells);
+        const int t = r / Up1, u = r - t * Up1;
+        const int64_t row = static_cast<int64_t>(b) * cells + r;
+        const double lP = logp[b];
+        float S = 0.f;
+        // the row's arcs for L5r: (v0, occ0, v1, occ1) as bit patterns; v0 = -2: more than two arcs (generic)
+        float4 fx = make_float4(__int_as_float(-1), 0.f, __int_as_float(-1), 0.f);
+        if (t < T_b[b] && u <= U_b[b] && isfinite(lP)) {
+            const int k0 = row_off[row], k1 = row_off[row + 1];
+            for (int k = k0; k < k1; ++k) {
+                const int a = row_arc[k];
+                const float o = arc_occ(L, w, alpha, beta, lP, a);
+                S += o;
+                if (k == k0) fx = make_float4(__int_as_float(L.v[a]), o, fx.z, fx.w);
+                if (k == k0 + 1) fx = make_float4(fx.x, fx.y, __int_as_float(L.v[a]), o);
+            }
+            if (k1 - k0 > 2) fx.x = __int_as_float(-2);
+        }
+        rowS[row] = S;
+        rowfix[row] = fx;
+    }
+}
+
+__global__ void __launch_bounds__(256) l5_rows_fused(const float* logits, const float* __restrict__ lse, Lat L,
+                                                     const float* __restrict__ w, const double* __restrict__ alpha,
+                                                     const double* __restrict__ beta, const float* __restrict__ rowS,
+                                                     const float4* __restrict__ rowfix,
+                                                     const int32_t* __restrict__ row_off,
+                                                     const int32_t* __restrict__ row_arc, const int32_t* __restrict__ T_b,
+                                                     const int32_t* __restrict__ U_b, const double* __restrict__ logp,
+                                                     int Tmax, int Umax, int V, float* grads, bool vec4, int b0) {
+    const int lane = threadIdx.x & 31;
+    const int b = b0 + blockIdx.y;
+    const int Up1 = Umax + 1;
+    const int r = static_cast<int>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    if (r >= Tmax * Up1) return;
+    const int t = r / Up1, u = r - t * Up1;
+    const int64_t row = static_cast<int64_t>(b) * Tmax * Up1 + r;
+    const double lP = logp[b];
+    const bool live = t < T_b[b] && u <= U_b[b] && isfinite(lP);
+    const float S = live ? rowS[row] : 0.f;
+    const float l = live ? lse[row] : 0.f;
+    const float* zr = logits + row * V;
+    float* gr = grads + row * V;
+    const bool on = live && S != 0.f && l != -INFINITY;
+    const float ll = l * kLog2e;
+    const int nv = V >> 2;
+    float4 x[8];
+    if (vec4) {  // the first chunk's loads go out before the arc fetches below
+        const float4* z4 = reinterpret_cast<const float4*>(zr);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int i = j * 32 + lane;
+            if (on && i < nv) x[j] = z4[i];
+        }
+    }
+    const float4 fx = live ? rowfix[row] : make_float4(__int_as_float(-1), 0.f, __int_as_float(-1), 0.f);
+    const int fv0 = __float_as_int(fx.x), fv1 = __float_as_int(fx.z);
+    const bool generic = fv0 == -2;  // more than two bound arcs: the row index, 32 arcs per warp pass
+    const int k0 = generic ? row_off[row] : 0, k1 = generic ? row_off[row + 1] : 0;
+    const int a0 = (k0 + lane < k1) ? row_arc[k0 + lane] : -1;
+    const int va0 = a0 >= 0 ? L.v[a0] : -1;
+    const float oa0 = a0 >= 0 ? arc_occ(L, w, alpha, beta, lP, a0) : 0.f;
+    // subtract the row's arcs' occupancies from the count (<= 4) elements [first, first + count) held in g
+    auto sub_arcs = [&](float (&g)[4], int first, int count) {
+        for (int kb = k0; kb < k1; kb += 32) {
+            int va = va0;
+            float oa = oa0;
+            if (kb > k0) {  // rows with more than 32 bound arcs: later groups on the fly
+                const int a = kb + lane < k1 ? row_arc[kb + lane] : -1;
+                va = a >= 0 ? L.v[a] : -1;
+                oa = a >= 0 ? arc_occ(L, w, alpha, beta, lP, a) : 0.f;
+            }
+            const int n = min(32, k1 - kb);
+            for (int i = 0; i < n; ++i) {
+                const int vi = __shfl_sync(0xffffffffu, va, i);
+                const float oi = __shfl_sync(0xffffffffu, oa, i);
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    if (c < count && vi == first + c) g[c] -= oi;
+            }
+        }
+    };
+    if (vec4) {
+        const float4* z4 = reinterpret_cast<const float4*>(zr);
+        float4* g4 = reinterpret_cast<float4*>(gr);
+        for (int base = 0; base < nv; base += 256) {
+            if (base > 0) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int i = base + j * 32 + lane;
+                    if (on && i < nv) x[j] = z4[i];
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int i = base + j * 32 + lane;
+                float g[4] = {0.f, 0.f, 0.f, 0.f};
+                if (on && i < nv) {
+                    g[0] = ex2(fmaf(x[j].x, kLog2e, -ll)) * S;
+                    g[1] = ex2(fmaf(x[j].y, kLog2e, -ll)) * S;
+                    g[2] = ex2(fmaf(x[j].z, kLog2e, -ll)) * S;
+                    g[3] = ex2(fmaf(x[j].w, kLog2e, -ll)) * S;
+                }
+                if (generic) {
+                    sub_arcs(g, 4 * i, 4);  // warp-uniform condition
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        if (fv0 == 4 * i + c) g[c] -= fx.y;
+                        if (fv1 == 4 * i + c) g[c] -= fx.w;
+                    }
+                }
+                if (i < nv) g4[i] = make_float4(g[0], g[1], g[2], g[3]);
+            }
+        }
+        return;
+    }
+    for (int i0 = 0; i0 < V; i0 += 32) {
+        const int i = i0 + lane;
+        float g[4] = {(on && i < V) ? ex2((zr[i] - l) * kLog2e) * S : 0.f, 0.f, 0.f, 0.f};
+        if (generic) {
+            sub_arcs(g, i, 1);
+        } else {
+            if (fv0 == i) g[0] -= fx.y;
+            if (fv1 == i) g[0] -= fx.w;
+        }
+        if (i < V) gr[i] = g[0];
+    }
+}
+
 }  // namespace
 
 size_t lattice_workspace_bytes(int64_t B, int64_t Tmax, int64_t Umax, int64_t S, int64_t A) {
     const int64_t rows = B * Tmax * (Umax + 1);
     return align256(sizeof(float) * rows) * 2 + align256(sizeof(float) * A) + 2 * align256(sizeof(double) * S) +
-           align256(sizeof(double) * B) + 2 * align256(sizeof(StateRec) * S);
+           align256(sizeof(double) * B) + 2 * align256(sizeof(StateRec) * S) + align256(sizeof(float4) * rows);
 }
 
 }  // namespace rnnt
@@ -345,7 +494,8 @@ extern "C" rnnt_status rnnt_lattice_loss(const float* logits, const int32_t* log
                                          const int32_t* lvl_off, const int32_t* level_off, const int32_t* in_off,
                                          const int32_t* out_off, const int32_t* out_arc, const int32_t* arc_src,
                                          const int32_t* arc_dst, const int32_t* arc_t, const int32_t* arc_u,
-                                         const int32_t* arc_v, const float* final_w, int num_states, int num_arcs,
+                                         const int32_t* arc_v, const float* final_w, const int32_t* row_off,
+                                         const int32_t* row_arc, int num_states, int num_arcs,
                                          float* losses, float* grads, void* workspace, size_t workspace_bytes,
                                          void* stream) {
     if (B < 0 || Tmax < 1 || Umax < 0 || V < 2 || num_states < 0 || num_arcs < 0) return RNNT_ERR_INVALID_ARG;
@@ -372,6 +522,7 @@ extern "C" rnnt_status rnnt_lattice_loss(const float* logits, const int32_t* log
     double* logp = reinterpret_cast<double*>(take(sizeof(double) * B));
     auto* rec_f = reinterpret_cast<rnnt::StateRec*>(take(sizeof(rnnt::StateRec) * num_states));
     auto* rec_b = reinterpret_cast<rnnt::StateRec*>(take(sizeof(rnnt::StateRec) * num_states));
+    auto* rowfix = reinterpret_cast<float4*>(take(sizeof(float4) * rows));  // row index path: 2 (v, occ) per row
 
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const Lat L{state_off, lvl_off, level_off, in_off, out_off, out_arc, arc_src, arc_dst, arc_t, arc_u, arc_v,
@@ -412,11 +563,19 @@ extern "C" rnnt_status rnnt_lattice_loss(const float* logits, const int32_t* log
                                                                               losses, b0);
         if (nch > 1 && !ok(cudaEventRecord(pool->k2_done[c], a))) return RNNT_ERR_CUDA;
     }
-    // Back half: L4 -> L5 -> L6 per chunk on s.
+    // Back half per chunk on s: with a row index, one fused row pass (L5'); without, L4 -> L5 -> L6.
     for (int c = 0; c < nch; ++c) {
         const int b0 = cb0[c], nb = cb0[c + 1] - b0;
         if (nch > 1 && !ok(cudaStreamWaitEvent(s, pool->k2_done[c], 0))) return RNNT_ERR_CUDA;
         if (!grads) continue;
+        if (row_off) {
+            rnnt::l4_row_sums<<<592, 256, 0, s>>>(L, w, alpha, beta, logp, row_off, row_arc, logit_lens, target_lens,
+                                                  Tmax, Umax, rowS, rowfix, b0, nb);
+            rnnt::l5_rows_fused<<<dim3(static_cast<unsigned>(bx), nb), 256, 0, s>>>(
+                logits, lse, L, w, alpha, beta, rowS, rowfix, row_off, row_arc, logit_lens, target_lens, logp, Tmax,
+                Umax, V, grads, vec4, b0);
+            continue;
+        }
         if (!ok(cudaMemsetAsync(rowS + b0 * cells, 0, sizeof(float) * nb * cells, s))) return RNNT_ERR_CUDA;
         const dim3 arc_grid(64, nb);
         rnnt::l46_occupancy<false><<<arc_grid, 256, 0, s>>>(L, w, alpha, beta, logp, Tmax, Umax, V, rowS, grads, b0);

@@ -52,6 +52,21 @@ class LatticeBatch:
         return [(int(self.arc_src[i]) - s0, int(self.arc_dst[i]) - s0, int(self.arc_t[i]), int(self.arc_u[i]),
                  int(self.arc_v[i])) for i in range(a0, a1)]
 
+    def row_index(self, Tmax: int, Umax: int):
+        """(row_off [B*Tmax*(Umax+1) + 1], row_arc): the arcs bound to logits row (b, t, u), row index
+        (b*Tmax + t)*(Umax+1) + u, in arc order -- lets the engine form each row's gradient in one pass."""
+        Up1 = Umax + 1
+        b_of_state = np.repeat(np.arange(self.B), np.diff(self.state_off))
+        b = b_of_state[self.arc_src]
+        bound = self.arc_v >= 0
+        rows = (b.astype(np.int64) * Tmax + self.arc_t) * Up1 + self.arc_u
+        arcs = np.nonzero(bound)[0]
+        order = np.argsort(rows[arcs], kind="stable")
+        row_arc = arcs[order].astype(np.int32)
+        counts = np.bincount(rows[arcs], minlength=self.B * Tmax * Up1)
+        row_off = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
+        return row_off, row_arc
+
     def final_of(self, b):
         s0, s1 = int(self.state_off[b]), int(self.state_off[b + 1])
         return {s - s0: float(self.final_w[s]) for s in range(s0, s1) if np.isfinite(self.final_w[s])}

@@ -99,3 +99,21 @@ def test_engine_schedule_paths(rb, lat, shape, variant):
     ref_l, ref_g = oracle.batch(pb["logits"].numpy(), pb["targets"], pb["logit_lens"], pb["target_lens"], 0,
                                 variant)
     _close(losses.cpu().numpy().astype(np.float64), grads.cpu().numpy(), ref_l, ref_g)
+
+
+def test_row_index_path_is_deterministic_and_matches_atomic_path(rb, lat):
+    """The row-index gradient pass (no atomics) equals the float-atomic passes and repeats bit for bit."""
+    cfg = workloads.random_config(3, 50, 17, 200, seed=63, variant="force_final")
+    pb = workloads.problem(cfg)
+    L = lat.grid_lattices(pb["logit_lens"], pb["target_lens"], pb["targets"], 0, "force_final")
+    z = pb["logits"].cuda()
+    B, Tmax, Up1, V = z.shape
+    d_rows = rb.lattice_to_device(L, "cuda", Tmax, Up1 - 1)
+    d_atom = rb.lattice_to_device(L, "cuda")
+    l1, g1 = rb.rnnt_lattice_loss(z, d_rows, pb["logit_lens"], pb["target_lens"])
+    l2, g2 = rb.rnnt_lattice_loss(z, d_rows, pb["logit_lens"], pb["target_lens"])
+    l3, g3 = rb.rnnt_lattice_loss(z, d_atom, pb["logit_lens"], pb["target_lens"])
+    torch.cuda.synchronize()
+    assert torch.equal(g1, g2) and torch.equal(l1, l2)
+    assert torch.equal(l1, l3)
+    assert (g1 - g3).abs().max().item() <= 1e-6
