@@ -127,3 +127,27 @@ def test_joint_loss_grad_matches_oracle(rb, shape, variant):
     for name, mine, r in zip(("d_enc", "d_pred", "d_weight", "d_bias"), out[1:], ref[1:]):
         err = np.abs(mine.cpu().numpy().astype(np.float64) - r).max()
         assert err <= 2e-3 * np.abs(r).max(), (name, err, np.abs(r).max())
+
+
+def test_joint_edge_cases(rb):
+    """T = 1, U = 0 and an invalid length in one batch; B = 0 is a no-op."""
+    H, V = 128, 128
+    enc, pred, W, b = workloads.joint_inputs(3, 5, 3, H, V, seed=37)
+    y = np.array([[1, 2, 3], [4, 5, 6], [7, 8, 9]], np.int32)
+    T_b = np.array([1, 5, 6], np.int32)   # utterance 2: T > Tmax -> NaN loss, zero gradients
+    U_b = np.array([3, 0, 2], np.int32)
+    l = rb.rnnt_joint_loss(enc.cuda(), pred.cuda(), W.cuda(), b.cuda(), y, T_b, U_b, 0, "allow_ignore")
+    out = rb.rnnt_joint_loss_grad(enc.cuda(), pred.cuda(), W.cuda(), b.cuda(), y, T_b, U_b, 0, "allow_ignore")
+    torch.cuda.synchronize()
+    ref = oj.joint_loss_and_grads(enc[:2].double().numpy(), pred[:2].double().numpy(), W.double().numpy(),
+                                  b.double().numpy(), y[:2], T_b[:2], U_b[:2], 0, "allow_ignore")
+    lg = l.cpu().numpy().astype(np.float64)
+    assert np.isnan(lg[2]) and np.isnan(out[0][2].item())
+    assert (np.abs(lg[:2] - ref[0]) / np.maximum(np.abs(ref[0]), 1.0)).max() <= 1e-5
+    assert not out[1][2].any() and not out[2][2].any()
+    # the two valid utterances' gradients; W / bias gradients get nothing from the invalid one
+    for mine, r in ((out[1][:2], ref[1]), (out[2][:2], ref[2]), (out[3], ref[3]), (out[4], ref[4])):
+        assert np.abs(mine.cpu().numpy().astype(np.float64) - r).max() <= 2e-3 * np.abs(r).max()
+    e = torch.zeros(0, 5, H, dtype=torch.bfloat16, device="cuda")
+    p = torch.zeros(0, 4, H, dtype=torch.bfloat16, device="cuda")
+    assert rb.rnnt_joint_loss(e, p, W.cuda(), b.cuda(), np.zeros((0, 3), np.int32), [], []).numel() == 0
