@@ -54,6 +54,17 @@ struct Elem<__nv_bfloat16> {
         }
         return make_uint4(w[0], w[1], w[2], w[3]);
     }
+    // 64-bit vectors (4 elements): rows whose length is a multiple of 4 but not of 8 (e.g. V = 500)
+    __device__ __forceinline__ static void unpack(const uint2& v, float (&f)[4]) {
+        f[0] = __uint_as_float(v.x << 16);
+        f[1] = __uint_as_float(v.x & 0xffff0000u);
+        f[2] = __uint_as_float(v.y << 16);
+        f[3] = __uint_as_float(v.y & 0xffff0000u);
+    }
+    __device__ __forceinline__ static uint2 pack(const float (&f)[4]) {
+        const __nv_bfloat162 a = __floats2bfloat162_rn(f[0], f[1]), b = __floats2bfloat162_rn(f[2], f[3]);
+        return make_uint2(*reinterpret_cast<const uint32_t*>(&a), *reinterpret_cast<const uint32_t*>(&b));
+    }
     __device__ __forceinline__ static float to_f32(__nv_bfloat16 x) { return __bfloat162float(x); }
     __device__ __forceinline__ static __nv_bfloat16 from_f32(float x) { return __float2bfloat16_rn(x); }
 };
@@ -78,6 +89,18 @@ struct Elem<__half> {
             w[i] = *reinterpret_cast<const uint32_t*>(&h);
         }
         return make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    __device__ __forceinline__ static void unpack(const uint2& v, float (&f)[4]) {
+        const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&v.x));
+        const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&v.y));
+        f[0] = a.x;
+        f[1] = a.y;
+        f[2] = b.x;
+        f[3] = b.y;
+    }
+    __device__ __forceinline__ static uint2 pack(const float (&f)[4]) {
+        const __half2 a = __floats2half2_rn(f[0], f[1]), b = __floats2half2_rn(f[2], f[3]);
+        return make_uint2(*reinterpret_cast<const uint32_t*>(&a), *reinterpret_cast<const uint32_t*>(&b));
     }
     __device__ __forceinline__ static float to_f32(__half x) { return __half2float(x); }
     __device__ __forceinline__ static __half from_f32(float x) { return __float2half_rn(x); }
@@ -104,6 +127,34 @@ __device__ __forceinline__ void stv(uint4* p, const uint4& v, uint64_t pol) {
                  "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol)
                  : "memory");
 }
+// 64-bit variants (16-bit rows with V % 8 == 4)
+__device__ __forceinline__ uint2 ldv_ro(const uint2* p, uint64_t pol) {
+    uint2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
+                 : "=r"(v.x), "=r"(v.y)
+                 : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ uint2 ldv(const uint2* p, uint64_t pol) {
+    uint2 v;
+    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
+                 : "=r"(v.x), "=r"(v.y)
+                 : "l"(p), "l"(pol)
+                 : "memory");
+    return v;
+}
+__device__ __forceinline__ void stv(uint2* p, const uint2& v, uint64_t pol) {
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.u32 [%0], {%1,%2}, %3;" ::"l"(p), "r"(v.x), "r"(v.y),
+                 "l"(pol)
+                 : "memory");
+}
+template <typename VecT>
+__device__ __forceinline__ VecT zero_vec();
+template <>
+__device__ __forceinline__ uint4 zero_vec<uint4>() { return make_uint4(0u, 0u, 0u, 0u); }
+template <>
+__device__ __forceinline__ uint2 zero_vec<uint2>() { return make_uint2(0u, 0u); }
+
 template <typename T>
 __device__ __forceinline__ float lds_scalar(const T* p) {  // scalar read-only load, widened to fp32
     return Elem<T>::to_f32(__ldg(p));

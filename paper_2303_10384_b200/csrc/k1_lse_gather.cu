@@ -153,12 +153,12 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32, 4)
 // the per-row overhead (index math, gathers, butterflies, stores) per byte.  Measured c3 bf16: 0.882 ->
 // 0.865 ms (A/B).  16-bit K1 stays at ~3.8 TB/s: with half the bytes per element it is bound by the one
 // ex2 per element (MUFU ~55 % busy, issue ~67 %) and latency, not by HBM (46 % of peak).
-template <typename Z>
+template <typename Z, typename VecT>
 __global__ void __launch_bounds__(kRowWarpsPerBlock * 32, 3)
     k1_lse_gather_w2(const Z* __restrict__ logits, const int32_t* __restrict__ targets,
                      const int32_t* __restrict__ T_b, const int32_t* __restrict__ U_b, int b0, int Tmax, int Umax,
                      int V, int blank, float* __restrict__ lse_out, double2* __restrict__ lp_out) {
-    constexpr int E = Elem<Z>::kPerVec, kU = kPerLane / E;
+    constexpr int E = static_cast<int>(sizeof(VecT) / sizeof(Z)), kU = kPerLane / E;
     const int lane = threadIdx.x & 31;
     const int b = b0 + static_cast<int>(blockIdx.y);
     const int Up1 = Umax + 1;
@@ -178,15 +178,15 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32, 3)
     const int64_t row0 = static_cast<int64_t>(b) * Tmax * Up1 + r0;
     const uint64_t pol = l2_evict_first();
     const int nvec = V / E;
-    const uint4* row4[2] = {reinterpret_cast<const uint4*>(logits + row0 * static_cast<int64_t>(V)),
-                            reinterpret_cast<const uint4*>(logits + (row0 + 1) * static_cast<int64_t>(V))};
-    uint4 raw[2][kU];
+    const VecT* row4[2] = {reinterpret_cast<const VecT*>(logits + row0 * static_cast<int64_t>(V)),
+                            reinterpret_cast<const VecT*>(logits + (row0 + 1) * static_cast<int64_t>(V))};
+    VecT raw[2][kU];
 #pragma unroll
     for (int k = 0; k < 2; ++k)
 #pragma unroll
         for (int j = 0; j < kU; ++j) {
             const int i = j * 32 + lane;
-            raw[k][j] = (live[k] && i < nvec) ? ldv_ro(row4[k] + i, pol) : make_uint4(0u, 0u, 0u, 0u);
+            raw[k][j] = (live[k] && i < nvec) ? ldv_ro(row4[k] + i, pol) : zero_vec<VecT>();
         }
     int yv[2];
     bool ybad[2];
@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32, 3)
 #pragma unroll
                 for (int j = 0; j < kU; ++j) {
                     const int i = base + j * 32 + lane;
-                    raw[k][j] = (live[k] && i < nvec) ? ldv_ro(row4[k] + i, pol) : make_uint4(0u, 0u, 0u, 0u);
+                    raw[k][j] = (live[k] && i < nvec) ? ldv_ro(row4[k] + i, pol) : zero_vec<VecT>();
                 }
         }
         const bool partial = base + 32 * kU > nvec;  // warp-uniform
@@ -437,13 +437,18 @@ cudaError_t launch_t(const Problem& p, const Workspace& w, cudaStream_t s) {
         }
         return cudaGetLastError();
     }
-    if constexpr (sizeof(Z) == 2) {  // 16-bit wide rows: two rows per warp
-      if (vec) {
+    if constexpr (sizeof(Z) == 2) {  // 16-bit wide rows: two rows per warp, 128-bit or (V % 8 == 4) 64-bit loads
+      const bool vec8 = (p.V % 4 == 0) && (reinterpret_cast<uintptr_t>(z) % 8 == 0);
+      if (vec || vec8) {
         const int64_t bx2 = (rows_per_utt + 2 * kRowWarpsPerBlock - 1) / (2 * kRowWarpsPerBlock);
         for (int b0 = 0; b0 < p.B; b0 += 65535) {
             const dim3 grid(static_cast<unsigned>(bx2), static_cast<unsigned>(min(65535, p.B - b0)));
-            k1_lse_gather_w2<Z><<<grid, kRowWarpsPerBlock * 32, 0, s>>>(z, p.targets, p.T_b, p.U_b, b0, p.Tmax,
-                                                                     p.Umax, p.V, p.blank, w.lse, w.lp);
+            if (vec)
+                k1_lse_gather_w2<Z, uint4><<<grid, kRowWarpsPerBlock * 32, 0, s>>>(z, p.targets, p.T_b, p.U_b, b0,
+                                                                                p.Tmax, p.Umax, p.V, p.blank, w.lse, w.lp);
+            else
+                k1_lse_gather_w2<Z, uint2><<<grid, kRowWarpsPerBlock * 32, 0, s>>>(z, p.targets, p.T_b, p.U_b, b0,
+                                                                                p.Tmax, p.Umax, p.V, p.blank, w.lse, w.lp);
         }
         return cudaGetLastError();
       }

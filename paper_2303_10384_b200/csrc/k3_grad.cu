@@ -23,7 +23,7 @@ namespace {
 
 constexpr int kPerLane = 32;  // elements per lane per chunk
 
-template <typename Z, bool kVec>
+template <typename Z, bool kVec, typename VecT = uint4>
 __global__ void __launch_bounds__(kRowWarpsPerBlock * 32)
     k3_grad_w(const Z* logits, const int32_t* __restrict__ targets, const int32_t* __restrict__ T_b,
             const int32_t* __restrict__ U_b, int b0, int Tmax, int Umax, int V, int blank,
@@ -45,13 +45,13 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32)
     const int64_t row = static_cast<int64_t>(b) * Tmax * Up1 + r;
     Z* grow = grads + row * static_cast<int64_t>(V);
     const Z* zrow = logits + row * static_cast<int64_t>(V);
-    constexpr int E = Elem<Z>::kPerVec;
+    constexpr int E = static_cast<int>(sizeof(VecT) / sizeof(Z));
 
     if (!live) {
         if constexpr (kVec) {
             const uint64_t pol = l2_evict_first();
-            uint4* g4 = reinterpret_cast<uint4*>(grow);
-            for (int i = lane; i < V / E; i += 32) stv(g4 + i, make_uint4(0u, 0u, 0u, 0u), pol);
+            VecT* g4 = reinterpret_cast<VecT*>(grow);
+            for (int i = lane; i < V / E; i += 32) stv(g4 + i, zero_vec<VecT>(), pol);
         } else {
             for (int i = lane; i < V; i += 32) grow[i] = Elem<Z>::from_f32(0.f);
         }
@@ -60,9 +60,9 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32)
 
     constexpr int kU = kPerLane / E;
     const uint64_t pol = l2_evict_first();
-    const uint4* z4 = reinterpret_cast<const uint4*>(zrow);
+    const VecT* z4 = reinterpret_cast<const VecT*>(zrow);
     const int nvec = V / E;
-    uint4 raw[kU];
+    VecT raw[kU];
     if constexpr (kVec) {  // issue the row's first chunk before the per-row scalars: both latencies overlap
 #pragma unroll
         for (int j = 0; j < kU; ++j) {
@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32)
     const float lsel = (lse == -INFINITY) ? INFINITY : lse * kLog2e;  // all -inf row -> p = 0
 
     if constexpr (kVec) {
-        uint4* g4 = reinterpret_cast<uint4*>(grow);
+        VecT* g4 = reinterpret_cast<VecT*>(grow);
         const int bq = blank / E, yq = (yv < 0) ? -1 : (yv / E);
         const int bk = blank % E, yk = (yv < 0) ? 0 : (yv % E);
         const f32x2 l2e = pk(kLog2e, kLog2e), nl = pk(-lsel, -lsel), g2 = pk(gam, gam);
@@ -280,10 +280,18 @@ cudaError_t launch_t(const Problem& p, const Workspace& w, cudaStream_t s) {
         }
         return cudaGetLastError();
     }
+    // 16-bit rows whose length is a multiple of 4 but not of 8 (e.g. V = 500): 64-bit vectors
+    const bool vec8 = !vec && sizeof(Z) == 2 && (p.V % 4 == 0) && (reinterpret_cast<uintptr_t>(z) % 8 == 0) &&
+                      (reinterpret_cast<uintptr_t>(g) % 8 == 0);
     const int64_t bx = (rows_per_utt + kRowWarpsPerBlock - 1) / kRowWarpsPerBlock;
     for (int b0 = 0; b0 < p.B; b0 += 65535) {
         const dim3 grid(static_cast<unsigned>(bx), static_cast<unsigned>(min(65535, p.B - b0)));
-        if (vec)
+        if (vec8) {
+            if constexpr (sizeof(Z) == 2)
+                k3_grad_w<Z, true, uint2><<<grid, kRowWarpsPerBlock * 32, 0, s>>>(
+                    z, p.targets, p.T_b, p.U_b, b0, p.Tmax, p.Umax, p.V, p.blank, p.grad_scale, w.lse, w.lp, w.alpha,
+                    w.beta, w.logp, g);
+        } else if (vec)
             k3_grad_w<Z, true><<<grid, kRowWarpsPerBlock * 32, 0, s>>>(
                 z, p.targets, p.T_b, p.U_b, b0, p.Tmax, p.Umax, p.V, p.blank, p.grad_scale, w.lse, w.lp, w.alpha,
                 w.beta, w.logp, g);

@@ -48,7 +48,8 @@ def _check(rb, pb, variant, dtype, z16=None, grads=True):
     return l, g
 
 
-SHAPES = [(3, 9, 4, 8, 0), (4, 33, 31, 136, 135), (2, 70, 40, 264, 77), (3, 41, 63, 1024, 999), (6, 5, 2, 16, 1)]
+SHAPES = [(3, 9, 4, 8, 0), (4, 33, 31, 136, 135), (2, 70, 40, 264, 77), (3, 41, 63, 1024, 999), (6, 5, 2, 16, 1),
+          (3, 40, 17, 500, 0), (2, 13, 6, 12, 11)]  # the last two: V % 8 == 4 (64-bit vector path; P:124 V = 500)
 
 
 @pytest.mark.parametrize("dtype", (torch.bfloat16, torch.float16), ids=("bf16", "fp16"))
