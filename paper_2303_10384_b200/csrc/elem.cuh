@@ -30,6 +30,14 @@ struct Elem<float> {
         return make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]),
                           __float_as_uint(f[3]));
     }
+    // 64-bit vectors (2 elements): rows whose length is even but not a multiple of 4
+    __device__ __forceinline__ static void unpack(const uint2& v, float (&f)[2]) {
+        f[0] = __uint_as_float(v.x);
+        f[1] = __uint_as_float(v.y);
+    }
+    __device__ __forceinline__ static uint2 pack(const float (&f)[2]) {
+        return make_uint2(__float_as_uint(f[0]), __float_as_uint(f[1]));
+    }
     __device__ __forceinline__ static float to_f32(float x) { return x; }
     __device__ __forceinline__ static float from_f32(float x) { return x; }
 };

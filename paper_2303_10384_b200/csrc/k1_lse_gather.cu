@@ -22,7 +22,7 @@ namespace {
 
 constexpr int kPerLane = 32;  // elements per lane per chunk
 
-template <typename Z, bool kVec>
+template <typename Z, bool kVec, typename VecT = uint4>
 __global__ void __launch_bounds__(kRowWarpsPerBlock * 32, 4)
     k1_lse_gather_w(const Z* __restrict__ logits, const int32_t* __restrict__ targets,
                   const int32_t* __restrict__ T_b, const int32_t* __restrict__ U_b, int b0, int Tmax, int Umax,
@@ -40,11 +40,11 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32, 4)
 
     const int64_t row = static_cast<int64_t>(b) * Tmax * Up1 + r;
     const Z* zrow = logits + row * static_cast<int64_t>(V);
-    constexpr int E = Elem<Z>::kPerVec, kU = kPerLane / E;
+    constexpr int E = static_cast<int>(sizeof(VecT) / sizeof(Z)), kU = kPerLane / E;
     const uint64_t pol = l2_evict_first();
-    const uint4* row4 = reinterpret_cast<const uint4*>(zrow);
+    const VecT* row4 = reinterpret_cast<const VecT*>(zrow);
     const int nvec = V / E;
-    uint4 raw[kU];
+    VecT raw[kU];
     // 16-bit rows: the first chunk goes out before anything that depends on other loads (measured: K1 bf16
     // 0.95 -> 0.88 ms).  fp32 rows keep the loads after the gather (the early issue costs fp32 28 registers
     // and a quarter of its occupancy: measured slower).
@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32, 4)
 #pragma unroll
         for (int j = 0; j < kU; ++j) {
             const int i = j * 32 + lane;
-            raw[j] = (i < nvec) ? ldv_ro(row4 + i, pol) : make_uint4(0u, 0u, 0u, 0u);
+            raw[j] = (i < nvec) ? ldv_ro(row4 + i, pol) : zero_vec<VecT>();
         }
     }
 
@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32, 4)
 #pragma unroll
                 for (int j = 0; j < kU; ++j) {
                     const int i = base + j * 32 + lane;
-                    raw[j] = (i < nvec) ? ldv_ro(row4 + i, pol) : make_uint4(0u, 0u, 0u, 0u);
+                    raw[j] = (i < nvec) ? ldv_ro(row4 + i, pol) : zero_vec<VecT>();
                 }
             }
             float x[kPerLane];
@@ -453,10 +453,14 @@ cudaError_t launch_t(const Problem& p, const Workspace& w, cudaStream_t s) {
         return cudaGetLastError();
       }
     }
+    const bool vec2 = !vec && sizeof(Z) == 4 && (p.V % 2 == 0) && (reinterpret_cast<uintptr_t>(z) % 8 == 0);
     const int64_t bx = (rows_per_utt + kRowWarpsPerBlock - 1) / kRowWarpsPerBlock;
     for (int b0 = 0; b0 < p.B; b0 += 65535) {
         const dim3 grid(static_cast<unsigned>(bx), static_cast<unsigned>(min(65535, p.B - b0)));
-        if (vec)
+        if (vec2)  // fp32 rows with V % 4 == 2: 64-bit vectors
+            k1_lse_gather_w<Z, true, uint2><<<grid, kRowWarpsPerBlock * 32, 0, s>>>(
+                z, p.targets, p.T_b, p.U_b, b0, p.Tmax, p.Umax, p.V, p.blank, w.lse, w.lp);
+        else if (vec)
             k1_lse_gather_w<Z, true><<<grid, kRowWarpsPerBlock * 32, 0, s>>>(
                 z, p.targets, p.T_b, p.U_b, b0, p.Tmax, p.Umax, p.V, p.blank, w.lse, w.lp);
         else

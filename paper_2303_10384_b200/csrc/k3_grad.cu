@@ -280,14 +280,13 @@ cudaError_t launch_t(const Problem& p, const Workspace& w, cudaStream_t s) {
         }
         return cudaGetLastError();
     }
-    // 16-bit rows whose length is a multiple of 4 but not of 8 (e.g. V = 500): 64-bit vectors
-    const bool vec8 = !vec && sizeof(Z) == 2 && (p.V % 4 == 0) && (reinterpret_cast<uintptr_t>(z) % 8 == 0) &&
+    // 64-bit vectors: 16-bit rows with V % 8 == 4 (e.g. V = 500), fp32 rows with V % 4 == 2
+    const bool vec8 = !vec && (p.V % (8 / sizeof(Z)) == 0) && (reinterpret_cast<uintptr_t>(z) % 8 == 0) &&
                       (reinterpret_cast<uintptr_t>(g) % 8 == 0);
     const int64_t bx = (rows_per_utt + kRowWarpsPerBlock - 1) / kRowWarpsPerBlock;
     for (int b0 = 0; b0 < p.B; b0 += 65535) {
         const dim3 grid(static_cast<unsigned>(bx), static_cast<unsigned>(min(65535, p.B - b0)));
         if (vec8) {
-            if constexpr (sizeof(Z) == 2)
                 k3_grad_w<Z, true, uint2><<<grid, kRowWarpsPerBlock * 32, 0, s>>>(
                     z, p.targets, p.T_b, p.U_b, b0, p.Tmax, p.Umax, p.V, p.blank, p.grad_scale, w.lse, w.lp, w.alpha,
                     w.beta, w.logp, g);

@@ -69,7 +69,8 @@ SHAPES = [  # (B, Tmax, Umax, V, blank) -- several tiles of 32 threads / 128 flo
     (3, 9, 4, 8, 0), (4, 33, 31, 129, 128), (2, 70, 40, 260, 77), (5, 41, 63, 1000, 999),
     (3, 17, 96, 64, 5), (2, 120, 200, 36, 3), (6, 5, 2, 2, 1), (2, 300, 33, 512, 0),
     (2, 7, 3, 6000, 4321),   # multi-chunk rows, partial last chunk (vector path)
-    (2, 6, 3, 5001, 17)]     # multi-chunk rows, scalar path
+    (2, 6, 3, 5001, 17),     # multi-chunk rows, scalar path
+    (3, 23, 9, 130, 7), (2, 7, 3, 6002, 11)]  # V % 4 == 2: 64-bit vector path (single / multi-chunk rows)
 
 
 @pytest.mark.parametrize("shape", SHAPES, ids=lambda s: "B{}_T{}_U{}_V{}_b{}".format(*s))
