@@ -163,6 +163,20 @@ __device__ __forceinline__ uint4 zero_vec<uint4>() { return make_uint4(0u, 0u, 0
 template <>
 __device__ __forceinline__ uint2 zero_vec<uint2>() { return make_uint2(0u, 0u); }
 
+// A vector of -inf in storage type Z (fills the slots past V without a per-element select)
+template <typename Z> struct NegInfWord;
+template <> struct NegInfWord<float> { static constexpr uint32_t kWord = 0xff800000u; };
+template <> struct NegInfWord<__nv_bfloat16> { static constexpr uint32_t kWord = 0xff80ff80u; };
+template <> struct NegInfWord<__half> { static constexpr uint32_t kWord = 0xfc00fc00u; };
+template <typename Z, typename VecT>
+__device__ __forceinline__ VecT neg_inf_vec() {
+    constexpr uint32_t w = NegInfWord<Z>::kWord;
+    if constexpr (sizeof(VecT) == 16)
+        return make_uint4(w, w, w, w);
+    else
+        return make_uint2(w, w);
+}
+
 template <typename T>
 __device__ __forceinline__ float lds_scalar(const T* p) {  // scalar read-only load, widened to fp32
     return Elem<T>::to_f32(__ldg(p));
