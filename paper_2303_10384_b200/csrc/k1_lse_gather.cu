@@ -151,7 +151,8 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32, 4)
 // 16-bit wide rows, two rows per warp (k1_lse_gather_w2): a warp loads the first chunk of both its rows
 // before anything else, then finishes the two rows with interleaved reductions (independent chains), halving
 // the per-row overhead (index math, gathers, butterflies, stores) per byte.  Measured c3 bf16: 0.882 ->
-// 0.865 ms (A/B); slots past V loaded as -inf vectors instead of a per-element select: 0.862 -> 0.808 ms.  16-bit K1 stays at ~3.8 TB/s: with half the bytes per element it is bound by the one
+// 0.865 ms (A/B); slots past V set to -inf vectors instead of a per-element select: 0.862 -> 0.808 ms, and
+// only in a partial chunk (no default fill of the load registers): -> 0.753 ms.  16-bit K1 stays at ~3.8 TB/s: with half the bytes per element it is bound by the one
 // ex2 per element (MUFU ~55 % busy, issue ~67 %) and latency, not by HBM (46 % of peak).
 template <typename Z, typename VecT>
 __global__ void __launch_bounds__(kRowWarpsPerBlock * 32, 3)
@@ -181,13 +182,24 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32, 3)
     const VecT* row4[2] = {reinterpret_cast<const VecT*>(logits + row0 * static_cast<int64_t>(V)),
                             reinterpret_cast<const VecT*>(logits + (row0 + 1) * static_cast<int64_t>(V))};
     VecT raw[2][kU];
+    // loads only where in range (no default register fill); a partial chunk gets its -inf slots afterwards
+    auto load_chunk = [&](int base) {
 #pragma unroll
-    for (int k = 0; k < 2; ++k)
+        for (int k = 0; k < 2; ++k)
 #pragma unroll
-        for (int j = 0; j < kU; ++j) {
-            const int i = j * 32 + lane;
-            raw[k][j] = (live[k] && i < nvec) ? ldv_ro(row4[k] + i, pol) : neg_inf_vec<Z, VecT>();
+            for (int j = 0; j < kU; ++j) {
+                const int i = base + j * 32 + lane;
+                if (live[k] && i < nvec) raw[k][j] = ldv_ro(row4[k] + i, pol);
+            }
+        if (base + 32 * kU > nvec) {  // warp-uniform: only a last, partial chunk
+#pragma unroll
+            for (int k = 0; k < 2; ++k)
+#pragma unroll
+                for (int j = 0; j < kU; ++j)
+                    if (base + j * 32 + lane >= nvec) raw[k][j] = neg_inf_vec<Z, VecT>();
         }
+    };
+    load_chunk(0);
     int yv[2];
     bool ybad[2];
     float zb[2] = {0.f, 0.f}, zy[2] = {0.f, 0.f};
@@ -220,15 +232,7 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32, 3)
         m[k] = cm;
     };
     for (int base = 0; base < nvec; base += 32 * kU) {
-        if (base > 0) {
-#pragma unroll
-            for (int k = 0; k < 2; ++k)
-#pragma unroll
-                for (int j = 0; j < kU; ++j) {
-                    const int i = base + j * 32 + lane;
-                    raw[k][j] = (live[k] && i < nvec) ? ldv_ro(row4[k] + i, pol) : neg_inf_vec<Z, VecT>();
-                }
-        }
+        if (base > 0) load_chunk(base);
         // slots past V were loaded as -inf vectors: no per-element select
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
