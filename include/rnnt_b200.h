@@ -200,7 +200,8 @@ rnnt_status rnnt_joint_viterbi(const void* enc, const void* pred, const void* we
 /* Training step of the fused joint (NEXT-4 backward; R22, R23): losses as rnnt_joint_loss, and the
  * gradients of sum_b losses[b] with respect to the joint's inputs, fp32 row-major:
  *   d_enc [B][Tmax][H], d_pred [B][Umax+1][H] (zero on padded frames / units), d_weight [V][H], d_bias [V]
- *   (or NULL).  dz = d loss / d z is formed on chip from the recomputed logits (K3's formula) and stored in bf16
+ *   (or NULL); grad_scale [B] or NULL: gradients of sum_b grad_scale[b] * losses[b] (1/B gives the mean),
+ *   as rnnt_loss.  dz = d loss / d z is formed on chip from the recomputed logits (K3's formula) and stored in bf16
  *   for the two backward GEMMs (dh = dz W stored in bf16, dW = dz^T h; cuBLAS, fp32 accumulation); tanh' uses
  *   the stored bf16 h.  workspace: rnnt_joint_grad_workspace_bytes(...) bytes (it holds dz, h and dh of every
  *   padded cell: ~ (2 V + 4 H) bytes per cell).  Same constraints as rnnt_joint_loss. */
@@ -208,8 +209,8 @@ size_t rnnt_joint_grad_workspace_bytes(int B, int Tmax, int Umax, int H, int V);
 rnnt_status rnnt_joint_loss_grad(const void* enc, const void* pred, const void* weight, const float* bias,
                                  const int32_t* targets, const int32_t* logit_lens, const int32_t* target_lens,
                                  int B, int Tmax, int Umax, int H, int V, int blank, int variant, float* losses,
-                                 float* d_enc, float* d_pred, float* d_weight, float* d_bias, void* workspace,
-                                 size_t workspace_bytes, void* stream);
+                                 float* d_enc, float* d_pred, float* d_weight, float* d_bias,
+                                 const float* grad_scale, void* workspace, size_t workspace_bytes, void* stream);
 
 const char* rnnt_status_string(rnnt_status status);
 

@@ -57,7 +57,7 @@ def _load():
         "rnnt_joint_loss_ex": ([P, P, P, P, P, P, P, I, I, I, I, I, I, I, P, P, S, P, P], I),
         "rnnt_joint_viterbi": ([P, P, P, P, P, P, P, I, I, I, I, I, I, I, P, P, P, P, S, P], I),
         "rnnt_joint_grad_workspace_bytes": ([I, I, I, I, I], S),
-        "rnnt_joint_loss_grad": ([P, P, P, P, P, P, P, I, I, I, I, I, I, I, P, P, P, P, P, P, S, P], I),
+        "rnnt_joint_loss_grad": ([P, P, P, P, P, P, P, I, I, I, I, I, I, I, P, P, P, P, P, P, P, S, P], I),
         "rnnt_status_string": ([I], ctypes.c_char_p),
         "rnnt_version": ([], ctypes.c_char_p),
     }
@@ -243,11 +243,12 @@ def rnnt_joint_loss(enc, pred, weight, bias, targets, logit_lens, target_lens, b
 
 
 def rnnt_joint_loss_grad(enc, pred, weight, bias, targets, logit_lens, target_lens, blank=0, variant="rnnt",
-                         workspace=None, stream=None, outputs=None):
+                         workspace=None, stream=None, outputs=None, grad_scale=None):
     """Training step of the fused joint (NEXT-4 backward): returns (losses [B], d_enc [B, Tmax, H],
     d_pred [B, Umax+1, H], d_weight [V, H], d_bias [V]), the gradients (fp32) of sum(losses).  Inputs as
     rnnt_joint_loss; bias may be None (then d_bias is still returned, for a zero bias).  outputs: optional
-    preallocated (losses, d_enc, d_pred, d_weight, d_bias) fp32 tensors of those shapes."""
+    preallocated (losses, d_enc, d_pred, d_weight, d_bias) fp32 tensors of those shapes.  grad_scale: optional
+    [B] per-utterance weights (gradients of sum_b grad_scale[b] * losses[b]; 1/B gives the mean)."""
     for name, x in (("enc", enc), ("pred", pred), ("weight", weight)):
         if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.bfloat16 and x.is_contiguous()):
             raise TypeError(f"{name} must be a contiguous CUDA bfloat16 tensor (no CPU fallback)")
@@ -270,10 +271,13 @@ def rnnt_joint_loss_grad(enc, pred, weight, bias, targets, logit_lens, target_le
     if workspace is None:
         need = int(library.rnnt_joint_grad_workspace_bytes(B, Tmax, Umax, H, V))
         workspace = torch.empty(max(need, 1), dtype=torch.uint8, device=dev)
+    if grad_scale is not None:
+        grad_scale = grad_scale.to(device=dev, dtype=torch.float32).contiguous()
     _check(library.rnnt_joint_loss_grad(_ptr(enc), _ptr(pred), _ptr(weight), _ptr(bias), _ptr(targets),
                                         _ptr(logit_lens), _ptr(target_lens), B, Tmax, Umax, H, V, int(blank),
                                         VARIANTS[variant], _ptr(losses), _ptr(d_enc), _ptr(d_pred), _ptr(d_weight),
-                                        _ptr(d_bias), _ptr(workspace), workspace.numel(), _stream(stream)))
+                                        _ptr(d_bias), _ptr(grad_scale), _ptr(workspace), workspace.numel(),
+                                        _stream(stream)))
     return losses, d_enc, d_pred, d_weight, d_bias
 
 

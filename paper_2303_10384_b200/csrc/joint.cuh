@@ -18,6 +18,7 @@ struct GradIO {
     const double* alpha;
     const double* beta;
     const double* logp;
+    const float* grad_scale;  // [B] or nullptr (= 1): dz of utterance b is scaled by it (e.g. 1/B for a mean)
     __nv_bfloat16* dz;
     __nv_bfloat16* h;
 };

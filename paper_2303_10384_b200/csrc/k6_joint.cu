@@ -248,6 +248,7 @@ struct JointArgs {
     const double* alpha;
     const double* beta;
     const double* logp;
+    const float* grad_scale;
     __nv_bfloat16* dz_out;  // [rows][Vp] row-major, Vp = V rounded up to whole N tiles (tail columns 0)
     __nv_bfloat16* h_out;   // [rows][H + kJointHPad]: h, then (1, 0, ..., 0)
 };
@@ -431,6 +432,11 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
                     if (u < U) {
                         sy = __expf(static_cast<float>(al + l.y + a.beta[dcell + Up1 + 1] - lP));
                         gy = yv;
+                    }
+                    if (a.grad_scale) {
+                        const float sc = a.grad_scale[b];
+                        sb *= sc;
+                        sy *= sc;
                     }
                     gam = sb + sy;
                     lsel = (lse == -INFINITY) ? INFINITY : lse * kLog2e;  // an all -inf row: p = 0
@@ -830,13 +836,14 @@ rnnt_status joint_front(const void* enc, const void* pred, const void* weight, c
     JointArgs args{static_cast<const __nv_bfloat16*>(enc), static_cast<const __nv_bfloat16*>(pred), bias, targets,
                    logit_lens, target_lens, B, Tmax, Umax, H, V, blank,
                    static_cast<int64_t>(B) * Tmax * (Umax + 1), stages, rowmap, nrows, 0, nullptr, w.lse, w.lp,
-                   nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+                   nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     if (g) {
         args.lse_in = g->lse;
         args.lp_in = g->lp;
         args.alpha = g->alpha;
         args.beta = g->beta;
         args.logp = g->logp;
+        args.grad_scale = g->grad_scale;
         args.dz_out = g->dz;
         args.h_out = g->h;
     }

@@ -162,8 +162,8 @@ extern "C" rnnt_status rnnt_joint_loss_grad(const void* enc, const void* pred, c
                                             const int32_t* targets, const int32_t* logit_lens,
                                             const int32_t* target_lens, int B, int Tmax, int Umax, int H, int V,
                                             int blank, int variant, float* losses, float* d_enc, float* d_pred,
-                                            float* d_weight, float* d_bias, void* workspace,
-                                            size_t workspace_bytes, void* stream) {
+                                            float* d_weight, float* d_bias, const float* grad_scale,
+                                            void* workspace, size_t workspace_bytes, void* stream) {
     using namespace rnnt;
     if (variant < -1 || variant > 1) return RNNT_ERR_INVALID_ARG;
     if (B < 0 || Tmax < 1 || Umax < 0 || H < 1 || V < 2) return RNNT_ERR_INVALID_ARG;
@@ -192,7 +192,7 @@ extern "C" rnnt_status rnnt_joint_loss_grad(const void* enc, const void* pred, c
     Problem p{nullptr, targets, logit_lens, target_lens, B, Tmax, Umax, V, blank, vk, losses, nullptr, nullptr, kF32};
     if (launch_k2_alpha_beta(p, w, s) != cudaSuccess) return RNNT_ERR_CUDA;
     // backward pass 1: z again on the tensor cores -> dz (bf16), h
-    const GradIO g{w.lse, w.lp, w.alpha, w.beta, w.logp, dz, hb};
+    const GradIO g{w.lse, w.lp, w.alpha, w.beta, w.logp, grad_scale, dz, hb};
     st = joint_front(enc, pred, weight, bias, targets, logit_lens, target_lens, B, Tmax, Umax, H, V, blank,
                      workspace, workspace_bytes, s, nullptr, rowmap, nrows, false, &g);
     if (st != RNNT_OK) return st;

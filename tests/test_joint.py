@@ -151,3 +151,26 @@ def test_joint_edge_cases(rb):
     e = torch.zeros(0, 5, H, dtype=torch.bfloat16, device="cuda")
     p = torch.zeros(0, 4, H, dtype=torch.bfloat16, device="cuda")
     assert rb.rnnt_joint_loss(e, p, W.cuda(), b.cuda(), np.zeros((0, 3), np.int32), [], []).numel() == 0
+
+
+def test_joint_grad_scale(rb):
+    """grad_scale[b] scales utterance b's contribution: the gradients equal those of the oracle's sum of
+    scaled losses (here: only the gradients change; the losses stay per utterance)."""
+    B, T, U, H, V = 3, 20, 6, 128, 256
+    cfg = workloads.random_config(B, T, U, V, seed=43)
+    T_b, U_b = workloads.lengths(cfg)
+    y = workloads.targets(cfg, U_b)
+    enc, pred, W, b = workloads.joint_inputs(B, T, U, H, V, seed=43)
+    scale = torch.tensor([0.5, 2.0, 0.0])
+    out = rb.rnnt_joint_loss_grad(enc.cuda(), pred.cuda(), W.cuda(), b.cuda(), y, T_b, U_b, 0, "rnnt",
+                                  grad_scale=scale)
+    torch.cuda.synchronize()
+    refs = [oj.joint_loss_and_grads(enc[i:i + 1].double().numpy(), pred[i:i + 1].double().numpy(),
+                                    W.double().numpy(), b.double().numpy(), y[i:i + 1], T_b[i:i + 1], U_b[i:i + 1],
+                                    0, "rnnt") for i in range(B)]
+    d_w = sum(float(scale[i]) * refs[i][3] for i in range(B))
+    assert np.abs(out[3].cpu().numpy() - d_w).max() <= 2e-3 * np.abs(d_w).max()
+    assert not out[1][2].any()  # scale 0: no gradient into utterance 2's encoder frames
+    for i in range(2):
+        r = float(scale[i]) * refs[i][1][0]
+        assert np.abs(out[1][i].cpu().numpy() - r).max() <= 2e-3 * np.abs(r).max()
