@@ -101,3 +101,41 @@ def test_canaries_viterbi_and_lattice(rb):
                             "force_final", grad=False)
     assert np.allclose(losses.cpu().numpy(), ref_l, rtol=1e-5)
     assert np.isfinite(best.cpu().numpy()).all()
+
+
+def test_canaries_fused_joint_forward_and_training_step(rb):
+    """K6 / K6<grad> / K7 / cuBLAS: every input and output buffer of the fused joint between NaN canaries."""
+    from oracle import joint as oj
+    B, T, U, H, V = 3, 26, 9, 256, 500
+    cfg = workloads.random_config(B, T, U, V, seed=75, variant="force_final")
+    T_b, U_b = workloads.lengths(cfg)
+    y = workloads.targets(cfg, U_b)
+    enc, pred, W, bias = workloads.joint_inputs(B, T, U, H, V, seed=75)
+
+    def guarded_copy(x):
+        g = Guarded(x.numel() * x.element_size())
+        v = g.view(x.dtype, tuple(x.shape))
+        v.copy_(x.cuda())
+        return g, v
+
+    ge, e = guarded_copy(enc)
+    gp, p = guarded_copy(pred)
+    gw, w = guarded_copy(W)
+    gb, b = guarded_copy(bias)
+    outs_g = [Guarded(4 * n) for n in (B, B * T * H, B * (U + 1) * H, V * H, V)]
+    shapes = [(B,), (B, T, H), (B, U + 1, H), (V, H), (V,)]
+    outs = tuple(g.view(torch.float32, sh) for g, sh in zip(outs_g, shapes))
+    ws = Guarded(int(rb.library.rnnt_joint_grad_workspace_bytes(B, T, U, H, V)))
+    out = rb.rnnt_joint_loss_grad(e, p, w, b, y, T_b, U_b, 0, "force_final", outputs=outs,
+                                  workspace=ws.view(torch.uint8, (ws.n,)))
+    lf = Guarded(4 * B)
+    l = rb.rnnt_joint_loss(e, p, w, b, y, T_b, U_b, 0, "force_final", losses=lf.view(torch.float32, (B,)),
+                           workspace=ws.view(torch.uint8, (ws.n,)))
+    torch.cuda.synchronize()
+    for g in (ge, gp, gw, gb, ws, lf, *outs_g):
+        assert g.intact()
+    ref = oj.joint_loss_and_grads(enc.double().numpy(), pred.double().numpy(), W.double().numpy(),
+                                  bias.double().numpy(), y, T_b, U_b, 0, "force_final")
+    assert np.allclose(l.cpu().numpy(), ref[0], rtol=1e-5) and np.allclose(out[0].cpu().numpy(), ref[0], rtol=1e-5)
+    for mine, r in zip(out[1:], ref[1:]):
+        assert np.abs(mine.cpu().numpy().astype(np.float64) - r).max() <= 2e-3 * np.abs(r).max()
