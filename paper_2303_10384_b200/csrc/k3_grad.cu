@@ -154,14 +154,14 @@ constexpr int kVecPerLane = 8;  // 128-bit vectors per lane per chunk
 
 // G lanes per (b,t,u) row (G = 4..32, see lanes_per_row): a warp keeps 8 x 128-bit loads per lane in
 // flight whatever V and the storage type, exactly as K1.
-template <typename Z, int G>
+template <typename Z, int G, typename VecT = uint4>
 __global__ void __launch_bounds__(kRowWarpsPerBlock * 32)
     k3_grad_g(const Z* logits, const int32_t* __restrict__ targets, const int32_t* __restrict__ T_b,
             const int32_t* __restrict__ U_b, int b0, int Tmax, int Umax, int V, int blank,
             const float* __restrict__ grad_scale, const float* __restrict__ lse_in,
             const double2* __restrict__ lp_in, const double* __restrict__ alpha,
             const double* __restrict__ beta, const double* __restrict__ logp, Z* grads) {
-    constexpr int E = Elem<Z>::kPerVec, kU = kVecPerLane, kRowsPerWarp = 32 / G;
+    constexpr int E = static_cast<int>(sizeof(VecT) / sizeof(Z)), kU = kVecPerLane, kRowsPerWarp = 32 / G;
     const int lane = threadIdx.x & 31;
     const int sl = lane & (G - 1);
     const int b = b0 + static_cast<int>(blockIdx.y);
@@ -177,16 +177,16 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32)
 
     const int64_t row = static_cast<int64_t>(b) * Tmax * Up1 + r;
     const uint64_t pol = l2_evict_first();
-    uint4* g4 = reinterpret_cast<uint4*>(grads + row * static_cast<int64_t>(V));
-    const uint4* z4 = reinterpret_cast<const uint4*>(logits + row * static_cast<int64_t>(V));
+    VecT* g4 = reinterpret_cast<VecT*>(grads + row * static_cast<int64_t>(V));
+    const VecT* z4 = reinterpret_cast<const VecT*>(logits + row * static_cast<int64_t>(V));
     const int nvec = V / E;
 
     if (!live) {  // padding / invalid / no-path: exact zeros, the logits are never read
-        for (int i = sl; i < nvec; i += G) stv(g4 + i, make_uint4(0u, 0u, 0u, 0u), pol);
+        for (int i = sl; i < nvec; i += G) stv(g4 + i, zero_vec<VecT>(), pol);
         return;
     }
 
-    uint4 raw[kU];
+    VecT raw[kU];
 #pragma unroll
     for (int j = 0; j < kU; ++j) {  // the row's first chunk, issued before the per-row scalars
         const int i = j * G + sl;
@@ -250,13 +250,13 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32)
     }
 }
 
-template <typename Z, int G>
+template <typename Z, int G, typename VecT = uint4>
 void launch_g(const Problem& p, const Workspace& w, cudaStream_t s, const Z* z, Z* g, int64_t rows_per_utt) {
     constexpr int kRowsPerBlock = kRowWarpsPerBlock * (32 / G);
     const int64_t bx = (rows_per_utt + kRowsPerBlock - 1) / kRowsPerBlock;
     for (int b0 = 0; b0 < p.B; b0 += 65535) {
         const dim3 grid(static_cast<unsigned>(bx), static_cast<unsigned>(min(65535, p.B - b0)));
-        k3_grad_g<Z, G><<<grid, kRowWarpsPerBlock * 32, 0, s>>>(z, p.targets, p.T_b, p.U_b, b0, p.Tmax, p.Umax,
+        k3_grad_g<Z, G, VecT><<<grid, kRowWarpsPerBlock * 32, 0, s>>>(z, p.targets, p.T_b, p.U_b, b0, p.Tmax, p.Umax,
                                                                  p.V, p.blank, p.grad_scale, w.lse, w.lp, w.alpha,
                                                                  w.beta, w.logp, g);
     }
@@ -283,6 +283,15 @@ cudaError_t launch_t(const Problem& p, const Workspace& w, cudaStream_t s) {
     // 64-bit vectors: 16-bit rows with V % 8 == 4 (e.g. V = 500), fp32 rows with V % 4 == 2
     const bool vec8 = !vec && (p.V % (8 / sizeof(Z)) == 0) && (reinterpret_cast<uintptr_t>(z) % 8 == 0) &&
                       (reinterpret_cast<uintptr_t>(g) % 8 == 0);
+    const int lanes8 = vec8 ? lanes_per_row(static_cast<int>(p.V / (8 / sizeof(Z)))) : 32;
+    if (vec8 && lanes8 < 32) {  // narrow 64-bit rows: grouped kernel, 8 x 64-bit loads per lane
+        switch (lanes8) {
+            case 4: launch_g<Z, 4, uint2>(p, w, s, z, g, rows_per_utt); break;
+            case 8: launch_g<Z, 8, uint2>(p, w, s, z, g, rows_per_utt); break;
+            default: launch_g<Z, 16, uint2>(p, w, s, z, g, rows_per_utt); break;
+        }
+        return cudaGetLastError();
+    }
     const int64_t bx = (rows_per_utt + kRowWarpsPerBlock - 1) / kRowWarpsPerBlock;
     for (int b0 = 0; b0 < p.B; b0 += 65535) {
         const dim3 grid(static_cast<unsigned>(bx), static_cast<unsigned>(min(65535, p.B - b0)));
