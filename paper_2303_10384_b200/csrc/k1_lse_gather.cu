@@ -433,10 +433,15 @@ cudaError_t launch_t(const Problem& p, const Workspace& w, cudaStream_t s) {
     constexpr int E = Elem<Z>::kPerVec;
     const bool vec = (p.V % E == 0) && (reinterpret_cast<uintptr_t>(z) % 16 == 0);
     const int g = vec ? lanes_per_row(p.V / E) : 32;
-    if (g <= 8) {  // narrow rows: grouped kernel (measured: 16-lane groups lose to one warp per row in K1)
+    // Widest row group: 16 lanes for fp32 (rows of <= 512 elements: p124's V = 500 K1 0.435 -> 0.338 ms),
+    // 8 for 16-bit storage (16-lane groups measured slower than the two-rows-per-warp kernel: bf16 c3 1.09 vs
+    // 0.88 ms).
+    constexpr int gmax = sizeof(Z) == 4 ? 16 : 8;
+    if (g <= gmax) {  // narrow rows: grouped kernel
         switch (g) {
             case 4: launch_g<Z, 4>(p, w, s, z, rows_per_utt); break;
-            default: launch_g<Z, 8>(p, w, s, z, rows_per_utt); break;
+            case 8: launch_g<Z, 8>(p, w, s, z, rows_per_utt); break;
+            default: launch_g<Z, 16>(p, w, s, z, rows_per_utt); break;
         }
         return cudaGetLastError();
     }
