@@ -152,8 +152,7 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32, 4)
 // before anything else, then finishes the two rows with interleaved reductions (independent chains), halving
 // the per-row overhead (index math, gathers, butterflies, stores) per byte.  Measured c3 bf16: 0.882 ->
 // 0.865 ms (A/B); slots past V set to -inf vectors instead of a per-element select: 0.862 -> 0.808 ms, and
-// only in a partial chunk (no default fill of the load registers): -> 0.753 ms.  16-bit K1 stays at ~3.8 TB/s: with half the bytes per element it is bound by the one
-// ex2 per element (MUFU ~55 % busy, issue ~67 %) and latency, not by HBM (46 % of peak).
+// only in a partial chunk (no default fill of the load registers): -> 0.753 ms.
 template <typename Z, typename VecT>
 __global__ void __launch_bounds__(kRowWarpsPerBlock * 32, 3)
     k1_lse_gather_w2(const Z* __restrict__ logits, const int32_t* __restrict__ targets,
@@ -289,12 +288,12 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32, 3)
 
 constexpr int kVecPerLane = 8;  // 128-bit loads per lane per chunk
 
-template <typename Z, int G>
+template <typename Z, int G, typename VecT = uint4>
 __global__ void __launch_bounds__(kRowWarpsPerBlock * 32)
     k1_lse_gather_g(const Z* __restrict__ logits, const int32_t* __restrict__ targets,
                   const int32_t* __restrict__ T_b, const int32_t* __restrict__ U_b, int b0, int Tmax, int Umax,
                   int V, int blank, float* __restrict__ lse_out, double2* __restrict__ lp_out) {
-    constexpr int E = Elem<Z>::kPerVec, kU = kVecPerLane, kRowsPerWarp = 32 / G;
+    constexpr int E = static_cast<int>(sizeof(VecT) / sizeof(Z)), kU = kVecPerLane, kRowsPerWarp = 32 / G;
     const int lane = threadIdx.x & 31;
     const int sl = lane & (G - 1);  // lane within the row group
     const int b = b0 + static_cast<int>(blockIdx.y);
@@ -316,7 +315,7 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32)
 
     const int64_t row = static_cast<int64_t>(b) * Tmax * Up1 + r;
     const Z* zrow = logits + row * static_cast<int64_t>(V);
-    const uint4* row4 = reinterpret_cast<const uint4*>(zrow);
+    const VecT* row4 = reinterpret_cast<const VecT*>(zrow);
     const uint64_t pol = l2_evict_first();
     // Populate gather: lanes 0 / 1 of the group fetch z[blank] / z[y] with scalar loads issued alongside the
     // row's loads (same sectors, merged in L2: no extra DRAM traffic, no register indexing).
@@ -329,11 +328,11 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32)
     float m = -INFINITY;  // lane-local running max
     float s = 0.f;        // lane-local sum of e^(x - m)
     for (int base = 0; base < nvec; base += G * kU) {
-        uint4 raw[kU];
+        VecT raw[kU];
 #pragma unroll
         for (int j = 0; j < kU; ++j) {
             const int i = base + j * G + sl;
-            raw[j] = (live && i < nvec) ? ldv_ro(row4 + i, pol) : make_uint4(0u, 0u, 0u, 0u);
+            raw[j] = (live && i < nvec) ? ldv_ro(row4 + i, pol) : zero_vec<VecT>();
         }
         // Only a partial last chunk needs -inf fill for the slots past V (warp-uniform condition).
         const bool partial = base + G * kU > nvec;
@@ -402,13 +401,13 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32)
     }
 }
 
-template <typename Z, int G>
+template <typename Z, int G, typename VecT = uint4>
 void launch_g(const Problem& p, const Workspace& w, cudaStream_t s, const Z* z, int64_t rows_per_utt) {
     constexpr int kRowsPerBlock = kRowWarpsPerBlock * (32 / G);
     const int64_t bx = (rows_per_utt + kRowsPerBlock - 1) / kRowsPerBlock;
     for (int b0 = 0; b0 < p.B; b0 += 65535) {
         const dim3 grid(static_cast<unsigned>(bx), static_cast<unsigned>(min(65535, p.B - b0)));
-        k1_lse_gather_g<Z, G><<<grid, kRowWarpsPerBlock * 32, 0, s>>>(z, p.targets, p.T_b, p.U_b, b0, p.Tmax,
+        k1_lse_gather_g<Z, G, VecT><<<grid, kRowWarpsPerBlock * 32, 0, s>>>(z, p.targets, p.T_b, p.U_b, b0, p.Tmax,
                                                                        p.Umax, p.V, p.blank, w.lse, w.lp);
     }
 }
@@ -447,6 +446,15 @@ cudaError_t launch_t(const Problem& p, const Workspace& w, cudaStream_t s) {
     }
     if constexpr (sizeof(Z) == 2) {  // 16-bit wide rows: two rows per warp, 128-bit or (V % 8 == 4) 64-bit loads
       const bool vec8 = (p.V % 4 == 0) && (reinterpret_cast<uintptr_t>(z) % 8 == 0);
+      const int g8 = (!vec && vec8) ? lanes_per_row(p.V / 4) : 32;
+      if (g8 < 32) {  // narrow 64-bit rows (e.g. V = 500): row groups, 8 x 64-bit loads per lane
+        switch (g8) {
+            case 4: launch_g<Z, 4, uint2>(p, w, s, z, rows_per_utt); break;
+            case 8: launch_g<Z, 8, uint2>(p, w, s, z, rows_per_utt); break;
+            default: launch_g<Z, 16, uint2>(p, w, s, z, rows_per_utt); break;
+        }
+        return cudaGetLastError();
+      }
       if (vec || vec8) {
         const int64_t bx2 = (rows_per_utt + 2 * kRowWarpsPerBlock - 1) / (2 * kRowWarpsPerBlock);
         for (int b0 = 0; b0 < p.B; b0 += 65535) {
