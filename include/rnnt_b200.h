@@ -177,9 +177,11 @@ rnnt_status rnnt_loss_host(const float* logits_host, const int32_t* targets_host
  * are computed tile by tile on the tensor cores (tcgen05, fp32 accumulation) and reduced on chip to the
  * log-softmax normalizer and the Populate gathers -- the [B,Tmax,Umax+1,V] tensor is never written -- and
  * the losses follow as for rnnt_loss / wrnnt_loss of z (variant: -1 = RNN-T, else a wrnnt_variant).
- *   enc    [B][Tmax][H] bf16, pred [B][Umax+1][H] bf16, weight [V][H] bf16 (16-byte aligned), bias [V] fp32
- *          or NULL (= 0); targets / lens / losses / workspace as for rnnt_loss (rnnt_workspace_bytes).
- * Forward only (losses).  Requires H % 128 == 0 and H <= 512 (else RNNT_ERR_UNSUPPORTED); any V >= 2. */
+ *   enc    [B][Tmax][H] bf16, pred [B][Umax+1][H] bf16, weight [V][H] bf16, bias [V] fp32 or NULL (= 0),
+ *          all four 16-byte aligned (else RNNT_ERR_INVALID_ARG); targets / lens / losses / workspace as for
+ *          rnnt_loss (rnnt_workspace_bytes).
+ * Forward only (losses).  Requires H % 128 == 0 and H <= 512 (else RNNT_ERR_UNSUPPORTED); any V >= 2 (shared
+ * memory does not grow with V: the bias is read from global memory). */
 rnnt_status rnnt_joint_loss(const void* enc, const void* pred, const void* weight, const float* bias,
                             const int32_t* targets, const int32_t* logit_lens, const int32_t* target_lens,
                             int B, int Tmax, int Umax, int H, int V, int blank, int variant, float* losses,

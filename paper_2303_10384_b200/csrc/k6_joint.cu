@@ -261,17 +261,33 @@ struct JointArgs {
 // multicasts it into both CTAs' shared memory (half the W traffic from L2 per SM); the pair walks the same
 // W sequence in lockstep (a stage is refilled once both MMAs released it) and the same number of row tiles
 // (the second CTA's last one may be a dummy past the end).
-template <bool kGrad, int kCl>
+constexpr int kSBiasMaxV = 4096;  // largest V whose bias is staged in shared memory (16 KB)
+
+// bias(v..v+3) from global memory (read-only path; 16-byte aligned, checked by joint_front).  Columns past V
+// (the last N tile's tail, where TMA zero-fills W's missing rows) get -inf: absent from the max and the sum,
+// so V need not be a multiple of the tile.  Warp-uniform branch (v depends only on the column chunk).
+__device__ __forceinline__ float4 bias4(const JointArgs& a, int v) {
+    if (v + 4 <= a.V) return a.bias ? __ldg(reinterpret_cast<const float4*>(a.bias + v)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    float f[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) f[k] = v + k < a.V ? (a.bias ? __ldg(a.bias + v + k) : 0.f) : -INFINITY;
+    return make_float4(f[0], f[1], f[2], f[3]);
+}
+
+// kSB: the bias (padded to whole N tiles with -inf) is staged once in shared memory -- when it is small
+// (Vp <= kSBiasMaxV); else it is read per chunk from global memory (bias4), issued ahead of the TMEM load.
+// Measured: the shared copy is ~14% faster on the forward at V = 1024 (epilogue latency).
+template <bool kGrad, int kCl, bool kSB>
 __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
     k6_joint_lse(const __grid_constant__ CUtensorMap w_map, const JointArgs a) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    // carve: [W stages (1024-aligned)] [A staging 128 x H bf16] [bias V fp32] [barriers] [tmem slot]
+    // carve: [W stages (1024-aligned)] [A staging 128 x H bf16] [epilogue exchange] [barriers] [tmem slot]
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* wst = base;
     uint8_t* stage_a = wst + static_cast<size_t>(a.stages) * kStageBytes;
-    float* sbias = reinterpret_cast<float*>(stage_a + static_cast<size_t>(kRowsPerTile) * a.H * 2);
     const int Vp = (a.V + kNTile - 1) / kNTile * kNTile;  // V rounded up to whole N tiles
-    float4* xchg = reinterpret_cast<float4*>(sbias + Vp);  // [2][128] epilogue group 1 -> group 0 partials
+    float* sbias = reinterpret_cast<float*>(stage_a + static_cast<size_t>(kRowsPerTile) * a.H * 2);  // kSB: [Vp]
+    float4* xchg = reinterpret_cast<float4*>(sbias + (kSB ? Vp : 0));  // [2][128] epilogue group 1 -> 0 partials
     uint64_t* bars = reinterpret_cast<uint64_t*>(xchg + 2 * kRowsPerTile);
     uint64_t* b_full = bars;                   // [stages]
     uint64_t* b_empty = bars + kMaxStages;     // [stages]
@@ -283,6 +299,8 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int H = a.H, V = a.V;
+    if (kSB)  // read by the epilogue only, after the __syncthreads of the setup below
+        for (int i = threadIdx.x; i < Vp; i += blockDim.x) sbias[i] = i < V ? (a.bias ? a.bias[i] : 0.f) : -INFINITY;
     const int KB = H / kKBlock, NT = Vp / kNTile;
     const int64_t rows = *a.nrows;  // valid cells only: padding costs no GEMM work
     const int64_t ntiles = (rows + kRowsPerTile - 1) / kRowsPerTile;
@@ -298,9 +316,6 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
         return true;
     };
 
-    // Columns past V (the last N tile's tail): TMA zero-fills W's missing rows, and a -inf bias makes those
-    // logits -inf, i.e. absent from the max and the sum (V need not be a multiple of the tile).
-    for (int i = threadIdx.x; i < Vp; i += blockDim.x) sbias[i] = i < V ? (a.bias ? a.bias[i] : 0.f) : -INFINITY;
     if (threadIdx.x == 0) {
         for (int s = 0; s < a.stages; ++s) {
             mbar_init(&b_full[s], 1);
@@ -448,16 +463,18 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
                     tc_fence_after();
 #pragma unroll 1
                     for (int c = eg * (kNTile / 64); c < (eg + 1) * (kNTile / 64); ++c) {
+                        const int v0 = n * kNTile + c * 32;
+                        float4 bq[8];  // !kSB: global bias loads in flight under the TMEM load
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) bq[j] = kSB ? make_float4(0.f, 0.f, 0.f, 0.f) : bias4(a, v0 + 4 * j);
                         uint32_t r[32];
                         TMEM_LD32(lane_base + kAccCol0 + acc * kNTile + c * 32, r);
                         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                         if (crow >= rows) continue;
-                        const int v0 = n * kNTile + c * 32;
-                        const float4* b4 = reinterpret_cast<const float4*>(sbias + v0);
                         float g[32];
 #pragma unroll
                         for (int j = 0; j < 8; ++j) {
-                            const float4 bb = b4[j];
+                            const float4 bb = kSB ? reinterpret_cast<const float4*>(sbias + v0)[j] : bq[j];
                             const f32x2 z0 = fadd2(pk(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1])), pk(bb.x, bb.y));
                             const f32x2 z1 = fadd2(pk(__uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3])), pk(bb.z, bb.w));
                             const float2 p0 = upk(fmul2(ex2x2(ffma2(z0, l2, nl)), g2));
@@ -500,6 +517,10 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
                 tc_fence_after();
 #pragma unroll 1
                 for (int c = eg * (kNTile / 64); c < (eg + 1) * (kNTile / 64); ++c) {  // group eg: half the columns
+                    const int v0 = n * kNTile + c * 32;
+                    float4 bq[8];  // !kSB: global bias loads in flight under the TMEM load
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) bq[j] = kSB ? make_float4(0.f, 0.f, 0.f, 0.f) : bias4(a, v0 + 4 * j);
                     uint32_t r[32];
                     TMEM_LD32(lane_base + kAccCol0 + acc * kNTile + c * 32, r);
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -507,12 +528,10 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
                         m = fmaxf(m, __uint_as_float(r[0]) + __uint_as_float(r[31]));
                         continue;
                     }
-                    const int v0 = n * kNTile + c * 32;
-                    const float4* b4 = reinterpret_cast<const float4*>(sbias + v0);
                     f32x2 zz[16];
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
-                        const float4 bb = b4[j];
+                        const float4 bb = kSB ? reinterpret_cast<const float4*>(sbias + v0)[j] : bq[j];
                         zz[2 * j] = fadd2(pk(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1])), pk(bb.x, bb.y));
                         zz[2 * j + 1] =
                             fadd2(pk(__uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3])), pk(bb.z, bb.w));
@@ -744,10 +763,9 @@ __global__ void __launch_bounds__(256) k6_rowmap(const int32_t* __restrict__ T_b
     if (b == B - 1 && blockIdx.x == 0 && threadIdx.x == 0) *nrows = off + n;
 }
 
-size_t joint_smem_bytes(int H, int V, int stages) {
+size_t joint_smem_bytes(int H, int V, int stages) {  // V = 0: bias not staged (!kSB)
     return 1024 + static_cast<size_t>(stages) * kStageBytes + static_cast<size_t>(kRowsPerTile) * H * 2 +
-           static_cast<size_t>((V + kNTile - 1) / kNTile * kNTile) * 4 + 2 * kRowsPerTile * 16 +
-           (2 * kMaxStages + 2 + 2 * kAccBufs) * 8 + 16;
+           static_cast<size_t>((V + kNTile - 1) / kNTile * kNTile) * 4 + 2 * kRowsPerTile * 16 + (2 * kMaxStages + 2 + 2 * kAccBufs) * 8 + 16;
 }
 
 using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -797,7 +815,8 @@ rnnt_status joint_front(const void* enc, const void* pred, const void* weight, c
     if (!enc || !pred || !weight || !logit_lens || !target_lens || !workspace) return RNNT_ERR_INVALID_ARG;
     if (Umax > 0 && !targets) return RNNT_ERR_INVALID_ARG;
     if (workspace_bytes < rnnt::workspace_bytes(B, Tmax, Umax)) return RNNT_ERR_WORKSPACE_TOO_SMALL;
-    if ((reinterpret_cast<uintptr_t>(enc) | reinterpret_cast<uintptr_t>(pred) | reinterpret_cast<uintptr_t>(weight)) % 16)
+    if ((reinterpret_cast<uintptr_t>(enc) | reinterpret_cast<uintptr_t>(pred) | reinterpret_cast<uintptr_t>(weight) |
+         reinterpret_cast<uintptr_t>(bias)) % 16)
         return RNNT_ERR_INVALID_ARG;
     EncodeTiled enc_fn = encode_fn();
     if (!enc_fn) return RNNT_ERR_CUDA;
@@ -819,11 +838,15 @@ rnnt_status joint_front(const void* enc, const void* pred, const void* weight, c
         cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
         return RNNT_ERR_CUDA;
     int stages = kMaxStages;
-    while (stages > 2 && joint_smem_bytes(H, V, stages) > static_cast<size_t>(smem_max)) --stages;
-    const size_t smem = joint_smem_bytes(H, V, stages);
+    const bool sb = V <= kSBiasMaxV;  // bias staged in shared memory (small vocabularies), else read from global
+    const int Vs = sb ? V : 0;
+    while (stages > 2 && joint_smem_bytes(H, Vs, stages) > static_cast<size_t>(smem_max)) --stages;
+    const size_t smem = joint_smem_bytes(H, Vs, stages);
     if (smem > static_cast<size_t>(smem_max)) return RNNT_ERR_UNSUPPORTED;
-    auto kern = g ? (cl > 1 ? k6_joint_lse<true, 2> : k6_joint_lse<true, 1>)
-                  : (cl > 1 ? k6_joint_lse<false, 2> : k6_joint_lse<false, 1>);
+    auto kern = sb ? (g ? (cl > 1 ? k6_joint_lse<true, 2, true> : k6_joint_lse<true, 1, true>)
+                        : (cl > 1 ? k6_joint_lse<false, 2, true> : k6_joint_lse<false, 1, true>))
+                   : (g ? (cl > 1 ? k6_joint_lse<true, 2, false> : k6_joint_lse<true, 1, false>)
+                        : (cl > 1 ? k6_joint_lse<false, 2, false> : k6_joint_lse<false, 1, false>));
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
         return RNNT_ERR_CUDA;
 

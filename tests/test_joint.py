@@ -65,6 +65,36 @@ def test_joint_matches_materialised_loss_path(rb):
     assert torch.allclose(l, l_ref, rtol=1e-5, atol=1e-5)
 
 
+@pytest.mark.parametrize("variant", ("rnnt", "allow_ignore"))
+def test_joint_large_vocabulary(rb, variant):
+    # V = 32003: 251 N tiles, ragged last tile; shared memory does not depend on V (bias read from global)
+    _case(rb, 2, 6, 3, 128, 32003, seed=41, variant=variant)
+
+
+def test_joint_grad_large_vocabulary(rb):
+    B, T, U, H, V = 2, 5, 3, 128, 8195
+    cfg = workloads.random_config(B, T, U, V, seed=43, variant="force_final")
+    T_b, U_b = workloads.lengths(cfg)
+    y = workloads.targets(cfg, U_b)
+    enc, pred, W, b = workloads.joint_inputs(B, T, U, H, V, seed=43)
+    out = rb.rnnt_joint_loss_grad(enc.cuda(), pred.cuda(), W.cuda(), b.cuda(), y, T_b, U_b, 0, "force_final")
+    torch.cuda.synchronize()
+    ref = oj.joint_loss_and_grads(enc.double().numpy(), pred.double().numpy(), W.double().numpy(),
+                                  b.double().numpy(), y, T_b, U_b, 0, "force_final")
+    l = out[0].cpu().numpy().astype(np.float64)
+    assert (np.abs(l - ref[0]) / np.maximum(np.abs(ref[0]), 1.0)).max() <= 1e-5
+    for name, mine, r in zip(("d_enc", "d_pred", "d_weight", "d_bias"), out[1:], ref[1:]):
+        err = np.abs(mine.cpu().numpy().astype(np.float64) - r).max()
+        assert err <= 2e-3 * np.abs(r).max(), (name, err, np.abs(r).max())
+
+
+def test_joint_rejects_misaligned_bias(rb):
+    enc, pred, W, b = workloads.joint_inputs(1, 4, 2, 128, 130, seed=5)
+    bb = torch.zeros(131, device="cuda")[1:]  # 4-byte offset
+    with pytest.raises(rb.RnntError):
+        rb.rnnt_joint_loss(enc.cuda(), pred.cuda(), W.cuda(), bb, [[1, 2]], [4], [2])
+
+
 def test_joint_rejects_unsupported_shapes(rb):
     enc = torch.zeros(1, 4, 96, dtype=torch.bfloat16, device="cuda")
     pred = torch.zeros(1, 3, 96, dtype=torch.bfloat16, device="cuda")
