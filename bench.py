@@ -490,6 +490,7 @@ def main_joint(args, rb, rdist, rank, world, local, dev):
     targets = torch.from_numpy(y_np).to(dev)
     T_b = torch.from_numpy(T_np).to(dev)
     U_b = torch.from_numpy(U_np).to(dev)
+    valid_rows = rb.joint_valid_rows(T_np, U_np, Tmax, Umax)  # host lengths: the GEMMs skip the padding
     losses = torch.empty(B, dtype=torch.float32, device=dev)
     loss_sum = torch.empty((), dtype=torch.float64, device=dev)
     grad = args.mode == "joint_grad"
@@ -511,7 +512,7 @@ def main_joint(args, rb, rdist, rank, world, local, dev):
     def step(events=None):
         if grad:
             rb.rnnt_joint_loss_grad(enc, pred, W, bias, targets, T_b, U_b, gcfg.blank, variant, workspace=workspace,
-                                    outputs=outs)
+                                    outputs=outs, valid_rows=valid_rows)
         else:
             rb.rnnt_joint_loss(enc, pred, W, bias, targets, T_b, U_b, gcfg.blank, variant, losses=losses,
                                workspace=workspace, events=events)
@@ -556,9 +557,8 @@ def main_joint(args, rb, rdist, rank, world, local, dev):
     k2_ms = statistics.mean(r[2].elapsed_time(r[3]) for r in evs) if not grad else None
     rows = int(sum(int(t) * (int(u) + 1) for t, u in zip(T_np, U_np)))  # K6 runs on the valid cells only
     flops = 2.0 * rows * V * H
-    if grad:  # K6 forward + K6<grad> recompute (valid rows) + the two backward GEMMs (all padded rows)
-        rows_p = B * Tmax * (Umax + 1)
-        flops = 2.0 * 2 * rows * V * H + 2.0 * 2 * rows_p * V * H
+    if grad:  # K6 forward + K6<grad> recompute + the two backward GEMMs, all over the valid cells (valid_rows)
+        flops = 4 * 2.0 * rows * V * H
     tf = flops / ((ms_step if grad else k6_ms) / 1e3) / 1e12
     with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
         mp = json.load(f)

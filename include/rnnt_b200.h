@@ -206,13 +206,18 @@ rnnt_status rnnt_joint_viterbi(const void* enc, const void* pred, const void* we
  *   as rnnt_loss.  dz = d loss / d z is formed on chip from the recomputed logits (K3's formula) and stored in bf16
  *   for the two backward GEMMs (dh = dz W stored in bf16, dW = dz^T h; cuBLAS, fp32 accumulation); tanh' uses
  *   the stored bf16 h.  workspace: rnnt_joint_grad_workspace_bytes(...) bytes (it holds dz, h and dh of every
- *   padded cell: ~ (2 V + 4 H) bytes per cell).  Same constraints as rnnt_joint_loss. */
+ *   padded cell: ~ (2 V + 4 H) bytes per cell).  Same constraints as rnnt_joint_loss.
+ *   valid_rows: the number of valid cells, sum over the valid utterances (1 <= T_b <= Tmax, 0 <= U_b <= Umax)
+ *   of T_b (U_b + 1), when the caller knows it (the host usually holds the lengths), else -1.  Given, the two
+ *   GEMMs run over the valid cells only (no work on padding); it must equal the device's count, else every
+ *   loss is set to NaN (and the gradients are undefined).  Out of [-1, B Tmax (Umax+1)]: RNNT_ERR_INVALID_ARG. */
 size_t rnnt_joint_grad_workspace_bytes(int B, int Tmax, int Umax, int H, int V);
 rnnt_status rnnt_joint_loss_grad(const void* enc, const void* pred, const void* weight, const float* bias,
                                  const int32_t* targets, const int32_t* logit_lens, const int32_t* target_lens,
                                  int B, int Tmax, int Umax, int H, int V, int blank, int variant, float* losses,
                                  float* d_enc, float* d_pred, float* d_weight, float* d_bias,
-                                 const float* grad_scale, void* workspace, size_t workspace_bytes, void* stream);
+                                 const float* grad_scale, int64_t valid_rows, void* workspace,
+                                 size_t workspace_bytes, void* stream);
 
 const char* rnnt_status_string(rnnt_status status);
 

@@ -39,7 +39,7 @@ def _load():
         raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
                           f"g.build()'` (nvcc, sm_100a). There is no CPU fallback.")
     lib = ctypes.CDLL(LIB_PATH)
-    P, I, S = ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t
+    P, I, S, L = ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t, ctypes.c_int64
     common = [P, P, P, P, I, I, I, I, I, P, P, P, P, S, P]
     sigs = {
         "rnnt_workspace_bytes": ([I, I, I], S),
@@ -57,7 +57,7 @@ def _load():
         "rnnt_joint_loss_ex": ([P, P, P, P, P, P, P, I, I, I, I, I, I, I, P, P, S, P, P], I),
         "rnnt_joint_viterbi": ([P, P, P, P, P, P, P, I, I, I, I, I, I, I, P, P, P, P, S, P], I),
         "rnnt_joint_grad_workspace_bytes": ([I, I, I, I, I], S),
-        "rnnt_joint_loss_grad": ([P, P, P, P, P, P, P, I, I, I, I, I, I, I, P, P, P, P, P, P, P, S, P], I),
+        "rnnt_joint_loss_grad": ([P, P, P, P, P, P, P, I, I, I, I, I, I, I, P, P, P, P, P, P, L, P, S, P], I),
         "rnnt_status_string": ([I], ctypes.c_char_p),
         "rnnt_version": ([], ctypes.c_char_p),
     }
@@ -243,12 +243,14 @@ def rnnt_joint_loss(enc, pred, weight, bias, targets, logit_lens, target_lens, b
 
 
 def rnnt_joint_loss_grad(enc, pred, weight, bias, targets, logit_lens, target_lens, blank=0, variant="rnnt",
-                         workspace=None, stream=None, outputs=None, grad_scale=None):
+                         workspace=None, stream=None, outputs=None, grad_scale=None, valid_rows=None):
     """Training step of the fused joint (NEXT-4 backward): returns (losses [B], d_enc [B, Tmax, H],
     d_pred [B, Umax+1, H], d_weight [V, H], d_bias [V]), the gradients (fp32) of sum(losses).  Inputs as
     rnnt_joint_loss; bias may be None (then d_bias is still returned, for a zero bias).  outputs: optional
     preallocated (losses, d_enc, d_pred, d_weight, d_bias) fp32 tensors of those shapes.  grad_scale: optional
-    [B] per-utterance weights (gradients of sum_b grad_scale[b] * losses[b]; 1/B gives the mean)."""
+    [B] per-utterance weights (gradients of sum_b grad_scale[b] * losses[b]; 1/B gives the mean).
+    valid_rows: the valid-cell count sum_b T_b (U_b + 1) (the GEMMs then skip the padding; a wrong count gives
+    NaN losses); None computes it when both length arrays are on the host, else passes -1 (unknown)."""
     for name, x in (("enc", enc), ("pred", pred), ("weight", weight)):
         if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.bfloat16 and x.is_contiguous()):
             raise TypeError(f"{name} must be a contiguous CUDA bfloat16 tensor (no CPU fallback)")
@@ -259,6 +261,8 @@ def rnnt_joint_loss_grad(enc, pred, weight, bias, targets, logit_lens, target_le
     if bias is not None:
         bias = bias.to(device=dev, dtype=torch.float32).contiguous()
     targets = _as_i32(targets, dev).reshape(B, Umax) if Umax > 0 else None
+    if valid_rows is None:
+        valid_rows = joint_valid_rows(logit_lens, target_lens, Tmax, Umax)
     logit_lens = _as_i32(logit_lens, dev)
     target_lens = _as_i32(target_lens, dev)
     if outputs is None:
@@ -276,9 +280,20 @@ def rnnt_joint_loss_grad(enc, pred, weight, bias, targets, logit_lens, target_le
     _check(library.rnnt_joint_loss_grad(_ptr(enc), _ptr(pred), _ptr(weight), _ptr(bias), _ptr(targets),
                                         _ptr(logit_lens), _ptr(target_lens), B, Tmax, Umax, H, V, int(blank),
                                         VARIANTS[variant], _ptr(losses), _ptr(d_enc), _ptr(d_pred), _ptr(d_weight),
-                                        _ptr(d_bias), _ptr(grad_scale), _ptr(workspace), workspace.numel(),
-                                        _stream(stream)))
+                                        _ptr(d_bias), _ptr(grad_scale), int(valid_rows), _ptr(workspace),
+                                        workspace.numel(), _stream(stream)))
     return losses, d_enc, d_pred, d_weight, d_bias
+
+
+def joint_valid_rows(logit_lens, target_lens, Tmax, Umax):
+    """sum_b T_b (U_b + 1) over the valid utterances, from host lengths (numpy / list / CPU tensor); -1 when
+    either array is on the GPU (no device sync here)."""
+    if any(isinstance(x, torch.Tensor) and x.is_cuda for x in (logit_lens, target_lens)):
+        return -1
+    T = np.asarray(logit_lens.numpy() if isinstance(logit_lens, torch.Tensor) else logit_lens, np.int64).ravel()
+    U = np.asarray(target_lens.numpy() if isinstance(target_lens, torch.Tensor) else target_lens, np.int64).ravel()
+    ok = (T >= 1) & (T <= Tmax) & (U >= 0) & (U <= Umax)
+    return int((T * (U + 1))[ok].sum())
 
 
 def rnnt_joint_viterbi(enc, pred, weight, bias, targets, logit_lens, target_lens, blank=0, variant="rnnt",

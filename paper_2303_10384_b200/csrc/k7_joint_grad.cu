@@ -46,6 +46,24 @@ __global__ void __launch_bounds__(256) k7_zero_tail(const int* __restrict__ nrow
     }
 }
 
+// W [V][H] -> Wp [Vp][H], rows V..Vp-1 zero (dz's tail columns are zero too: K = Vp adds nothing).
+__global__ void __launch_bounds__(256) k7_pad_w(const __nv_bfloat16* __restrict__ w, int V, int Vp, int H,
+                                                __nv_bfloat16* __restrict__ wp) {
+    const int64_t n = static_cast<int64_t>(Vp) * H / 8, nv = static_cast<int64_t>(V) * H / 8;  // 16-byte units
+    const uint4* w4 = reinterpret_cast<const uint4*>(w);
+    uint4* o4 = reinterpret_cast<uint4*>(wp);
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        o4[i] = i < nv ? w4[i] : make_uint4(0u, 0u, 0u, 0u);
+}
+
+// valid_rows given by the caller must equal the row map's count; else every loss is NaN (loud failure: the
+// GEMMs ran over the wrong rows).
+__global__ void k7_check_rows(const int* __restrict__ nrows, int64_t valid_rows, int B, float* __restrict__ losses) {
+    if (*nrows == valid_rows) return;
+    for (int i = threadIdx.x; i < B; i += blockDim.x) losses[i] = __int_as_float(0x7fc00000);
+}
+
 // d_weight [V][H] and d_bias [V] out of the augmented dW GEMM's [V][H + kJointHPad] result.
 __global__ void __launch_bounds__(256) k7_split_dw(const float* __restrict__ dwa, int V, int H, float* __restrict__ dw,
                                                    float* __restrict__ db) {
@@ -201,7 +219,7 @@ cublasHandle_t blas_handle() {
 struct GradLayout {
     int64_t R;  // padded rows B * Tmax * (Umax + 1)
     int Vp;
-    size_t base, rowmap, nrows, dz, h, dh, dwa, total;
+    size_t base, rowmap, nrows, dz, h, dh, dwa, wp, total;
 };
 
 GradLayout grad_layout(int B, int Tmax, int Umax, int H, int V) {
@@ -223,6 +241,8 @@ GradLayout grad_layout(int B, int Tmax, int Umax, int H, int V) {
     off += align256(sizeof(__nv_bfloat16) * L.R * H);
     L.dwa = off;
     off += align256(sizeof(float) * static_cast<size_t>(V) * (H + kJointHPad));
+    L.wp = off;  // W padded to Vp rows (zero tail) when V % kJointVTile != 0: the dh GEMM runs with K = Vp
+    off += align256(sizeof(__nv_bfloat16) * static_cast<size_t>(L.Vp) * H);
     L.total = off;
     return L;
 }
@@ -240,7 +260,8 @@ extern "C" rnnt_status rnnt_joint_loss_grad(const void* enc, const void* pred, c
                                             const int32_t* target_lens, int B, int Tmax, int Umax, int H, int V,
                                             int blank, int variant, float* losses, float* d_enc, float* d_pred,
                                             float* d_weight, float* d_bias, const float* grad_scale,
-                                            void* workspace, size_t workspace_bytes, void* stream) {
+                                            int64_t valid_rows, void* workspace, size_t workspace_bytes,
+                                            void* stream) {
     using namespace rnnt;
     if (variant < -1 || variant > 1) return RNNT_ERR_INVALID_ARG;
     if (B < 0 || Tmax < 1 || Umax < 0 || H < 1 || V < 2) return RNNT_ERR_INVALID_ARG;
@@ -249,6 +270,7 @@ extern "C" rnnt_status rnnt_joint_loss_grad(const void* enc, const void* pred, c
     const GradLayout L = grad_layout(B, Tmax, Umax, H, V);
     if (workspace_bytes < L.total) return RNNT_ERR_WORKSPACE_TOO_SMALL;
     if (L.R >= (int64_t(1) << 31)) return RNNT_ERR_UNSUPPORTED;
+    if (valid_rows < -1 || valid_rows > L.R) return RNNT_ERR_INVALID_ARG;
     char* ws = static_cast<char*>(workspace);
     int* rowmap = reinterpret_cast<int*>(ws + L.rowmap);
     int* nrows = reinterpret_cast<int*>(ws + L.nrows);
@@ -274,20 +296,37 @@ extern "C" rnnt_status rnnt_joint_loss_grad(const void* enc, const void* pred, c
                      workspace, workspace_bytes, s, nullptr, rowmap, nrows, false, &g);
     if (st != RNNT_OK) return st;
     const int Hs = H + kJointHPad;
-    k7_zero_tail<<<1184, 256, 0, s>>>(nrows, L.R, L.Vp, Hs, dz, hb);
+    // rows the GEMMs cover: the caller's valid-row count (no padded rows: no zeroing, no wasted GEMM work), else
+    // every padded row with the tail [*nrows, R) zeroed on the device
+    const int R = static_cast<int>(valid_rows >= 0 ? valid_rows : L.R);
+    if (valid_rows < 0) {
+        k7_zero_tail<<<1184, 256, 0, s>>>(nrows, L.R, L.Vp, Hs, dz, hb);
+    } else {
+        k7_check_rows<<<1, 256, 0, s>>>(nrows, valid_rows, B, losses);
+    }
     if (cudaGetLastError() != cudaSuccess) return RNNT_ERR_CUDA;
+    const void* wk = weight;  // dh GEMM's W: K = Vp (a multiple of the tile) keeps cuBLAS on its sm_100 kernels
+    if (L.Vp != V) {
+        auto* wp = reinterpret_cast<__nv_bfloat16*>(ws + L.wp);
+        k7_pad_w<<<148, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(weight), V, L.Vp, H, wp);
+        if (cudaGetLastError() != cudaSuccess) return RNNT_ERR_CUDA;
+        wk = wp;
+    }
     // the two GEMMs and dbias (column-major views of the row-major arrays; bf16 in, fp32 accumulate / out)
     const float one = 1.f, zero = 0.f;
-    const int R = static_cast<int>(L.R);
     if (cublasSetStream(hd, s) != CUBLAS_STATUS_SUCCESS) return RNNT_ERR_CUDA;
-    // dh^T [H x R] = W^T [H x V] . dz^T [V x R]
-    if (cublasGemmEx(hd, CUBLAS_OP_N, CUBLAS_OP_N, H, R, V, &one, weight, CUDA_R_16BF, H, dz, CUDA_R_16BF, L.Vp,
-                     &zero, dh, CUDA_R_16BF, H, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT) != CUBLAS_STATUS_SUCCESS)
-        return RNNT_ERR_CUDA;
-    // [dW | dbias]^T [(H + 8) x V] = [h | 1 0..0]^T [(H + 8) x R] . dz [R x V]
-    if (cublasGemmEx(hd, CUBLAS_OP_N, CUBLAS_OP_T, Hs, V, R, &one, hb, CUDA_R_16BF, Hs, dz, CUDA_R_16BF, L.Vp, &zero,
-                     dwa, CUDA_R_32F, Hs, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT) != CUBLAS_STATUS_SUCCESS)
-        return RNNT_ERR_CUDA;
+    if (R == 0) {
+        if (cudaMemsetAsync(dwa, 0, sizeof(float) * static_cast<size_t>(V) * Hs, s) != cudaSuccess) return RNNT_ERR_CUDA;
+    } else {
+        // dh^T [H x R] = W^T [H x Vp] . dz^T [Vp x R]
+        if (cublasGemmEx(hd, CUBLAS_OP_N, CUBLAS_OP_N, H, R, L.Vp, &one, wk, CUDA_R_16BF, H, dz, CUDA_R_16BF, L.Vp,
+                         &zero, dh, CUDA_R_16BF, H, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT) != CUBLAS_STATUS_SUCCESS)
+            return RNNT_ERR_CUDA;
+        // [dW | dbias]^T [(H + 8) x V] = [h | 1 0..0]^T [(H + 8) x R] . dz [R x V]
+        if (cublasGemmEx(hd, CUBLAS_OP_N, CUBLAS_OP_T, Hs, V, R, &one, hb, CUDA_R_16BF, Hs, dz, CUDA_R_16BF, L.Vp,
+                         &zero, dwa, CUDA_R_32F, Hs, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT) != CUBLAS_STATUS_SUCCESS)
+            return RNNT_ERR_CUDA;
+    }
     k7_split_dw<<<296, 256, 0, s>>>(dwa, V, H, d_weight, d_bias);
     // K7: tanh' and the reductions into d enc / d pred
     float* part = reinterpret_cast<float*>(ws + L.dz);  // dz is dead after the GEMMs

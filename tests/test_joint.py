@@ -204,3 +204,27 @@ def test_joint_grad_scale(rb):
     for i in range(2):
         r = float(scale[i]) * refs[i][1][0]
         assert np.abs(out[1][i].cpu().numpy() - r).max() <= 2e-3 * np.abs(r).max()
+
+
+def test_joint_grad_valid_rows_paths(rb):
+    """Host lengths (valid_rows hint: GEMMs over the valid cells) and device lengths (-1: every padded row, tail
+    zeroed) give the same result; a wrong hint is a loud failure (NaN losses)."""
+    B, T, U, H, V = 4, 23, 9, 128, 500
+    cfg = workloads.random_config(B, T, U, V, seed=47, variant="rnnt")
+    T_b, U_b = workloads.lengths(cfg)
+    y = workloads.targets(cfg, U_b)
+    enc, pred, W, b = workloads.joint_inputs(B, T, U, H, V, seed=47)
+    args = (enc.cuda(), pred.cuda(), W.cuda(), b.cuda(), y)
+    n = rb.joint_valid_rows(T_b, U_b, T, U)
+    assert n == int(sum(int(t) * (int(u) + 1) for t, u in zip(T_b, U_b))) and n < B * T * (U + 1)
+    host = rb.rnnt_joint_loss_grad(*args, T_b, U_b, 0, "rnnt")
+    dev = rb.rnnt_joint_loss_grad(*args, torch.from_numpy(T_b).cuda(), torch.from_numpy(U_b).cuda(), 0, "rnnt")
+    torch.cuda.synchronize()
+    assert torch.equal(host[0], dev[0])
+    for a, c in zip(host[1:], dev[1:]):
+        assert torch.allclose(a, c, rtol=1e-5, atol=1e-6 * c.abs().max().item())
+    bad = rb.rnnt_joint_loss_grad(*args, T_b, U_b, 0, "rnnt", valid_rows=n - 1)
+    torch.cuda.synchronize()
+    assert torch.isnan(bad[0]).all()
+    with pytest.raises(rb.RnntError):
+        rb.rnnt_joint_loss_grad(*args, T_b, U_b, 0, "rnnt", valid_rows=B * T * (U + 1) + 1)
