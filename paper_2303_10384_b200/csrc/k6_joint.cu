@@ -286,7 +286,8 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
     uint8_t* wst = base;
     uint8_t* stage_a = wst + static_cast<size_t>(a.stages) * kStageBytes;
     const int Vp = (a.V + kNTile - 1) / kNTile * kNTile;  // V rounded up to whole N tiles
-    float* sbias = reinterpret_cast<float*>(stage_a + static_cast<size_t>(kRowsPerTile) * a.H * 2);  // kSB: [Vp]
+    // A staging: 128 rows of H + kJointHPad bf16 (the pad holds (1, 0, .., 0): row = h's global row, see kGrad)
+    float* sbias = reinterpret_cast<float*>(stage_a + static_cast<size_t>(kRowsPerTile) * (a.H + kJointHPad) * 2);
     float4* xchg = reinterpret_cast<float4*>(sbias + (kSB ? Vp : 0));  // [2][128] epilogue group 1 -> 0 partials
     uint64_t* bars = reinterpret_cast<uint64_t*>(xchg + 2 * kRowsPerTile);
     uint64_t* b_full = bars;                   // [stages]
@@ -301,6 +302,11 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
     const int H = a.H, V = a.V;
     if (kSB)  // read by the epilogue only, after the __syncthreads of the setup below
         for (int i = threadIdx.x; i < Vp; i += blockDim.x) sbias[i] = i < V ? (a.bias ? a.bias[i] : 0.f) : -INFINITY;
+    if (kGrad)  // staging rows' pad = h's extra column (1, 0, .., 0): the dW GEMM's extra output is dbias
+        for (int i = threadIdx.x; i < kRowsPerTile; i += blockDim.x)
+            *reinterpret_cast<uint4*>(stage_a + static_cast<size_t>(i) * (H + kJointHPad) * 2 + H * 2) =
+                make_uint4(0x3f80u, 0u, 0u, 0u);
+    if (kGrad) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // read by the bulk copies
     const int KB = H / kKBlock, NT = Vp / kNTile;
     const int64_t rows = *a.nrows;  // valid cells only: padding costs no GEMM work
     const int64_t ntiles = (rows + kRowsPerTile - 1) / kRowsPerTile;
@@ -603,7 +609,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
         const int q = warp & 3, kh = (warp - 12) >> 2;
         const int rl = q * 32 + lane;
         const int nch = H / 16;            // 16-byte chunks per K half
-        const int row_bytes = H * 2;
+        const int row_bytes = (H + kJointHPad) * 2;  // +16 B: conflict-free row reads without a swizzle
         uint8_t* my_row = stage_a + static_cast<size_t>(rl) * row_bytes;
         const uint4* f4 = reinterpret_cast<const uint4*>(a.f);
         const uint4* g4 = reinterpret_cast<const uint4*>(a.g);
@@ -618,6 +624,10 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
         };
         int p_next = -1;
         auto build = [&](int64_t tile, int p) {
+            if constexpr (kGrad) {  // the previous tile's h store must have read the staging buffer
+                if (warp == 12 && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                asm volatile("bar.sync 4, 256;" ::: "memory");  // the 8 builder warps
+            }
             // lane r: chunk offsets (16-byte units) of row q*32 + r's f and g rows, -1 past the end
             int fo = -1, go = -1;
             if (p >= 0) {
@@ -664,19 +674,28 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
                     }
                     const int r2 = q * 32 + rows_[j];
                     const int cg = kh * nch + cs[j];
-                    *reinterpret_cast<uint4*>(stage_a + static_cast<size_t>(r2) * row_bytes + ((cg ^ (r2 & 7)) << 4)) =
+                    *reinterpret_cast<uint4*>(stage_a + static_cast<size_t>(r2) * row_bytes + (cg << 4)) =
                         make_uint4(ow[0], ow[1], ow[2], ow[3]);
-                    if constexpr (kGrad) {  // h for the dW GEMM, compact rows (coalesced: lane = chunk)
-                        const int64_t crow = tile * kRowsPerTile + r2;
-                        // rows of H + 8: the extra 16 bytes hold (1, 0, ..., 0), so the dW GEMM's extra output
-                        // column is dbias = sum_rows dz (no separate GEMV over dz)
-                        __nv_bfloat16* hrow = a.h_out + crow * (H + kJointHPad);
-                        if (ok[j]) reinterpret_cast<uint4*>(hrow)[cg] = make_uint4(ow[0], ow[1], ow[2], ow[3]);
-                        if (ok[j] && cg == 0) reinterpret_cast<uint4*>(hrow + H)[0] = make_uint4(0x3f80u, 0u, 0u, 0u);
-                    }
                 }
             }
             __syncwarp();  // each thread copies its own row, written by the whole warp
+            if constexpr (kGrad) {
+                // h for the dW GEMM: the staging rows ARE h's global rows (H + 8 columns, the pad = (1, 0, ..)),
+                // and the tile's rows are consecutive compact rows -> ONE bulk async copy (TMA engine) of the
+                // tile, issued once all builders have written it; it overlaps the TMEM copy and the next build.
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("bar.sync 4, 256;" ::: "memory");
+                if (warp == 12 && lane == 0) {
+                    const int64_t nv = std::min<int64_t>(kRowsPerTile, rows - tile * kRowsPerTile);
+                    if (nv > 0) {
+                        __nv_bfloat16* dst = a.h_out + tile * kRowsPerTile * (H + kJointHPad);
+                        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                                     "r"(smem_u32(stage_a)), "r"(static_cast<uint32_t>(nv * row_bytes))
+                                     : "memory");
+                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    }
+                }
+            }
         };
         const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16);
         uint32_t tl = 0;
@@ -695,7 +714,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
                     const int cg = kh * nch + c0 + i;
-                    const uint4 v = *reinterpret_cast<const uint4*>(my_row + ((cg ^ (rl & 7)) << 4));
+                    const uint4 v = *reinterpret_cast<const uint4*>(my_row + (cg << 4));
                     r[4 * i + 0] = v.x;
                     r[4 * i + 1] = v.y;
                     r[4 * i + 2] = v.z;
@@ -722,6 +741,8 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
         if (warp == 8) o[7] = w_accfull;
         if (warp == 12) o[6] = w_aempty;
     }
+    if (kGrad && warp == 12 && lane == 0)  // the last h store completes before the CTA's shared memory is released
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     tc_fence_before();
     if constexpr (kCl > 1)
         cluster_sync_all();  // no CTA leaves while its partner may still multicast into it
@@ -764,7 +785,7 @@ __global__ void __launch_bounds__(256) k6_rowmap(const int32_t* __restrict__ T_b
 }
 
 size_t joint_smem_bytes(int H, int V, int stages) {  // V = 0: bias not staged (!kSB)
-    return 1024 + static_cast<size_t>(stages) * kStageBytes + static_cast<size_t>(kRowsPerTile) * H * 2 +
+    return 1024 + static_cast<size_t>(stages) * kStageBytes + static_cast<size_t>(kRowsPerTile) * (H + kJointHPad) * 2 +
            static_cast<size_t>((V + kNTile - 1) / kNTile * kNTile) * 4 + 2 * kRowsPerTile * 16 + (2 * kMaxStages + 2 + 2 * kAccBufs) * 8 + 16;
 }
 
