@@ -358,6 +358,15 @@ def main():
         return statistics.mean(r[a].elapsed_time(r[b_]) for r in evs)
     k_ms = {"k1_lse_gather": span(0, 1), "k2_alpha_beta": span(4, 5), "k3_grad": span(2, 3),
             "k2_exposed_wait": span(1, 2)}
+    # per-step spread (median / p10 / p90): K1 start -> last kernel end of each step, from the
+    # event-carrying replay (loss_grad: K3 end; loss: K2 end)
+    step_dist = None
+    if args.mode in ("loss_grad", "loss") and K >= 2:
+        ends = 3 if args.mode == "loss_grad" else 5
+        per = sorted(r[0].elapsed_time(r[ends]) for r in evs)
+        q = lambda f: per[min(len(per) - 1, int(round(f * (len(per) - 1))))]
+        step_dist = {"p10": q(0.1), "p50": q(0.5), "p90": q(0.9), "n": len(per),
+                     "span": "K1 start -> " + ("K3 end" if args.mode == "loss_grad" else "K2 end")}
     T_np, U_np = pb["logit_lens"], pb["target_lens"]
     valid_elems = int(sum(int(t) * (int(u) + 1) for t, u in zip(T_np, U_np))) * V
     all_elems = B * Tmax * Up1 * V
@@ -409,6 +418,8 @@ def main():
                     "metric itself is fp32",
             "kernel_frac_of_peak": {"k1_lse_gather": k1_gbs / peak, "k3_grad": k3_gbs and k3_gbs / peak},
             "step_frac_of_3pass_roofline": (3 * esize * valid_elems / (ms_step / 1e3) / 1e9) / peak,
+            "step_frac_of_2pass_bound": (2 * esize * valid_elems / (ms_step / 1e3) / 1e9) / peak,
+            "step_ms_dist": step_dist,
             "clocks": clk,
             "gpu_launches": launches_per_step(args.mode, B, gcfg) * K,
             "loss_sum_last_step": loss_total,
