@@ -69,8 +69,8 @@ def parse():
     return ap.parse_args()
 
 
-def workload_desc(cfg, variant):
-    return (f"{cfg.name}: B={cfg.B_per_gpu}/GPU, Tmax={cfg.Tmax}, Umax={cfg.Umax}, V={cfg.V}, fp32 logits, "
+def workload_desc(cfg, variant, dtype="f32"):
+    return (f"{cfg.name}: B={cfg.B_per_gpu}/GPU, Tmax={cfg.Tmax}, Umax={cfg.Umax}, V={cfg.V}, {dtype} logits, "
             f"{'RNN-T' if variant == 'rnnt' else 'W-RNNT ' + variant}"
             f"{f' ({cfg.B} over {cfg.B // cfg.B_per_gpu} GPUs)' if cfg.B != cfg.B_per_gpu else ''}"
             f"{', variable lengths' if cfg.variable_lengths else ', full lengths'}")
@@ -358,15 +358,15 @@ def main():
         return statistics.mean(r[a].elapsed_time(r[b_]) for r in evs)
     k_ms = {"k1_lse_gather": span(0, 1), "k2_alpha_beta": span(4, 5), "k3_grad": span(2, 3),
             "k2_exposed_wait": span(1, 2)}
-    # per-step spread (median / p10 / p90): K1 start -> last kernel end of each step, from the
-    # event-carrying replay (loss_grad: K3 end; loss: K2 end)
+    # per-step spread (median / p10 / p90): K1 start -> K3 end of each step, from the
+    # event-carrying replay
     step_dist = None
-    if args.mode in ("loss_grad", "loss") and K >= 2:
-        ends = 3 if args.mode == "loss_grad" else 5
+    if args.mode == "loss_grad" and K >= 2:  # (loss mode has no event after the last chunk's K2)
+        ends = 3
         per = sorted(r[0].elapsed_time(r[ends]) for r in evs)
         q = lambda f: per[min(len(per) - 1, int(round(f * (len(per) - 1))))]
         step_dist = {"p10": q(0.1), "p50": q(0.5), "p90": q(0.9), "n": len(per),
-                     "span": "K1 start -> " + ("K3 end" if args.mode == "loss_grad" else "K2 end")}
+                     "span": "K1 start -> K3 end"}
     T_np, U_np = pb["logit_lens"], pb["target_lens"]
     valid_elems = int(sum(int(t) * (int(u) + 1) for t, u in zip(T_np, U_np))) * V
     all_elems = B * Tmax * Up1 * V
@@ -383,14 +383,14 @@ def main():
     peak, peak_src = measured_peaks()
     if args.mode == "loss_grad":
         roof = {"bound": "hbm", "kernel": "k3_grad", "achieved": k3_gbs, "peak": peak, "unit": "GB/s",
-                "frac": k3_gbs / peak, "traffic": ncu_traffic("k3_grad", args.config),
+                "frac": k3_gbs / peak, "traffic": ncu_traffic("k3_grad", args.config) if args.dtype == "f32" else None,
                 "algorithmic_bytes_per_launch": k3_bytes, "peak_source": peak_src}
     else:
         nbytes = k1_bytes + (k3_bytes if args.mode == "lattice" else 0)  # lattice: the whole loss+grad step
         gbs = nbytes / ((k1_ms if args.mode == "loss" else ms_step) / 1e3) / 1e9
         roof = {"bound": "hbm", "kernel": "k1_lse_gather" if args.mode == "loss" else f"step ({args.mode})",
                 "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
-                "traffic": ncu_traffic("k1_lse_gather", args.config) if args.mode == "loss" else None,
+                "traffic": ncu_traffic("k1_lse_gather", args.config) if args.mode == "loss" and args.dtype == "f32" else None,
                 "algorithmic_bytes_per_launch": nbytes, "peak_source": peak_src}
 
     # sanity: finite losses and the all-reduced sum
@@ -404,7 +404,7 @@ def main():
             "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
             "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": args.dtype, "data": "synthetic",
-            "config": {"workload": workload_desc(base, variant), "variant": variant, "B_per_gpu": B,
+            "config": {"workload": workload_desc(base, variant, args.dtype), "variant": variant, "B_per_gpu": B,
                        "global_batch": B * world, "parallelism": f"dp{world} (batch shards, NCCL all-reduce of "
                        f"the fp64 loss sum)", "l2": f"inputs {z.numel() * esize / 1e9:.2f} GB/GPU > 126 MB L2: no flush",
                        "grads": "in place" if inplace else "out of place",
