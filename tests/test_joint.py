@@ -88,6 +88,33 @@ def test_joint_grad_large_vocabulary(rb):
         assert err <= 2e-3 * np.abs(r).max(), (name, err, np.abs(r).max())
 
 
+@pytest.mark.parametrize("scale", [2.0, 8.0])
+def test_joint_large_preactivations(rb, scale):
+    """enc, pred scaled up (|f + g| up to ~6 sigma * scale: saturated tanh, h = +-1 in bf16 for large |x|):
+    loss and gradients still match the oracle's bf16(tanh(f + g)).  d enc / d pred bar 5e-3 of the largest
+    entry: they sum dh (stored in bf16, reading R23) times tanh' = 1 - h^2 over up to U+1 / T terms, and a
+    one-ulp difference in a bf16 dh (fp32 vs fp64 accumulation of dz W) shifts a term by 2^-8 of itself;
+    measured 2.6e-3 at scale 2 (5e-6 at scale 8, where most tanh' vanish)."""
+    B, T, U, H, V = 2, 17, 6, 256, 384
+    cfg = workloads.random_config(B, T, U, V, seed=53, variant="allow_ignore")
+    T_b, U_b = workloads.lengths(cfg)
+    y = workloads.targets(cfg, U_b)
+    enc, pred, W, b = workloads.joint_inputs(B, T, U, H, V, seed=53)
+    enc = (enc.float() * scale).to(torch.bfloat16)
+    pred = (pred.float() * scale).to(torch.bfloat16)
+    out = rb.rnnt_joint_loss_grad(enc.cuda(), pred.cuda(), W.cuda(), b.cuda(), y, T_b, U_b, 0, "allow_ignore")
+    l = rb.rnnt_joint_loss(enc.cuda(), pred.cuda(), W.cuda(), b.cuda(), y, T_b, U_b, 0, "allow_ignore")
+    torch.cuda.synchronize()
+    ref = oj.joint_loss_and_grads(enc.double().numpy(), pred.double().numpy(), W.double().numpy(),
+                                  b.double().numpy(), y, T_b, U_b, 0, "allow_ignore")
+    for losses in (l, out[0]):
+        lg = losses.cpu().numpy().astype(np.float64)
+        assert (np.abs(lg - ref[0]) / np.maximum(np.abs(ref[0]), 1.0)).max() <= 1e-5, (lg, ref[0])
+    for name, mine, r, bar in zip(("d_enc", "d_pred", "d_weight", "d_bias"), out[1:], ref[1:], (5e-3, 5e-3, 2e-3, 2e-3)):
+        err = np.abs(mine.cpu().numpy().astype(np.float64) - r).max()
+        assert err <= bar * np.abs(r).max(), (name, err, np.abs(r).max())
+
+
 def test_joint_rejects_misaligned_bias(rb):
     enc, pred, W, b = workloads.joint_inputs(1, 4, 2, 128, 130, seed=5)
     bb = torch.zeros(131, device="cuda")[1:]  # 4-byte offset
