@@ -595,6 +595,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
         const int nch = H / 16;            // 16-byte chunks per K half
         const int row_bytes = (H + kJointHPad) * 2;  // +16 B: conflict-free row reads without a swizzle
         uint8_t* my_row = stage_a + static_cast<size_t>(rl) * row_bytes;
+        const uint32_t sa_base = smem_u32(stage_a);  // 32-bit shared addresses for the builders' stores
         const uint4* f4 = reinterpret_cast<const uint4*>(a.f);
         const uint4* g4 = reinterpret_cast<const uint4*>(a.g);
         const int items = 32 * nch;        // (row of the quarter, chunk of the half)
@@ -634,8 +635,10 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
                     const bool in_range = i0 + j * 32 < items;
                     const int fro = __shfl_sync(0xffffffffu, fo, rr & 31), gro = __shfl_sync(0xffffffffu, go, rr & 31);
                     ok[j] = in_range && fro >= 0;
-                    fa[j] = ok[j] ? __ldg(f4 + fro + c) : make_uint4(0u, 0u, 0u, 0u);
-                    ga[j] = ok[j] ? __ldg(g4 + gro + c) : make_uint4(0u, 0u, 0u, 0u);
+                    // unconditional loads (row 0 stands in past the end; its output is zeroed below): no
+                    // per-register zero fill
+                    fa[j] = __ldg(f4 + (ok[j] ? fro : 0) + c);
+                    ga[j] = __ldg(g4 + (ok[j] ? gro : 0) + c);
                     rr += drr;
                     c += dc;
                     if (c >= nch) {
@@ -658,8 +661,9 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
                     }
                     const int r2 = q * 32 + rows_[j];
                     const int cg = kh * nch + cs[j];
-                    *reinterpret_cast<uint4*>(stage_a + static_cast<size_t>(r2) * row_bytes + (cg << 4)) =
-                        make_uint4(ow[0], ow[1], ow[2], ow[3]);
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sa_base + r2 * row_bytes + (cg << 4)),
+                                 "r"(ow[0]), "r"(ow[1]), "r"(ow[2]), "r"(ow[3])
+                                 : "memory");
                 }
             }
             __syncwarp();  // each thread copies its own row, written by the whole warp
