@@ -637,8 +637,8 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
                     ok[j] = in_range && fro >= 0;
                     // unconditional loads (row 0 stands in past the end; its output is zeroed below): no
                     // per-register zero fill
-                    fa[j] = __ldg(f4 + (ok[j] ? fro : 0) + c);
-                    ga[j] = __ldg(g4 + (ok[j] ? gro : 0) + c);
+                    fa[j] = __ldg(f4 + static_cast<uint32_t>((ok[j] ? fro : 0) + c));  // 32-bit index: one IMAD.WIDE
+                    ga[j] = __ldg(g4 + static_cast<uint32_t>((ok[j] ? gro : 0) + c));
                     rr += drr;
                     c += dc;
                     if (c >= nch) {
