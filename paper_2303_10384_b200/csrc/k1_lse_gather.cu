@@ -167,13 +167,14 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32, 3)
     const int U = min(U_b[b], Umax);
     int tt[2], uu[2];
     bool live[2];
+    tt[0] = r0 / Up1;  // one division per warp: row r0 + 1 is the next cell of the same or the next frame
+    uu[0] = r0 - tt[0] * Up1;
+    const bool wrap = uu[0] + 1 == Up1;
+    tt[1] = tt[0] + (wrap ? 1 : 0);
+    uu[1] = wrap ? 0 : uu[0] + 1;
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-        const int r = r0 + k;
-        tt[k] = r / Up1;
-        uu[k] = r - tt[k] * Up1;
-        live[k] = r < Tmax * Up1 && tt[k] < T && uu[k] <= U;  // padding rows are never read
-    }
+    for (int k = 0; k < 2; ++k)
+        live[k] = r0 + k < Tmax * Up1 && tt[k] < T && uu[k] <= U;  // padding rows are never read
     if (!live[0] && !live[1]) return;
     const int64_t row0 = static_cast<int64_t>(b) * Tmax * Up1 + r0;
     const uint64_t pol = l2_evict_first();
