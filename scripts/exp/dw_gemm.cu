@@ -1,3 +1,4 @@
+// Build: nvcc -O2 -gencode arch=compute_100a,code=sm_100a -o scripts/exp/dw_gemm scripts/exp/dw_gemm.cu -lcublas
 // Shape experiment for the joint backward's dW GEMM: [M x V] = A[M x R] . B[R x V]^T-view, bf16 in, fp32 out.
 #include <cublas_v2.h>
 #include <cuda_bf16.h>
