@@ -470,9 +470,12 @@ def main():
         threads = oracle_threads(base, args.cpu_threads)
         ids = [i % base.B_per_gpu for i in range(threads)]
         secs = oracle_sample(base, variant, threads, ids)
+        secs1 = oracle_sample(base, variant, 1, ids[:1])  # the oracle on one core too
         line["cpu_baseline"] = {"value": len(ids) / secs, "unit": UNIT, "cores": threads, "kind": "oracle",
                                 "sample": f"{len(ids)} utterances of {base.name} (one per OpenMP thread), full "
-                                          f"double-precision loss+grad, {secs:.1f} s wall",
+                                          f"double-precision loss+grad, {secs:.1f} s wall; single-core: 1 "
+                                          f"utterance, {secs1:.2f} s",
+                                "single_core_value": 1.0 / secs1,
                                 "host_cores_available": host_cores()}
     if rank == 0:
         print(json.dumps(line), flush=True)
