@@ -200,6 +200,20 @@ __device__ __forceinline__ float2 tanh2_mufu(float x0, float x1) {
     const float2 d = upk(fadd2(pk(ex2(y.x), ex2(y.y)), pk(1.f, 1.f)));
     return upk(ffma2(pk(rcp_approx(d.x), rcp_approx(d.y)), pk(-2.f, -2.f), pk(1.f, 1.f)));
 }
+// z[k] for a per-lane k in [0, 32) without local memory: a 5-level select tree (31 FSEL) instead of 32
+// compare-and-move pairs.
+__device__ __forceinline__ float select32(const float (&z)[32], int k) {
+    float s[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) s[i] = (k & 1) ? z[2 * i + 1] : z[2 * i];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s[i] = (k & 2) ? s[2 * i + 1] : s[2 * i];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) s[i] = (k & 4) ? s[2 * i + 1] : s[2 * i];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) s[i] = (k & 8) ? s[2 * i + 1] : s[2 * i];
+    return (k & 16) ? s[1] : s[0];
+}
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
     return *reinterpret_cast<const uint32_t*>(&v);
@@ -553,11 +567,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
                         for (int j = 0; j < 32; ++j)
                             if (v0 + j == a.blank) zb = z[j];
                     }
-                    if (static_cast<unsigned>(yv - v0) < 32u) {
-#pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            if (v0 + j == yv) zy = z[j];
-                    }
+                    if (static_cast<unsigned>(yv - v0) < 32u) zy = select32(z, yv - v0);  // some lane's label is in most chunks
                 }
                 tc_fence_before();
                 mbar_arrive(&acc_empty[acc]);
