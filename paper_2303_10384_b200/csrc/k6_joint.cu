@@ -295,6 +295,8 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
     uint64_t* acc_full = a_full + 2;                 // [kAccBufs]
     uint64_t* acc_empty = a_full + 2 + kAccBufs;     // [kAccBufs]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_full + 2 + 2 * kAccBufs);
+    // kGrad: per epilogue warp, a 32-row x 32-column bf16 dz staging block (2 KB), 16-byte chunks XOR-swizzled
+    uint8_t* dzst = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tmem_slot + 4) + 127) & ~uintptr_t(127));
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int H = a.H, V = a.V;
@@ -433,7 +435,6 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
             if constexpr (kGrad) {
                 // Per-row occupancies of the two scored arcs leaving (t,u), as K3 (k3_grad.cu): padded rows,
                 // invalid or no-path utterances (logP not finite) get dz = 0.
-                const int64_t crow = tile * kRowsPerTile + rl;  // compact row: dz / h row index
                 const double lP = in ? a.logp[b] : 0.0;
                 const bool gl = live && isfinite(lP);
                 float gam = 0.f, sb = 0.f, sy = 0.f, lsel = INFINITY;
@@ -474,7 +475,6 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
                         uint32_t r[32];
                         TMEM_LD32(lane_base + kAccCol0 + acc * kNTile + c * 32, r);
                         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                        if (crow >= rows) continue;
                         float g[32];
 #pragma unroll
                         for (int j = 0; j < 8; ++j) {
@@ -498,15 +498,34 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
                             for (int j = 0; j < 32; ++j)
                                 if (v0 + j == gy) g[j] -= sy;
                         }
-                        uint4* dst = reinterpret_cast<uint4*>(a.dz_out + crow * NT * kNTile + v0);
+                        // dz through the warp's staging block: each lane writes its row's 4 chunks, then reads back
+                        // (row = lane / 4 + 8 s, chunk = lane % 4) so that every global store instruction writes
+                        // 8 whole 64-byte row segments (8 L1 wavefronts instead of 32 for thread-per-row stores)
+                        const uint32_t st = smem_u32(dzst) + static_cast<uint32_t>(warp - 4) * 2048u;
+                        __syncwarp();  // the previous chunk's reads are done
 #pragma unroll
                         for (int q4 = 0; q4 < 4; ++q4) {
+                            const uint32_t w0 = gl ? pack_bf16x2(g[8 * q4 + 0], g[8 * q4 + 1]) : 0u;
+                            const uint32_t w1 = gl ? pack_bf16x2(g[8 * q4 + 2], g[8 * q4 + 3]) : 0u;
+                            const uint32_t w2 = gl ? pack_bf16x2(g[8 * q4 + 4], g[8 * q4 + 5]) : 0u;
+                            const uint32_t w3 = gl ? pack_bf16x2(g[8 * q4 + 6], g[8 * q4 + 7]) : 0u;
+                            const uint32_t ad = st + lane * 64u + ((q4 ^ ((lane >> 1) & 3)) << 4);
+                            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(ad), "r"(w0), "r"(w1), "r"(w2),
+                                         "r"(w3)
+                                         : "memory");
+                        }
+                        __syncwarp();
+#pragma unroll
+                        for (int s4 = 0; s4 < 4; ++s4) {
+                            const int rr = (lane >> 2) + 8 * s4, kk = lane & 3;
                             uint4 o;
-                            o.x = gl ? pack_bf16x2(g[8 * q4 + 0], g[8 * q4 + 1]) : 0u;
-                            o.y = gl ? pack_bf16x2(g[8 * q4 + 2], g[8 * q4 + 3]) : 0u;
-                            o.z = gl ? pack_bf16x2(g[8 * q4 + 4], g[8 * q4 + 5]) : 0u;
-                            o.w = gl ? pack_bf16x2(g[8 * q4 + 6], g[8 * q4 + 7]) : 0u;
-                            dst[q4] = o;
+                            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                                         : "=r"(o.x), "=r"(o.y), "=r"(o.z), "=r"(o.w)
+                                         : "r"(st + rr * 64u + ((kk ^ ((rr >> 1) & 3)) << 4))
+                                         : "memory");
+                            const int64_t orow = tile * kRowsPerTile + q * 32 + rr;
+                            if (orow < rows)
+                                *reinterpret_cast<uint4*>(a.dz_out + orow * NT * kNTile + v0 + kk * 8) = o;
                         }
                     }
                     tc_fence_before();
@@ -782,8 +801,9 @@ __global__ void __launch_bounds__(256) k6_rowmap(const int32_t* __restrict__ T_b
     if (b == B - 1 && blockIdx.x == 0 && threadIdx.x == 0) *nrows = off + n;
 }
 
-size_t joint_smem_bytes(int H, int V, int stages) {  // V = 0: bias not staged (!kSB)
-    return 1024 + static_cast<size_t>(stages) * kStageBytes + static_cast<size_t>(kRowsPerTile) * (H + kJointHPad) * 2 +
+size_t joint_smem_bytes(int H, int V, int stages, bool grad) {  // V = 0: bias not staged (!kSB)
+    return (grad ? 8 * 2048 + 128 : 0) +  // kGrad: the epilogue warps' dz staging blocks
+           1024 + static_cast<size_t>(stages) * kStageBytes + static_cast<size_t>(kRowsPerTile) * (H + kJointHPad) * 2 +
            static_cast<size_t>((V + kNTile - 1) / kNTile * kNTile) * 4 + 2 * kRowsPerTile * 16 + (2 * kMaxStages + 2 + 2 * kAccBufs) * 8 + 16;
 }
 
@@ -859,8 +879,8 @@ rnnt_status joint_front(const void* enc, const void* pred, const void* weight, c
     int stages = kMaxStages;
     const bool sb = V <= kSBiasMaxV;  // bias staged in shared memory (small vocabularies), else read from global
     const int Vs = sb ? V : 0;
-    while (stages > 2 && joint_smem_bytes(H, Vs, stages) > static_cast<size_t>(smem_max)) --stages;
-    const size_t smem = joint_smem_bytes(H, Vs, stages);
+    while (stages > 2 && joint_smem_bytes(H, Vs, stages, g != nullptr) > static_cast<size_t>(smem_max)) --stages;
+    const size_t smem = joint_smem_bytes(H, Vs, stages, g != nullptr);
     if (smem > static_cast<size_t>(smem_max)) return RNNT_ERR_UNSUPPORTED;
     auto kern = sb ? (g ? (cl > 1 ? k6_joint_lse<true, 2, true> : k6_joint_lse<true, 1, true>)
                         : (cl > 1 ? k6_joint_lse<false, 2, true> : k6_joint_lse<false, 1, true>))
