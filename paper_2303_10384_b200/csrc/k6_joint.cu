@@ -651,33 +651,22 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
                 fo = (b * a.Tmax + t) * (H / 8) + kh * nch;
                 go = (b * (a.Umax + 1) + u) * (H / 8) + kh * nch;
             }
-            int rr = lane / nch, c = lane - (lane / nch) * nch;  // this lane's first item
-            const int drr = 32 / nch, dc = 32 - drr * nch;        // item += 32 (nch in {8, 16, 24, 32})
-            for (int i0 = 0; i0 < items; i0 += 4 * 32) {
+            // items = 32 nch is a multiple of 4 * 32 (nch in {8, 16, 24, 32}): every batch is full
+            auto batch = [&](const int (&rows_)[4], const int (&cs)[4]) {
                 uint4 fa[4], ga[4];
-                int rows_[4], cs[4];
                 bool ok[4];
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                    rows_[j] = rr;
-                    cs[j] = c;
-                    const bool in_range = i0 + j * 32 < items;
-                    const int fro = __shfl_sync(0xffffffffu, fo, rr & 31), gro = __shfl_sync(0xffffffffu, go, rr & 31);
-                    ok[j] = in_range && fro >= 0;
+                    const int fro = __shfl_sync(0xffffffffu, fo, rows_[j] & 31);
+                    const int gro = __shfl_sync(0xffffffffu, go, rows_[j] & 31);
+                    ok[j] = fro >= 0;
                     // unconditional loads (row 0 stands in past the end; its output is zeroed below): no
-                    // per-register zero fill
-                    fa[j] = __ldg(f4 + static_cast<uint32_t>((ok[j] ? fro : 0) + c));  // 32-bit index: one IMAD.WIDE
-                    ga[j] = __ldg(g4 + static_cast<uint32_t>((ok[j] ? gro : 0) + c));
-                    rr += drr;
-                    c += dc;
-                    if (c >= nch) {
-                        c -= nch;
-                        ++rr;
-                    }
+                    // per-register zero fill; 32-bit indices: one IMAD.WIDE per load
+                    fa[j] = __ldg(f4 + static_cast<uint32_t>((ok[j] ? fro : 0) + cs[j]));
+                    ga[j] = __ldg(g4 + static_cast<uint32_t>((ok[j] ? gro : 0) + cs[j]));
                 }
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                    if (i0 + j * 32 >= items) break;
                     const uint32_t fw[4] = {fa[j].x, fa[j].y, fa[j].z, fa[j].w};
                     const uint32_t gw[4] = {ga[j].x, ga[j].y, ga[j].z, ga[j].w};
                     uint32_t ow[4];
@@ -693,6 +682,31 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
                     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sa_base + r2 * row_bytes + (cg << 4)),
                                  "r"(ow[0]), "r"(ow[1]), "r"(ow[2]), "r"(ow[3])
                                  : "memory");
+                }
+            };
+            if (nch == 32) {  // H = 512: lane = chunk, item j of a batch = row i0 / 32 + j
+                for (int i0 = 0; i0 < items; i0 += 4 * 32) {
+                    const int r0 = i0 >> 5;
+                    const int rows_[4] = {r0, r0 + 1, r0 + 2, r0 + 3}, cs[4] = {lane, lane, lane, lane};
+                    batch(rows_, cs);
+                }
+            } else {
+                int rr = lane / nch, c = lane - (lane / nch) * nch;  // this lane's first item
+                const int drr = 32 / nch, dc = 32 - drr * nch;        // item += 32
+                for (int i0 = 0; i0 < items; i0 += 4 * 32) {
+                    int rows_[4], cs[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        rows_[j] = rr;
+                        cs[j] = c;
+                        rr += drr;
+                        c += dc;
+                        if (c >= nch) {
+                            c -= nch;
+                            ++rr;
+                        }
+                    }
+                    batch(rows_, cs);
                 }
             }
             __syncwarp();  // each thread copies its own row, written by the whole warp
