@@ -27,6 +27,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdio>
 
 #include "common.cuh"
@@ -652,18 +653,21 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
                 go = (b * (a.Umax + 1) + u) * (H / 8) + kh * nch;
             }
             // items = 32 nch is a multiple of 4 * 32 (nch in {8, 16, 24, 32}): every batch is full
-            auto batch = [&](const int (&rows_)[4], const int (&cs)[4]) {
+            // fast: the tile has no rows past the end and no diagnostics -> no per-item / per-word selects
+            const bool fast = (tile + 1) * kRowsPerTile <= rows && a.dbg == 0;
+            auto batch = [&](const int (&rows_)[4], const int (&cs)[4], auto fast_c) {
+                constexpr bool kFast = decltype(fast_c)::value;
                 uint4 fa[4], ga[4];
                 bool ok[4];
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     const int fro = __shfl_sync(0xffffffffu, fo, rows_[j] & 31);
                     const int gro = __shfl_sync(0xffffffffu, go, rows_[j] & 31);
-                    ok[j] = fro >= 0;
+                    ok[j] = kFast || fro >= 0;
                     // unconditional loads (row 0 stands in past the end; its output is zeroed below): no
                     // per-register zero fill; 32-bit indices: one IMAD.WIDE per load
-                    fa[j] = __ldg(f4 + static_cast<uint32_t>((ok[j] ? fro : 0) + cs[j]));
-                    ga[j] = __ldg(g4 + static_cast<uint32_t>((ok[j] ? gro : 0) + cs[j]));
+                    fa[j] = __ldg(f4 + static_cast<uint32_t>((kFast || ok[j] ? fro : 0) + cs[j]));
+                    ga[j] = __ldg(g4 + static_cast<uint32_t>((kFast || ok[j] ? gro : 0) + cs[j]));
                 }
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
@@ -675,7 +679,8 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
                         const float2 x = unpack_bf16x2(fw[e]), y = unpack_bf16x2(gw[e]);
                         const float2 xs = upk(fadd2(pk(x.x, x.y), pk(y.x, y.y)));
                         const float2 h = tanh2_mufu(xs.x, xs.y);
-                        ow[e] = !ok[j] ? 0u : (a.dbg & 1) ? (fw[e] ^ gw[e]) : pack_bf16x2(h.x, h.y);
+                        ow[e] = kFast ? pack_bf16x2(h.x, h.y)
+                                      : !ok[j] ? 0u : (a.dbg & 1) ? (fw[e] ^ gw[e]) : pack_bf16x2(h.x, h.y);
                     }
                     const int r2 = q * 32 + rows_[j];
                     const int cg = kh * nch + cs[j];
@@ -688,7 +693,10 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
                 for (int i0 = 0; i0 < items; i0 += 4 * 32) {
                     const int r0 = i0 >> 5;
                     const int rows_[4] = {r0, r0 + 1, r0 + 2, r0 + 3}, cs[4] = {lane, lane, lane, lane};
-                    batch(rows_, cs);
+                    if (fast)
+                        batch(rows_, cs, std::true_type{});
+                    else
+                        batch(rows_, cs, std::false_type{});
                 }
             } else {
                 int rr = lane / nch, c = lane - (lane / nch) * nch;  // this lane's first item
@@ -706,7 +714,10 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
                             ++rr;
                         }
                     }
-                    batch(rows_, cs);
+                    if (fast)
+                        batch(rows_, cs, std::true_type{});
+                    else
+                        batch(rows_, cs, std::false_type{});
                 }
             }
             __syncwarp();  // each thread copies its own row, written by the whole warp
