@@ -17,7 +17,7 @@ agg = collections.OrderedDict()
 out = [f"# ncu --set full --clock-control none ({tag}); one bench step of {cfg}; kernels launched per utterance chunk",
        f"# report: {os.path.basename(rep)}"]
 for r in rows[2:]:
-    name = r[ix["Kernel Name"]].split("::")[-1].split("(")[0]
+    name = r[ix["Kernel Name"]].split("(")[0].split("::")[-1]  # strip the argument list first
     fam = name.split("<")[0]
     out.append(f"\n[{name}]  grid={r[ix['launch__grid_size']]} block={r[ix['launch__block_size']]}")
     for k in keys:
