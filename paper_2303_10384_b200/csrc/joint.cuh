@@ -34,5 +34,9 @@ rnnt_status joint_front(const void* enc, const void* pred, const void* weight, c
 
 constexpr int kJointVTile = 128;  // K6's N tile: dz rows are padded to a multiple of it
 constexpr int kJointHPad = 8;     // h rows carry 8 extra bf16 columns: (1, 0, ..., 0), for dbias in the dW GEMM
+// h's global row stride, H + 64 bf16: 128-byte aligned rows (the staging tile's H + 8 rows, stored as they are,
+// start at a different 16-byte offset mod 128 each and cost K7 +21 % DRAM reads, profiles/r01_v17_k7_ncu_full.txt);
+// the dW GEMM reads columns [0, H + kJointHPad) of it (lda = H + kJointHGPad).
+constexpr int kJointHGPad = 64;
 
 }  // namespace rnnt

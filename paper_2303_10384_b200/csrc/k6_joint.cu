@@ -249,7 +249,7 @@ struct JointArgs {
     const double* logp;
     const float* grad_scale;
     __nv_bfloat16* dz_out;  // [rows][Vp] row-major, Vp = V rounded up to whole N tiles (tail columns 0)
-    __nv_bfloat16* h_out;   // [rows][H + kJointHPad]: h, then (1, 0, ..., 0)
+    __nv_bfloat16* h_out;   // [rows][H + kJointHGPad]: h, then (1, 0, ..., 0), then unused
 };
 
 // kGrad = false: the forward (lse + gathers).  kGrad = true: the backward's first pass -- the same GEMM
@@ -640,7 +640,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
         int p_next = -1;
         auto build = [&](int64_t tile, int p) {
             if constexpr (kGrad) {  // the previous tile's h store must have read the staging buffer
-                if (warp == 12 && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                if (warp == 12) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                 asm volatile("bar.sync 4, 256;" ::: "memory");  // the 8 builder warps
             }
             // lane r: chunk offsets (16-byte units) of row q*32 + r's f and g rows, -1 past the end
@@ -722,20 +722,22 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
             }
             __syncwarp();  // each thread copies its own row, written by the whole warp
             if constexpr (kGrad) {
-                // h for the dW GEMM: the staging rows ARE h's global rows (H + 8 columns, the pad = (1, 0, ..)),
-                // and the tile's rows are consecutive compact rows -> ONE bulk async copy (TMA engine) of the
-                // tile, issued once all builders have written it; it overlaps the TMEM copy and the next build.
+                // h for the dW GEMM: the staging rows ARE h's rows (H + 8 columns, the pad = (1, 0, ..)) and the
+                // tile's rows are consecutive compact rows; stored at the 128-byte aligned global stride
+                // H + kJointHGPad by one bulk async copy (TMA engine) per row, lane l of warp 12 taking rows
+                // l, l + 32, .. once all builders have written the tile; it overlaps the TMEM copy and the next build.
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 asm volatile("bar.sync 4, 256;" ::: "memory");
-                if (warp == 12 && lane == 0) {
+                if (warp == 12) {
                     const int64_t nv = std::min<int64_t>(kRowsPerTile, rows - tile * kRowsPerTile);
-                    if (nv > 0) {
-                        __nv_bfloat16* dst = a.h_out + tile * kRowsPerTile * (H + kJointHPad);
+                    for (int r = lane; r < nv; r += 32) {
+                        __nv_bfloat16* dst = a.h_out + (tile * kRowsPerTile + r) * (H + kJointHGPad);
                         asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
-                                     "r"(smem_u32(stage_a)), "r"(static_cast<uint32_t>(nv * row_bytes))
+                                     "r"(smem_u32(stage_a) + static_cast<uint32_t>(r * row_bytes)),
+                                     "r"(static_cast<uint32_t>(row_bytes))
                                      : "memory");
-                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                     }
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 }
             }
         };
@@ -783,7 +785,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
         if (warp == 8) o[7] = w_accfull;
         if (warp == 12) o[6] = w_aempty;
     }
-    if (kGrad && warp == 12 && lane == 0)  // the last h store completes before the CTA's shared memory is released
+    if (kGrad && warp == 12)  // the last h stores complete before the CTA's shared memory is released
         asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     tc_fence_before();
     if constexpr (kCl > 1)

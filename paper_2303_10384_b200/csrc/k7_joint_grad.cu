@@ -30,13 +30,13 @@ namespace {
 
 constexpr int kJointMaxDevices = 64;
 
-// Zero rows [*nrows, R) of dz ([R][Vp]) and h ([R][Hs]) so the padded-row GEMMs see no stale data.
-__global__ void __launch_bounds__(256) k7_zero_tail(const int* __restrict__ nrows, int64_t R, int Vp, int Hs,
+// Zero rows [*nrows, R) of dz ([R][Vp]) and h ([R][Hg]) so the padded-row GEMMs see no stale data.
+__global__ void __launch_bounds__(256) k7_zero_tail(const int* __restrict__ nrows, int64_t R, int Vp, int Hg,
                                                     __nv_bfloat16* dz, __nv_bfloat16* h) {
     const int64_t r0 = *nrows;
-    const int64_t nz = (R - r0) * Vp / 8, nh = (R - r0) * Hs / 8;  // 16-byte units
+    const int64_t nz = (R - r0) * Vp / 8, nh = (R - r0) * Hg / 8;  // 16-byte units
     uint4* z4 = reinterpret_cast<uint4*>(dz + r0 * Vp);
-    uint4* h4 = reinterpret_cast<uint4*>(h + r0 * Hs);
+    uint4* h4 = reinterpret_cast<uint4*>(h + r0 * Hg);
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nz + nh;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         if (i < nz)
@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(128) k7_reduce(const __nv_bfloat16* __restrict
     const int t0 = chunk * kTC;
     const int tn = max(0, min(T - t0, kTC));
     const int c = blockIdx.z * 128 + lane * 4;
-    const int Hs = H + kJointHPad;
+    const int Hg = H + kJointHGPad;
     float4 enc[kTC];  // this warp's partial of d enc(b, t0 + k) over its units (registers; shared at the end)
 #pragma unroll
     for (int k = 0; k < kTC; ++k) enc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(128) k7_reduce(const __nv_bfloat16* __restrict
         auto ld = [&](int k, uint2& dw, uint2& hw) {
             const int64_t r = r0 + static_cast<int64_t>(k) * (U + 1);
             dw = __ldcs(reinterpret_cast<const uint2*>(dh + r * H + c));
-            hw = __ldcs(reinterpret_cast<const uint2*>(h + r * Hs + c));
+            hw = __ldcs(reinterpret_cast<const uint2*>(h + r * Hg + c));
         };
         if (tn == kTC) {  // whole chunk: all kTC rows' loads issued before any use
             uint2 dw[kTC], hw[kTC];
@@ -236,7 +236,7 @@ GradLayout grad_layout(int B, int Tmax, int Umax, int H, int V) {
     off += align256(std::max(sizeof(__nv_bfloat16) * L.R * L.Vp,
                              sizeof(float) * static_cast<size_t>((Tmax + kTC - 1) / kTC) * B * (Umax + 1) * H));
     L.h = off;
-    off += align256(sizeof(__nv_bfloat16) * L.R * (H + kJointHPad));
+    off += align256(sizeof(__nv_bfloat16) * L.R * (H + kJointHGPad));
     L.dh = off;
     off += align256(sizeof(__nv_bfloat16) * L.R * H);
     L.dwa = off;
@@ -300,7 +300,7 @@ extern "C" rnnt_status rnnt_joint_loss_grad(const void* enc, const void* pred, c
     // every padded row with the tail [*nrows, R) zeroed on the device
     const int R = static_cast<int>(valid_rows >= 0 ? valid_rows : L.R);
     if (valid_rows < 0) {
-        k7_zero_tail<<<1184, 256, 0, s>>>(nrows, L.R, L.Vp, Hs, dz, hb);
+        k7_zero_tail<<<1184, 256, 0, s>>>(nrows, L.R, L.Vp, H + kJointHGPad, dz, hb);
     } else {
         k7_check_rows<<<1, 256, 0, s>>>(nrows, valid_rows, B, losses);
     }
@@ -323,7 +323,7 @@ extern "C" rnnt_status rnnt_joint_loss_grad(const void* enc, const void* pred, c
                          &zero, dh, CUDA_R_16BF, H, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT) != CUBLAS_STATUS_SUCCESS)
             return RNNT_ERR_CUDA;
         // [dW | dbias]^T [(H + 8) x V] = [h | 1 0..0]^T [(H + 8) x R] . dz [R x V]
-        if (cublasGemmEx(hd, CUBLAS_OP_N, CUBLAS_OP_T, Hs, V, R, &one, hb, CUDA_R_16BF, Hs, dz, CUDA_R_16BF, L.Vp,
+        if (cublasGemmEx(hd, CUBLAS_OP_N, CUBLAS_OP_T, Hs, V, R, &one, hb, CUDA_R_16BF, H + kJointHGPad, dz, CUDA_R_16BF, L.Vp,
                          &zero, dwa, CUDA_R_32F, Hs, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT) != CUBLAS_STATUS_SUCCESS)
             return RNNT_ERR_CUDA;
     }

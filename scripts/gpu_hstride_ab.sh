@@ -1,0 +1,13 @@
+#!/bin/bash
+mkdir -p gpurun_out/hs
+timeout -s KILL 600 python -m pytest tests/test_joint.py tests/test_canaries.py -m gpu -q -p no:cacheprovider > gpurun_out/hs/pytest.log 2>&1
+echo "pytest exit $?" >> gpurun_out/hs/pytest.log
+for rep in 1 2 3; do
+  for lib in paper_2303_10384_b200/lib/librnnt_b200.so paper_2303_10384_b200/lib/ab/librnnt_b200_old.so; do
+    n=$(basename $lib .so)
+    for cfg in c3 p124; do
+      RNNT_B200_LIB=$PWD/$lib timeout -s KILL 300 python bench.py --mode joint_grad --config $cfg --no-e2e \
+        --no-cpu-baseline > gpurun_out/hs/${n}_${cfg}_$rep.json 2>/dev/null
+    done
+  done
+done
