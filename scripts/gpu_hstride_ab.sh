@@ -1,4 +1,6 @@
 #!/bin/bash
+# A/B of the aligned h stride: the in-tree library vs lib/ab/librnnt_b200_old.so (the previous commit built and
+# copied there by hand; git-ignored), joint training step c3 / p124, 3 alternating reps, plus the joint parity tests.
 mkdir -p gpurun_out/hs
 timeout -s KILL 600 python -m pytest tests/test_joint.py tests/test_canaries.py -m gpu -q -p no:cacheprovider > gpurun_out/hs/pytest.log 2>&1
 echo "pytest exit $?" >> gpurun_out/hs/pytest.log
