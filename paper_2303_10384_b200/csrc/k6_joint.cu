@@ -640,7 +640,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
         int p_next = -1;
         auto build = [&](int64_t tile, int p) {
             if constexpr (kGrad) {  // the previous tile's h store must have read the staging buffer
-                if (warp == 12) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // each thread its own row copies
                 asm volatile("bar.sync 4, 256;" ::: "memory");  // the 8 builder warps
             }
             // lane r: chunk offsets (16-byte units) of row q*32 + r's f and g rows, -1 past the end
@@ -724,13 +724,15 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
             if constexpr (kGrad) {
                 // h for the dW GEMM: the staging rows ARE h's rows (H + 8 columns, the pad = (1, 0, ..)) and the
                 // tile's rows are consecutive compact rows; stored at the 128-byte aligned global stride
-                // H + kJointHGPad by one bulk async copy (TMA engine) per row, lane l of warp 12 taking rows
-                // l, l + 32, .. once all builders have written the tile; it overlaps the TMEM copy and the next build.
+                // H + kJointHGPad by one bulk async copy (TMA engine) per row, spread over the builder warps
+                // 12-15 (lane l of warp 12 + j takes row 32 j + l: one copy per thread, the issue cost shared)
+                // once all builders have written the tile; it overlaps the TMEM copy and the next build.
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 asm volatile("bar.sync 4, 256;" ::: "memory");
-                if (warp == 12) {
+                {
                     const int64_t nv = std::min<int64_t>(kRowsPerTile, rows - tile * kRowsPerTile);
-                    for (int r = lane; r < nv; r += 32) {
+                    const int r = (warp - 12) * 32 + lane;
+                    if (r < nv) {
                         __nv_bfloat16* dst = a.h_out + (tile * kRowsPerTile + r) * (H + kJointHGPad);
                         asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
                                      "r"(smem_u32(stage_a) + static_cast<uint32_t>(r * row_bytes)),
@@ -785,7 +787,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
         if (warp == 8) o[7] = w_accfull;
         if (warp == 12) o[6] = w_aempty;
     }
-    if (kGrad && warp == 12)  // the last h stores complete before the CTA's shared memory is released
+    if (kGrad && warp >= 12)  // the last h stores complete before the CTA's shared memory is released
         asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     tc_fence_before();
     if constexpr (kCl > 1)
