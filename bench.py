@@ -7,7 +7,15 @@ that sum.  Default workload: c3 = BASELINE.json configs[2] (B=32 per GPU, T=500,
 plain RNN-T), weak scaling (32 utterances per GPU, global ids rank*32 + i).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--variant rnnt|force_final|allow_ignore]
+                  [--scaling weak|strong] [--backend nccl|gloo]
   python bench.py --impl reference ...   # the CPU oracle on the host cores (bounded sample)
+
+--gpus N > 1 from a bare shell re-executes itself under `torch.distributed.run` (one rank per GPU, 127.0.0.1);
+under torchrun it reads RANK / LOCAL_RANK / WORLD_SIZE.  --scaling weak keeps B per GPU fixed (the default;
+global ids rank*B + i); strong shards the config's global batch (c3: 32 utterances as 32/16/8/4 over
+1/2/4/8 GPUs).  At every N the K timed steps replay as one CUDA graph (the NCCL all-reduce of the loss sum
+is captured with them); --backend gloo (several ranks may share one GPU: a harness check, not a bench
+number) runs eagerly.
 
 Prints ONE JSON line on rank 0.
 """
@@ -66,7 +74,38 @@ def parse():
                          "(the default at N=1 for --mode loss_grad / loss: no host launch overhead between kernels)")
     ap.add_argument("--inplace", action="store_true",
                     help="write grads over the logits (automatic when two copies do not fit in HBM, e.g. c5)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: B per GPU fixed as N grows (BASELINE north_star (5)); strong: the config's global "
+                         "batch split over the N ranks")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N > 1 (gloo lets N ranks share one GPU: harness tests only)")
     return ap.parse_args()
+
+
+def free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch_cmd(argv, n, port):
+    """The torchrun command line that re-executes this script with n ranks (bench.py --gpus n from a bare
+    shell): same arguments, rendezvous on 127.0.0.1."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+            "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+
+
+def global_config(base, world, scaling):
+    """The global batch the N ranks share: weak = B per GPU x N (global ids rank*B + i), strong = the config's
+    own global batch (c3: 32), sharded contiguously."""
+    if scaling == "weak":
+        return dataclasses.replace(base, B=base.B_per_gpu * world)
+    if base.B < world:
+        raise SystemExit(f"--scaling strong: {base.B} utterances cannot be split over {world} ranks")
+    return base
 
 
 def workload_desc(cfg, variant, dtype="f32"):
@@ -86,7 +125,8 @@ def measured_peaks():
 
 
 def ncu_traffic(kernel: str, cfg_name: str):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu --set full capture."""
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch (the step's chunk launches averaged) from the
+    committed ncu --set full capture."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(path):
         return None
@@ -169,16 +209,19 @@ def oracle_sample(cfg, variant, nthreads, b_ids, pb=None):
     return time.perf_counter() - t0
 
 
+def n_chunks(B, cfg):
+    """Utterance chunks of one call (<= 4 when the call has >= 2^24 elements, see rnnt_api.cu overlap_chunks)."""
+    elems = B * cfg.Tmax * (cfg.Umax + 1) * cfg.V
+    return min(B, 4) if (B >= 2 and elems >= (1 << 24)) else 1
+
+
 def launches_per_step(mode, B, cfg):
-    """Our kernels per step: K1/K2/K3 once per utterance chunk (<= 4 chunks when the call has >= 2^24
-    elements, see rnnt_api.cu overlap_chunks) + the loss sum; viterbi = K1 + K4."""
+    """Our kernels per step: K1/K2/K3 once per utterance chunk + the loss sum; viterbi = K1 + K4."""
     if mode == "viterbi":
         return 2
     if mode == "lattice":
         return 6 + 1  # K1, L2, L3, L4, L5, L6 + loss sum (plus one memset)
-    elems = B * cfg.Tmax * (cfg.Umax + 1) * cfg.V
-    nch = min(B, 4) if (B >= 2 and elems >= (1 << 24)) else 1
-    return nch * (3 if mode == "loss_grad" else 2) + 1
+    return n_chunks(B, cfg) * (3 if mode == "loss_grad" else 2) + 1
 
 
 def host_cores():
@@ -226,7 +269,7 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": workload_desc(cfg, variant), "variant": variant},
+            "data": "synthetic", "config": ref_config(cfg, variant, args),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -234,18 +277,50 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def ref_config(cfg, variant, args):
+    """The GPU arm's config keys for the reference line (same workload, same batch per GPU)."""
+    world = args.gpus
+    gcfg = global_config(cfg, world, args.scaling)
+    B = len(list(range(gcfg.B))[0::world]) if args.scaling == "strong" else cfg.B_per_gpu
+    return {"workload": workload_desc(cfg, variant, args.dtype), "variant": variant, "B_per_gpu": B,
+            "global_batch": gcfg.B, "parallelism": f"dp{world} (batch shards, NCCL all-reduce of the fp64 loss sum)",
+            "l2": "n/a (host cores)", "grads": "out of place", "launch": "host (OpenMP, one utterance per thread)",
+            "scaling": args.scaling}
+
+
 # ------------------------------------------------------------------------------------------ GPU arm
+def capture_steps(step, K, evs, world):
+    """The K timed steps as one CUDA graph (and a second one carrying the per-kernel timing events).  At N > 1
+    the NCCL all-reduce is captured with the kernels, so every N launches the same way."""
+    graph, graph_ev = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        for i in range(K):
+            step(None)
+    with torch.cuda.graph(graph_ev):
+        for i in range(K):
+            step(evs[i] if evs is not None else None)
+    graph.replay()  # one untimed replay each: a graph's first launch uploads it
+    graph_ev.replay()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    return graph, graph_ev
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return subprocess.call(relaunch_cmd(sys.argv[1:], args.gpus, free_port()))
 
     import paper_2303_10384_b200 as rb
     from paper_2303_10384_b200 import dist as rdist
 
-    rank, world, local = rdist.init("nccl")
+    rank, world, local = rdist.init(args.backend)
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    local = rdist.device_index(local, args.backend)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if args.mode in ("joint", "joint_grad"):
@@ -253,7 +328,7 @@ def main():
 
     base = {**workloads.CONFIGS, **workloads.EXTRA_CONFIGS}[args.config]
     variant = args.variant or base.variant
-    gcfg = dataclasses.replace(base, B=base.B_per_gpu * world)   # weak scaling: B per GPU fixed
+    gcfg = global_config(base, world, args.scaling)
     b_ids = rdist.contiguous_shard(gcfg.B, rank, world)
     pb = workloads.problem(gcfg, b_ids=b_ids, device=dev)
     tdtype = {"f32": torch.float32, "bf16": torch.bfloat16, "f16": torch.float16}[args.dtype]
@@ -315,23 +390,15 @@ def main():
     torch.cuda.synchronize()
 
     graph = graph_ev = None
-    if not args.eager and world == 1 and args.mode in ("loss_grad", "loss"):
+    if not args.eager and args.backend == "nccl" and args.mode in ("loss_grad", "loss"):
         # All K timed steps captured as one CUDA graph (replayed once below): every kernel of every step runs,
         # only the host launch overhead goes.  The C-ABI call forks its K2 chunks onto internal streams and
-        # joins them back, so it is capturable (its internal streams were created by the warm-up calls).
+        # joins them back, so it is capturable (its internal streams were created by the warm-up calls); at
+        # N > 1 the NCCL all-reduce of the loss sum is captured too (warmed up above).
         # Timing events inside a graph become external event nodes, which cost a few microseconds each, so
         # the per-kernel split comes from a second graph of the same K steps with the events, replayed right
         # after the timed one.
-        graph, graph_ev = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
-            for i in range(K):
-                step(None)
-        with torch.cuda.graph(graph_ev):
-            for i in range(K):
-                step(evs[i])
-        graph.replay()  # one untimed replay each: a graph's first launch uploads it
-        graph_ev.replay()
-        torch.cuda.synchronize()
+        graph, graph_ev = capture_steps(step, K, evs, world)
 
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
@@ -351,7 +418,8 @@ def main():
     ms_local = start.elapsed_time(end)
     ms_total = rdist.max_over_ranks(ms_local, dev)
     ms_step = ms_total / K
-    value = B * world / (ms_step / 1e3)
+    units = int(rdist.sum_over_ranks(B, dev))  # utterances all ranks processed per step
+    value = units / (ms_step / 1e3)
 
     # per-kernel device durations inside the timed region (events: K1 start/end, K3 start/end, K2 start/end)
     def span(a, b_):
@@ -381,17 +449,25 @@ def main():
     k1_ms = k_ms.get("k1_lse_gather", ms_step)
     k1_gbs = k1_bytes / (k1_ms / 1e3) / 1e9
     peak, peak_src = measured_peaks()
+    nch = n_chunks(B, gcfg)  # K1 / K3 launches per step (one per utterance chunk)
     if args.mode == "loss_grad":
+        # per launch: the chunks' K3 launches run back to back on one stream, so the step's K3 bytes over the
+        # events' K3 span = one launch's bytes over its mean duration
+        traffic = ncu_traffic("k3_grad", args.config) if args.dtype == "f32" and world == 1 else None
         roof = {"bound": "hbm", "kernel": "k3_grad", "achieved": k3_gbs, "peak": peak, "unit": "GB/s",
-                "frac": k3_gbs / peak, "traffic": ncu_traffic("k3_grad", args.config) if args.dtype == "f32" else None,
-                "algorithmic_bytes_per_launch": k3_bytes, "peak_source": peak_src}
+                "frac": k3_gbs / peak, "traffic": traffic,
+                "algorithmic_bytes_per_launch": k3_bytes / nch, "launches_per_step": nch,
+                "algorithmic_bytes_per_step": k3_bytes, "peak_source": peak_src}
     else:
         nbytes = k1_bytes + (k3_bytes if args.mode == "lattice" else 0)  # lattice: the whole loss+grad step
         gbs = nbytes / ((k1_ms if args.mode == "loss" else ms_step) / 1e3) / 1e9
+        per = nch if args.mode == "loss" else 1
+        traffic = (ncu_traffic("k1_lse_gather", args.config) if args.mode == "loss" and args.dtype == "f32"
+                   and world == 1 else None)
         roof = {"bound": "hbm", "kernel": "k1_lse_gather" if args.mode == "loss" else f"step ({args.mode})",
                 "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
-                "traffic": ncu_traffic("k1_lse_gather", args.config) if args.mode == "loss" and args.dtype == "f32" else None,
-                "algorithmic_bytes_per_launch": nbytes, "peak_source": peak_src}
+                "traffic": traffic, "algorithmic_bytes_per_launch": nbytes / per,
+                "launches_per_step": per, "algorithmic_bytes_per_step": nbytes, "peak_source": peak_src}
 
     # sanity: finite losses and the all-reduced sum
     loss_total = float(loss_sum.item())
@@ -402,23 +478,26 @@ def main():
         line = {
             "metric": METRIC if args.mode == "loss_grad" else f"utterances/s {args.mode} (not the BASELINE metric)",
             "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
-            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": args.dtype, "data": "synthetic",
             "config": {"workload": workload_desc(base, variant, args.dtype), "variant": variant, "B_per_gpu": B,
-                       "global_batch": B * world, "parallelism": f"dp{world} (batch shards, NCCL all-reduce of "
-                       f"the fp64 loss sum)", "l2": f"inputs {z.numel() * esize / 1e9:.2f} GB/GPU > 126 MB L2: no flush",
+                       "global_batch": gcfg.B, "parallelism": f"dp{world} (batch shards, {args.backend.upper()} "
+                       f"all-reduce of the fp64 loss sum)", "l2": f"inputs {z.numel() * esize / 1e9:.2f} GB/GPU > 126 MB L2: no flush",
                        "grads": "in place" if inplace else "out of place",
                        **({"lattice": args.lattice} if args.mode == "lattice" else {}),
-                       "launch": (f"one CUDA graph of the {K} steps (kernel split: a second graph of the same "
-                                  f"{K} steps with timing events, replayed next)") if graph is not None else "eager"},
+                       "launch": (f"one CUDA graph of the {K} steps{' incl. the NCCL all-reduce' if world > 1 else ''} "
+                                  f"(kernel split: a second graph of the same {K} steps with timing events, "
+                                  f"replayed next)") if graph is not None else "eager",
+                       "scaling": args.scaling},
             "roofline": roof,
             "kernels_ms": k_ms,
             "kernel_gbs": {"k1_lse_gather": k1_gbs, "k3_grad": k3_gbs},
             "note": None if args.dtype == "f32" else "16-bit storage run (SURVEY §8(f) NEXT-1); the BASELINE "
                     "metric itself is fp32",
             "kernel_frac_of_peak": {"k1_lse_gather": k1_gbs / peak, "k3_grad": k3_gbs and k3_gbs / peak},
-            "step_frac_of_3pass_roofline": (3 * esize * valid_elems / (ms_step / 1e3) / 1e9) / peak,
-            "step_frac_of_2pass_bound": (2 * esize * valid_elems / (ms_step / 1e3) / 1e9) / peak,
+            **({"step_frac_of_3pass_roofline": (3 * esize * valid_elems / (ms_step / 1e3) / 1e9) / peak,
+                "step_frac_of_2pass_bound": (2 * esize * valid_elems / (ms_step / 1e3) / 1e9) / peak}
+               if args.mode == "loss_grad" else {}),
             "step_ms_dist": step_dist,
             "clocks": clk,
             "gpu_launches": launches_per_step(args.mode, B, gcfg) * K,
@@ -458,7 +537,7 @@ def main():
         e_ms = rdist.max_over_ranks(e_start.elapsed_time(e_end), dev) / args.e2e_steps
         h2d = zh.numel() * 4 + th.numel() * 4 + Th.numel() * 4 + Uh.numel() * 4
         d2h = gh.numel() * 4 + lh.numel() * 4
-        e2e = {"value": B * world / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+        e2e = {"value": units / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": e_ms, "steps": args.e2e_steps,
                "api": "rnnt_loss_host (pinned host buffers; chunked H2D / compute / D2H overlap)"}
         del dbuf
@@ -490,7 +569,7 @@ def main_joint(args, rb, rdist, rank, world, local, dev):
     log-softmax / Populate epilogue, then K2), inputs = Encoder / Predictor embeddings of size H."""
     base = {**workloads.CONFIGS, **workloads.EXTRA_CONFIGS}[args.config]
     variant = args.variant or base.variant
-    gcfg = dataclasses.replace(base, B=base.B_per_gpu * world)
+    gcfg = global_config(base, world, args.scaling)
     b_ids = rdist.contiguous_shard(gcfg.B, rank, world)
     H = args.hidden
     T_np, U_np = workloads.lengths(gcfg)
@@ -539,17 +618,8 @@ def main_joint(args, rb, rdist, rank, world, local, dev):
     if world > 1:
         torch.distributed.barrier()
     graph = graph_ev = None
-    if not args.eager and world == 1:
-        graph, graph_ev = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
-            for i in range(K):
-                step(None)
-        with torch.cuda.graph(graph_ev):
-            for i in range(K):
-                step(evs[i])
-        graph.replay()
-        graph_ev.replay()
-        torch.cuda.synchronize()
+    if not args.eager and args.backend == "nccl":
+        graph, graph_ev = capture_steps(step, K, evs, world)
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
         start.record()
@@ -566,7 +636,8 @@ def main_joint(args, rb, rdist, rank, world, local, dev):
     if world > 1:
         torch.distributed.barrier()
     ms_step = rdist.max_over_ranks(start.elapsed_time(end), dev) / K
-    value = B * world / (ms_step / 1e3)
+    units = int(rdist.sum_over_ranks(B, dev))
+    value = units / (ms_step / 1e3)
     k6_ms = statistics.mean(r[0].elapsed_time(r[1]) for r in evs) if not grad else None
     k2_ms = statistics.mean(r[2].elapsed_time(r[3]) for r in evs) if not grad else None
     rows = int(sum(int(t) * (int(u) + 1) for t, u in zip(T_np, U_np)))  # K6 runs on the valid cells only
@@ -588,11 +659,11 @@ def main_joint(args, rb, rdist, rank, world, local, dev):
                    "BASELINE metric)") if grad else "utterances/s fused joint+loss forward (not the BASELINE metric)",
         "value": value, "unit": UNIT,
         "n_gpus": world, "steps": K, "warmup": Wm, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": f"{base.name} shapes through the joint: B={B}/GPU, Tmax={Tmax}, Umax={Umax}, "
                                f"V={V}, H={H} (enc/pred bf16, W [V,H] bf16, fp32 accumulate), "
                                f"{'RNN-T' if variant == 'rnnt' else 'W-RNNT ' + variant}",
-                   "variant": variant, "B_per_gpu": B, "global_batch": B * world, "H": H,
+                   "variant": variant, "B_per_gpu": B, "global_batch": gcfg.B, "H": H, "scaling": args.scaling,
                    "l2": "no flush: the joint's inputs (enc/pred/W, "
                          f"{(enc.numel() + pred.numel() + W.numel()) * 2 / 1e6:.0f} MB) are meant to be L2/HBM "
                          "resident; the [B,T,U+1,V] logits are never written",
@@ -627,4 +698,4 @@ def main_joint(args, rb, rdist, rank, world, local, dev):
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main() or 0)

@@ -86,6 +86,49 @@ def _stream(stream):
     return ctypes.c_void_p(stream.cuda_stream)
 
 
+def _keep(stream, *tensors):
+    """The library queues its kernels on ``stream``; temporaries allocated here belong to the current stream's
+    pool.  When the caller passes another stream, record it on each temporary so that the caching allocator
+    does not hand their memory out again before the queued kernels are done with it."""
+    if stream is None or stream == torch.cuda.current_stream():
+        return
+    for t in tensors:
+        if isinstance(t, torch.Tensor) and t.is_cuda:
+            t.record_stream(stream)
+
+
+def _check_joint_inputs(enc, pred, weight):
+    """enc [B, Tmax, H], pred [B, Umax+1, H], weight [V, H]: contiguous CUDA bfloat16 on one device."""
+    for name, x in (("enc", enc), ("pred", pred), ("weight", weight)):
+        if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.bfloat16 and x.is_contiguous()):
+            raise TypeError(f"{name} must be a contiguous CUDA bfloat16 tensor (no CPU fallback)")
+    if enc.dim() != 3 or pred.dim() != 3 or weight.dim() != 2:
+        raise ValueError("shapes: enc [B, Tmax, H], pred [B, Umax+1, H], weight [V, H]")
+    B, Tmax, H = enc.shape
+    Up1 = pred.shape[1]
+    V = weight.shape[0]
+    if pred.shape != (B, Up1, H) or weight.shape != (V, H) or Up1 < 1:
+        raise ValueError("shapes: enc [B, Tmax, H], pred [B, Umax+1, H], weight [V, H]")
+    if pred.device != enc.device or weight.device != enc.device:
+        raise ValueError("enc, pred and weight must be on one device")
+    return B, Tmax, Up1 - 1, H, V
+
+
+def _check_f32_out(name, t, shape, device):
+    if not (isinstance(t, torch.Tensor) and t.dtype == torch.float32 and t.device == device and t.is_contiguous()
+            and tuple(t.shape) == tuple(shape)):
+        raise ValueError(f"{name} must be a contiguous float32 tensor of shape {tuple(shape)} on {device}")
+
+
+def _check_grad_scale(grad_scale, B, dev):
+    if grad_scale is None:
+        return None
+    grad_scale = torch.as_tensor(grad_scale).to(device=dev, dtype=torch.float32).contiguous()
+    if grad_scale.numel() != B:
+        raise ValueError(f"grad_scale needs {B} elements (one per utterance), got {grad_scale.numel()}")
+    return grad_scale
+
+
 def rnnt_workspace_bytes(B: int, Tmax: int, Umax: int) -> int:
     return int(library.rnnt_workspace_bytes(B, Tmax, Umax))
 
@@ -124,11 +167,11 @@ def _call(fn_variant, logits, targets, logit_lens, target_lens, blank, grads, gr
     if grads is not None and (grads.shape != logits.shape or not grads.is_contiguous()
                               or grads.dtype != logits.dtype or grads.device != dev):
         raise ValueError("grads must be contiguous, on the logits' device, with the logits' shape and dtype")
-    if grad_scale is not None:
-        grad_scale = grad_scale.to(device=dev, dtype=torch.float32).contiguous()
+    grad_scale = _check_grad_scale(grad_scale, B, dev)
     need = rnnt_workspace_bytes(B, Tmax, Umax)
     if workspace is None:
         workspace = torch.empty(max(need, 1), dtype=torch.uint8, device=dev)
+    _keep(stream, targets, logit_lens, target_lens, losses, grads, grad_scale, workspace)
     args = [_ptr(logits), _ptr(targets), _ptr(logit_lens), _ptr(target_lens), B, Tmax, Umax, V, int(blank),
             _ptr(losses), _ptr(grads), _ptr(grad_scale), _ptr(workspace), workspace.numel(), _stream(stream)]
     ev = None
@@ -197,6 +240,7 @@ def rnnt_viterbi(logits, targets, logit_lens, target_lens, blank=0, variant="rnn
     if workspace is None:
         workspace = torch.empty(max(rnnt_workspace_bytes(B, Tmax, Umax), 1), dtype=torch.uint8, device=dev)
     logits = logits.contiguous()  # a named reference keeps any copy alive across the call
+    _keep(stream, logits, targets, logit_lens, target_lens, best, frames, span, workspace)
     _check(library.rnnt_viterbi(_ptr(logits), DTYPES[logits.dtype], _ptr(targets), _ptr(logit_lens),
                                 _ptr(target_lens), B, Tmax, Umax, V, int(blank), VARIANTS[variant], _ptr(best),
                                 _ptr(frames) if Umax > 0 else None, _ptr(span), _ptr(workspace), workspace.numel(),
@@ -210,15 +254,7 @@ def rnnt_joint_loss(enc, pred, weight, bias, targets, logit_lens, target_lens, b
     is reduced on chip (tcgen05 GEMM + log-softmax / Populate epilogue) and never materialised; returns the
     per-utterance losses [B].  enc [B, Tmax, H], pred [B, Umax+1, H], weight [V, H]: CUDA bfloat16; bias [V]
     float32 or None.  events: None or 4 recorded torch.cuda.Events (K6 start / end, K2 start / end)."""
-    for name, x in (("enc", enc), ("pred", pred), ("weight", weight)):
-        if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.bfloat16 and x.is_contiguous()):
-            raise TypeError(f"{name} must be a contiguous CUDA bfloat16 tensor (no CPU fallback)")
-    B, Tmax, H = enc.shape
-    Up1 = pred.shape[1]
-    Umax = Up1 - 1
-    V = weight.shape[0]
-    if pred.shape != (B, Up1, H) or weight.shape != (V, H):
-        raise ValueError("shapes: enc [B, Tmax, H], pred [B, Umax+1, H], weight [V, H]")
+    B, Tmax, Umax, H, V = _check_joint_inputs(enc, pred, weight)
     dev = enc.device
     if bias is not None:
         bias = bias.to(device=dev, dtype=torch.float32).contiguous()
@@ -235,6 +271,7 @@ def rnnt_joint_loss(enc, pred, weight, bias, targets, logit_lens, target_lens, b
         if len(handles) != 4 or not all(handles):
             raise ValueError("need 4 recorded torch.cuda.Events")
         ev = ctypes.cast((ctypes.c_void_p * 4)(*handles), ctypes.c_void_p)
+    _keep(stream, bias, targets, logit_lens, target_lens, losses, workspace)
     _check(library.rnnt_joint_loss_ex(_ptr(enc), _ptr(pred), _ptr(weight), _ptr(bias), _ptr(targets),
                                       _ptr(logit_lens), _ptr(target_lens), B, Tmax, Umax, H, V, int(blank),
                                       VARIANTS[variant], _ptr(losses), _ptr(workspace), workspace.numel(),
@@ -251,12 +288,7 @@ def rnnt_joint_loss_grad(enc, pred, weight, bias, targets, logit_lens, target_le
     [B] per-utterance weights (gradients of sum_b grad_scale[b] * losses[b]; 1/B gives the mean).
     valid_rows: the valid-cell count sum_b T_b (U_b + 1) (the GEMMs then skip the padding; a wrong count gives
     NaN losses); None computes it when both length arrays are on the host, else passes -1 (unknown)."""
-    for name, x in (("enc", enc), ("pred", pred), ("weight", weight)):
-        if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.bfloat16 and x.is_contiguous()):
-            raise TypeError(f"{name} must be a contiguous CUDA bfloat16 tensor (no CPU fallback)")
-    B, Tmax, H = enc.shape
-    Umax = pred.shape[1] - 1
-    V = weight.shape[0]
+    B, Tmax, Umax, H, V = _check_joint_inputs(enc, pred, weight)
     dev = enc.device
     if bias is not None:
         bias = bias.to(device=dev, dtype=torch.float32).contiguous()
@@ -271,12 +303,18 @@ def rnnt_joint_loss_grad(enc, pred, weight, bias, targets, logit_lens, target_le
                    torch.empty((B, Umax + 1, H), dtype=torch.float32, device=dev),
                    torch.empty((V, H), dtype=torch.float32, device=dev),
                    torch.empty(V, dtype=torch.float32, device=dev))
+    if len(outputs) != 5:
+        raise ValueError("outputs: (losses, d_enc, d_pred, d_weight, d_bias)")
     losses, d_enc, d_pred, d_weight, d_bias = outputs
+    for name, t, shape in (("losses", losses, (B,)), ("d_enc", d_enc, (B, Tmax, H)),
+                           ("d_pred", d_pred, (B, Umax + 1, H)), ("d_weight", d_weight, (V, H)),
+                           ("d_bias", d_bias, (V,))):
+        _check_f32_out(name, t, shape, dev)
+    need = int(library.rnnt_joint_grad_workspace_bytes(B, Tmax, Umax, H, V))
     if workspace is None:
-        need = int(library.rnnt_joint_grad_workspace_bytes(B, Tmax, Umax, H, V))
         workspace = torch.empty(max(need, 1), dtype=torch.uint8, device=dev)
-    if grad_scale is not None:
-        grad_scale = grad_scale.to(device=dev, dtype=torch.float32).contiguous()
+    grad_scale = _check_grad_scale(grad_scale, B, dev)
+    _keep(stream, bias, targets, logit_lens, target_lens, grad_scale, workspace, *outputs)
     _check(library.rnnt_joint_loss_grad(_ptr(enc), _ptr(pred), _ptr(weight), _ptr(bias), _ptr(targets),
                                         _ptr(logit_lens), _ptr(target_lens), B, Tmax, Umax, H, V, int(blank),
                                         VARIANTS[variant], _ptr(losses), _ptr(d_enc), _ptr(d_pred), _ptr(d_weight),
@@ -300,12 +338,7 @@ def rnnt_joint_viterbi(enc, pred, weight, bias, targets, logit_lens, target_lens
                        workspace=None, stream=None):
     """Viterbi forced alignment on the fused joint's logits (K6 + K4; the logits are never written).  Inputs as
     rnnt_joint_loss; returns (best_logp fp32 [B], frames int32 [B, Umax], span int32 [B, 2]) as rnnt_viterbi."""
-    for name, x in (("enc", enc), ("pred", pred), ("weight", weight)):
-        if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.bfloat16 and x.is_contiguous()):
-            raise TypeError(f"{name} must be a contiguous CUDA bfloat16 tensor (no CPU fallback)")
-    B, Tmax, H = enc.shape
-    Umax = pred.shape[1] - 1
-    V = weight.shape[0]
+    B, Tmax, Umax, H, V = _check_joint_inputs(enc, pred, weight)
     dev = enc.device
     if bias is not None:
         bias = bias.to(device=dev, dtype=torch.float32).contiguous()
@@ -317,6 +350,7 @@ def rnnt_joint_viterbi(enc, pred, weight, bias, targets, logit_lens, target_lens
     span = torch.empty((B, 2), dtype=torch.int32, device=dev)
     if workspace is None:
         workspace = torch.empty(max(rnnt_workspace_bytes(B, Tmax, Umax), 1), dtype=torch.uint8, device=dev)
+    _keep(stream, bias, targets, logit_lens, target_lens, best, frames, span, workspace)
     _check(library.rnnt_joint_viterbi(_ptr(enc), _ptr(pred), _ptr(weight), _ptr(bias), _ptr(targets),
                                       _ptr(logit_lens), _ptr(target_lens), B, Tmax, Umax, H, V, int(blank),
                                       VARIANTS[variant], _ptr(best), _ptr(frames) if Umax > 0 else None, _ptr(span),
@@ -345,6 +379,7 @@ def rnnt_lattice_loss(logits, lattices, logit_lens, target_lens, grads=True, los
     ws = torch.empty(max(need, 1), dtype=torch.uint8, device=dev)
     logit_lens = _as_i32(logit_lens, dev)    # keep the device copies alive across the call
     target_lens = _as_i32(target_lens, dev)
+    _keep(stream, logit_lens, target_lens, losses, grads, ws, *[v for v in dv.values() if isinstance(v, torch.Tensor)])
     _check(library.rnnt_lattice_loss(
         _ptr(logits), _ptr(logit_lens), _ptr(target_lens), B, Tmax, Up1 - 1, V,
         *[_ptr(dv[k]) for k in ("state_off", "lvl_off", "level_off", "in_off", "out_off", "out_arc", "arc_src",
@@ -382,13 +417,31 @@ def rnnt_loss_host(logits_host, targets_host, logit_lens_host, target_lens_host,
 
     Returns (losses_host, grads_host).  Synchronize the stream before reading them.
     """
+    def host(name, t, dtype, shape):
+        if not (isinstance(t, torch.Tensor) and not t.is_cuda and t.dtype == dtype and t.is_contiguous()
+                and tuple(t.shape) == tuple(shape)):
+            raise TypeError(f"{name} must be a contiguous CPU {dtype} tensor of shape {tuple(shape)} "
+                            f"(got {getattr(t, 'dtype', type(t))} {tuple(getattr(t, 'shape', ()))})")
+        return t
+
+    if not (isinstance(logits_host, torch.Tensor) and logits_host.dim() == 4):
+        raise TypeError("logits_host must be a CPU float32 tensor [B, Tmax, Umax+1, V]")
     B, Tmax, Up1, V = logits_host.shape
     Umax = Up1 - 1
+    host("logits_host", logits_host, torch.float32, (B, Tmax, Up1, V))
+    host("logit_lens_host", logit_lens_host, torch.int32, (B,))
+    host("target_lens_host", target_lens_host, torch.int32, (B,))
+    if Umax > 0:
+        host("targets_host", targets_host, torch.int32, (B, Umax))
     if losses_host is None:
         losses_host = torch.empty(B, dtype=torch.float32, pin_memory=True)
+    host("losses_host", losses_host, torch.float32, (B,))
+    if grads_host is not None:
+        host("grads_host", grads_host, torch.float32, (B, Tmax, Up1, V))
     need = rnnt_host_buffer_bytes(B, Tmax, Umax, V)
     if device_buffer is None:
         device_buffer = torch.empty(need, dtype=torch.uint8, device="cuda")
+    _keep(stream, device_buffer)
     tg = targets_host if Umax > 0 else None
     _check(library.rnnt_loss_host(_ptr(logits_host), _ptr(tg), _ptr(logit_lens_host), _ptr(target_lens_host),
                                   B, Tmax, Umax, V, int(blank), VARIANTS[variant], _ptr(losses_host),

@@ -729,7 +729,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
                 // once all builders have written the tile; it overlaps the TMEM copy and the next build.
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 asm volatile("bar.sync 4, 256;" ::: "memory");
-                {
+                if (warp < 16) {  // builder warps 12-15 only: warps 16-19 would issue no copy
                     const int64_t nv = std::min<int64_t>(kRowsPerTile, rows - tile * kRowsPerTile);
                     const int r = (warp - 12) * 32 + lane;
                     if (r < nv) {
@@ -787,7 +787,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
         if (warp == 8) o[7] = w_accfull;
         if (warp == 12) o[6] = w_aempty;
     }
-    if (kGrad && warp >= 12)  // the last h stores complete before the CTA's shared memory is released
+    if (kGrad && warp >= 12 && warp < 16)  // the last h stores complete before the CTA's shared memory is released
         asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     tc_fence_before();
     if constexpr (kCl > 1)

@@ -34,6 +34,14 @@ def init(backend: str = "nccl"):
     return rank, world, local
 
 
+def device_index(local_rank: int, backend: str = "nccl") -> int:
+    """CUDA device of a rank: its local rank (one process per GPU).  Under gloo several ranks may share a GPU
+    (harness tests on a one-GPU box): local rank modulo the visible device count."""
+    if backend == "nccl":
+        return local_rank
+    return local_rank % max(1, torch.cuda.device_count())
+
+
 def contiguous_shard(n_global: int, rank: int, world: int):
     """Global utterance ids of ``rank``: a contiguous block; block sizes differ by at most one."""
     base, extra = divmod(n_global, world)
@@ -61,6 +69,15 @@ def allreduce_loss_sum(loss_sum: torch.Tensor, group=None) -> torch.Tensor:
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(loss_sum, op=dist.ReduceOp.SUM, group=group)
     return loss_sum
+
+
+def sum_over_ranks(value: float, device) -> float:
+    """Sum of a host scalar over ranks (the units all ranks processed)."""
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return value
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
 
 
 def max_over_ranks(value: float, device) -> float:

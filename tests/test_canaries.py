@@ -136,6 +136,8 @@ def test_canaries_fused_joint_forward_and_training_step(rb):
         assert g.intact()
     ref = oj.joint_loss_and_grads(enc.double().numpy(), pred.double().numpy(), W.double().numpy(),
                                   bias.double().numpy(), y, T_b, U_b, 0, "force_final")
+    bnd = oj.r23_bounds(enc.double().numpy(), pred.double().numpy(), W.double().numpy(), bias.double().numpy(),
+                        y, T_b, U_b, 0, "force_final")
     assert np.allclose(l.cpu().numpy(), ref[0], rtol=1e-5) and np.allclose(out[0].cpu().numpy(), ref[0], rtol=1e-5)
-    for mine, r in zip(out[1:], ref[1:]):
-        assert np.abs(mine.cpu().numpy().astype(np.float64) - r).max() <= 2e-3 * np.abs(r).max()
+    for mine, r, k in zip(out[1:], ref[1:], ("d_f", "d_g", "d_W", "d_bias")):
+        assert (np.abs(mine.cpu().numpy().astype(np.float64) - r) <= bnd[k]).all(), k
