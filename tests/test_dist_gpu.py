@@ -84,9 +84,10 @@ torch.cuda.set_device(0)
 dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
 cfg = workloads.random_config(3, 40, 9, 130, seed=5)
 pb = workloads.problem(cfg, device="cuda")
+y, T, U = (torch.as_tensor(pb[k]).to("cuda", torch.int32) for k in ("targets", "logit_lens", "target_lens"))
 losses = torch.empty(3, device="cuda"); s = torch.empty((), dtype=torch.float64, device="cuda")
 def step():
-    rb.rnnt_loss(pb["logits"], pb["targets"], pb["logit_lens"], pb["target_lens"], cfg.blank, losses=losses)
+    rb.rnnt_loss(pb["logits"], y, T, U, cfg.blank, losses=losses)
     rb.rnnt_loss_sum(losses, out=s)
     dist.all_reduce(s)      # world 1: still an NCCL kernel, captured like bench.py's at N > 1
 step(); torch.cuda.synchronize()
