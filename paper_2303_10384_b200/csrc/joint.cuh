@@ -32,6 +32,15 @@ rnnt_status joint_front(const void* enc, const void* pred, const void* weight, c
                         cudaStream_t s, void* const* events, int* rowmap = nullptr, int* nrows = nullptr,
                         bool make_map = true, const GradIO* g = nullptr);
 
+// K8 / K9 (k8_joint_bwd.cu): the backward GEMMs on the tensor cores.  K8: dpre = bf16((dz W) * (1 - h^2)) over R
+// rows; K9: d_weight = dz^T h, d_bias = column sums of dz (d_bias may be nullptr), through `part`
+// (k9_partial_bytes).  dz [R][Vp], h [R][Hg] (row pitch Hg), W [V][H], dpre [R][H]; H % 128 == 0, H <= 512.
+size_t k9_partial_bytes(int Vp, int H);
+cudaError_t launch_k8(const __nv_bfloat16* dz, const __nv_bfloat16* weight, const __nv_bfloat16* h,
+                      __nv_bfloat16* dpre, int R, int H, int Hg, int V, int Vp, cudaStream_t s);
+cudaError_t launch_k9(const __nv_bfloat16* dz, const __nv_bfloat16* h, int R, int H, int Hg, int V, int Vp,
+                      float* part, float* d_weight, float* d_bias, cudaStream_t s);
+
 constexpr int kJointVTile = 128;  // K6's N tile: dz rows are padded to a multiple of it
 constexpr int kJointHPad = 8;     // h rows carry 8 extra bf16 columns: (1, 0, ..., 0), for dbias in the dW GEMM
 // h's global row stride, H + 64 bf16: 128-byte aligned rows (the staging tile's H + 8 rows, stored as they are,

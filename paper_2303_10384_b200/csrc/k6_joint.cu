@@ -34,6 +34,7 @@
 #include "elem.cuh"
 #include "joint.cuh"
 #include "rnnt_b200.h"
+#include "tc.cuh"
 
 namespace rnnt {
 namespace {
@@ -48,84 +49,6 @@ constexpr int kMaxStages = 16;
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kAccCol0 = 256;
 
-// ---- PTX wrappers -------------------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "W%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra W%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-// mbar_wait that adds the cycles spent to *acc (diagnostics, RNNT_K6_DEBUG & 4)
-__device__ __forceinline__ void mbar_wait_t(uint64_t* bar, uint32_t parity, bool on, unsigned long long& acc) {
-    const long long t0 = on ? clock64() : 0;
-    mbar_wait(bar, parity);
-    if (on) acc += clock64() - t0;
-}
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
-        "[%4];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
-        : "memory");
-}
-// Cluster-multicast variant: the tile lands at the same shared-memory offset of every CTA in cta_mask, each
-// of whose mbarrier at `bar`'s offset receives the complete_tx.
-__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
-                                               uint16_t cta_mask) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster "
-        "[%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "h"(cta_mask)
-        : "memory");
-}
-__device__ __forceinline__ void cluster_sync_all() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ uint32_t cluster_rank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-// commit to the mbarrier at `bar`'s offset in every CTA of cta_mask (one elected lane of a converged warp)
-__device__ __forceinline__ void tc_commit_mc(uint64_t* bar, uint16_t cta_mask) {
-    asm volatile(
-        "{\n"
-        ".reg .pred e;\n"
-        "elect.sync _|e, 0xffffffff;\n"
-        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "h"(cta_mask)
-        : "memory");
-}
-__device__ __forceinline__ void tc_commit(uint64_t* bar) {  // by one elected lane of a converged warp
-    asm volatile(
-        "{\n"
-        ".reg .pred e;\n"
-        "elect.sync _|e, 0xffffffff;\n"
-        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
-        "}\n" ::"r"(smem_u32(bar))
-        : "memory");
-}
 // One K block (64 = 4 x K16) of D[tmem] (+)= A[tmem] . B[smem]^T, M = 128, N = kNTile, bf16 in, fp32
 // accumulate: the four MMAs in one asm block so that the operands reach the uniform datapath once (per-MMA
 // asm statements cost ~15 issue slots each in ELECT / R2UR conversions, as much as the MMA itself takes).
@@ -158,33 +81,6 @@ __device__ __forceinline__ void mma_kblock(uint32_t d_tmem, uint32_t a_tmem, uin
 // Instruction descriptor: fp32 D (bits 4-5 = 1), bf16 A (7-9 = 1) and B (10-12 = 1), both K-major,
 // N >> 3 at bits 17-22, M >> 4 at bits 24-28.
 constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(kNTile >> 3) << 17) | (uint32_t(128 >> 4) << 24);
-// Shared-memory matrix descriptor of a K-major SWIZZLE_128B tile (rows of 128 B, 8-row atoms of 1024 B):
-// start >> 4, LBO 16 B (unused for swizzled K-major), SBO 1024 B, version 1, layout SWIZZLE_128B (2).
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
-    return static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4) | (static_cast<uint64_t>(1) << 16) |
-           (static_cast<uint64_t>(1024 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) | (static_cast<uint64_t>(2) << 61);
-}
-
-#define TMEM_LD32(taddr, r)                                                                                     \
-    asm volatile(                                                                                               \
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18," \
-        "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                                         \
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),       \
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), \
-          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]),            \
-          "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),            \
-          "=r"(r[30]), "=r"(r[31])                                                                              \
-        : "r"(taddr))
-#define TMEM_ST32(taddr, r)                                                                                     \
-    asm volatile(                                                                                               \
-        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17," \
-        "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),                          \
-        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),      \
-        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),         \
-        "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),        \
-        "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])                     \
-        : "memory")
-
 __device__ __forceinline__ float rcp_approx(float x) {
     float y;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -215,14 +111,6 @@ __device__ __forceinline__ float select32(const float (&z)[32], int k) {
     for (int i = 0; i < 2; ++i) s[i] = (k & 8) ? s[2 * i + 1] : s[2 * i];
     return (k & 16) ? s[1] : s[0];
 }
-__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
-    const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
-    return *reinterpret_cast<const uint32_t*>(&v);
-}
-__device__ __forceinline__ float2 unpack_bf16x2(uint32_t w) {
-    return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
-}
-
 struct JointArgs {
     const __nv_bfloat16* f;
     const __nv_bfloat16* g;
