@@ -10,8 +10,7 @@
 namespace rnnt {
 
 // Backward-pass inputs / outputs of K6<true>: the forward's lse / lp and K2's alpha / beta / logP in; dz
-// ([rows][Vp] bf16, Vp = V rounded up to 128) and h ([rows][H + kJointHPad] bf16) out, rows = the compact
-// valid cells.
+// ([rows][Vp] bf16, Vp = V rounded up to 128) and h ([rows][H] bf16) out, rows = the compact valid cells.
 struct GradIO {
     const float* lse;
     const double2* lp;
@@ -32,20 +31,20 @@ rnnt_status joint_front(const void* enc, const void* pred, const void* weight, c
                         cudaStream_t s, void* const* events, int* rowmap = nullptr, int* nrows = nullptr,
                         bool make_map = true, const GradIO* g = nullptr);
 
-// K8 / K9 (k8_joint_bwd.cu): the backward GEMMs on the tensor cores.  K8: dpre = bf16((dz W) * (1 - h^2)) over R
-// rows; K9: d_weight = dz^T h, d_bias = column sums of dz (d_bias may be nullptr), through `part`
-// (k9_partial_bytes).  dz [R][Vp], h [R][Hg] (row pitch Hg), W [V][H], dpre [R][H]; H % 128 == 0, H <= 512.
+// K8 / K9 (k8_joint_bwd.cu): the backward GEMMs on the tensor cores.  K8: out = bf16(dz W) over R rows, or with
+// tanh_in_k8 bf16((dz W) * (1 - h^2)) (the pair kernel; the 2-D cluster A/B kernel always applies it); K9:
+// d_weight = dz^T h, d_bias = column sums of dz (d_bias may be nullptr), through `part` (k9_partial_bytes).
+// dz [R][Vp], h [R][Hg] (row pitch Hg), W [V][H], out [R][H]; H % 128 == 0, H <= 512.
 size_t k9_partial_bytes(int Vp, int H);
 cudaError_t launch_k8(const __nv_bfloat16* dz, const __nv_bfloat16* weight, const __nv_bfloat16* h,
-                      __nv_bfloat16* dpre, int R, int H, int Hg, int V, int Vp, cudaStream_t s);
+                      __nv_bfloat16* out, int R, int H, int Hg, int V, int Vp, bool tanh_in_k8, cudaStream_t s);
 cudaError_t launch_k9(const __nv_bfloat16* dz, const __nv_bfloat16* h, int R, int H, int Hg, int V, int Vp,
                       float* part, float* d_weight, float* d_bias, cudaStream_t s);
 
 constexpr int kJointVTile = 128;  // K6's N tile: dz rows are padded to a multiple of it
-constexpr int kJointHPad = 8;     // h rows carry 8 extra bf16 columns: (1, 0, ..., 0), for dbias in the dW GEMM
-// h's global row stride, H + 64 bf16: 128-byte aligned rows (the staging tile's H + 8 rows, stored as they are,
-// start at a different 16-byte offset mod 128 each and cost K7 +21 % DRAM reads, profiles/r01_v17_k7_ncu_full.txt);
-// the dW GEMM reads columns [0, H + kJointHPad) of it (lda = H + kJointHGPad).
-constexpr int kJointHGPad = 64;
+constexpr int kJointHPad = 8;     // K6's A staging rows: H + 8 bf16 (16 bytes of pad: conflict-free row reads)
+// h's global row stride beyond H: none (rows of H bf16 = 256 .. 1024 bytes, 128-byte aligned); round 1 carried a
+// (1, 0, .., 0) column for a library dbias GEMM and a 128-byte aligned stride H + 64 for K7.
+constexpr int kJointHGPad = 0;
 
 }  // namespace rnnt

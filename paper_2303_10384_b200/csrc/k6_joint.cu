@@ -137,7 +137,7 @@ struct JointArgs {
     const double* logp;
     const float* grad_scale;
     __nv_bfloat16* dz_out;  // [rows][Vp] row-major, Vp = V rounded up to whole N tiles (tail columns 0)
-    __nv_bfloat16* h_out;   // [rows][H + kJointHGPad]: h, then (1, 0, ..., 0), then unused
+    __nv_bfloat16* h_out;   // [rows][H]
 };
 
 // kGrad = false: the forward (lse + gathers).  kGrad = true: the backward's first pass -- the same GEMM
@@ -173,7 +173,8 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
     uint8_t* wst = base;
     uint8_t* stage_a = wst + static_cast<size_t>(a.stages) * kStageBytes;
     const int Vp = (a.V + kNTile - 1) / kNTile * kNTile;  // V rounded up to whole N tiles
-    // A staging: 128 rows of H + kJointHPad bf16 (the pad holds (1, 0, .., 0): row = h's global row, see kGrad)
+    // A staging: 128 rows of H + kJointHPad bf16 (the 16-byte pad: conflict-free thread-per-row reads; kGrad: the
+    // rows' first H columns are h's global rows)
     float* sbias = reinterpret_cast<float*>(stage_a + static_cast<size_t>(kRowsPerTile) * (a.H + kJointHPad) * 2);
     float4* xchg = reinterpret_cast<float4*>(sbias + (kSB ? Vp : 0));  // [2][128] epilogue group 1 -> 0 partials
     uint64_t* bars = reinterpret_cast<uint64_t*>(xchg + 2 * kRowsPerTile);
@@ -191,11 +192,6 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
     const int H = a.H, V = a.V;
     if (kSB)  // read by the epilogue only, after the __syncthreads of the setup below
         for (int i = threadIdx.x; i < Vp; i += blockDim.x) sbias[i] = i < V ? (a.bias ? a.bias[i] : 0.f) : -INFINITY;
-    if (kGrad)  // staging rows' pad = h's extra column (1, 0, .., 0): the dW GEMM's extra output is dbias
-        for (int i = threadIdx.x; i < kRowsPerTile; i += blockDim.x)
-            *reinterpret_cast<uint4*>(stage_a + static_cast<size_t>(i) * (H + kJointHPad) * 2 + H * 2) =
-                make_uint4(0x3f80u, 0u, 0u, 0u);
-    if (kGrad) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // read by the bulk copies
     const int KB = H / kKBlock, NT = Vp / kNTile;
     const int64_t rows = *a.nrows;  // valid cells only: padding costs no GEMM work
     const int64_t ntiles = (rows + kRowsPerTile - 1) / kRowsPerTile;
@@ -610,9 +606,9 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
             }
             __syncwarp();  // each thread copies its own row, written by the whole warp
             if constexpr (kGrad) {
-                // h for the dW GEMM: the staging rows ARE h's rows (H + 8 columns, the pad = (1, 0, ..)) and the
-                // tile's rows are consecutive compact rows; stored at the 128-byte aligned global stride
-                // H + kJointHGPad by one bulk async copy (TMA engine) per row, spread over the builder warps
+                // h for K9 and K7: the staging rows' first H columns ARE h's rows and the tile's rows are
+                // consecutive compact rows; stored at the global stride H by one bulk async copy (TMA engine) per row,
+                // spread over the builder warps
                 // 12-15 (lane l of warp 12 + j takes row 32 j + l: one copy per thread, the issue cost shared)
                 // once all builders have written the tile; it overlaps the TMEM copy and the next build.
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -621,10 +617,10 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
                     const int64_t nv = std::min<int64_t>(kRowsPerTile, rows - tile * kRowsPerTile);
                     const int r = (warp - 12) * 32 + lane;
                     if (r < nv) {
-                        __nv_bfloat16* dst = a.h_out + (tile * kRowsPerTile + r) * (H + kJointHGPad);
+                        __nv_bfloat16* dst = a.h_out + (tile * kRowsPerTile + r) * H;
                         asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
                                      "r"(smem_u32(stage_a) + static_cast<uint32_t>(r * row_bytes)),
-                                     "r"(static_cast<uint32_t>(row_bytes))
+                                     "r"(static_cast<uint32_t>(H * 2))
                                      : "memory");
                     }
                     asm volatile("cp.async.bulk.commit_group;" ::: "memory");

@@ -4,18 +4,20 @@
 //   dz(t,u,v)  = softmax(z)(v) (occ_b + occ_y) - [v = blank] occ_b - [v = y_u] occ_y      (K3's formula)
 //   dh(t,u,:)  = sum_v dz(t,u,v) W(v,:)                  dW(v,:) = sum_{t,u} dz(t,u,v) h(t,u,:)
 //   dbias(v)   = sum_{t,u} dz(t,u,v)
-//   dpre       = dh * (1 - h^2)   (dh in fp32 from TMEM, tanh' from the stored bf16 h; dpre stored in bf16)
+//   dpre       = dh * (1 - h^2)   (dh accumulated in fp32 in TMEM, stored in bf16; tanh' from the stored bf16 h)
 //   d enc(b,t,:) = sum_{u <= U_b} dpre(t,u,:)           d pred(b,u,:) = sum_{t < T_b} dpre(t,u,:)
 // over the valid cells.  Pipeline (all on the caller's stream, every kernel this library's own):
 //   K6 (forward: lse, gathers) -> K2 (alpha, beta, losses) -> K6<grad> (recomputes z on the tensor cores;
-//   its epilogue writes dz in bf16, its builders write h) -> K8 (dh = dz W on the tensor cores, tanh' in its
-//   epilogue -> dpre) and K9 (dW = dz^T h and dbias on the tensor cores, split over row ranges, k9_reduce)
-//   (k8_joint_bwd.cu) -> K7 (the two reductions of dpre).  The [B,T,U+1,V] logits never exist; dz does, in
+//   its epilogue writes dz in bf16, its builders write h) -> K8 (dh = dz W, CTA-pair tcgen05 GEMM) and K9
+//   (dW = dz^T h and dbias, CTA-pair tcgen05 GEMM split over row ranges, k9_reduce) (k8_joint_bwd.cu) -> K7
+//   (tanh' and the two reductions, one streaming pass over dh and h).  The [B,T,U+1,V] logits never exist; dz
+//   does, in
 //   bf16 (half the bytes of fp32 logits), because dW needs it against every row and dh against every v, and a
 //   128-row tile's fp32 dh (128 x H) alone fills TMEM at H = 512.  Rows are the compact valid
 //   cells (K6's row map); with the caller's valid-row count the GEMMs cover exactly those, else the padded row
 //   count B*Tmax*(Umax+1) with the tail rows zeroed.
 #include <algorithm>
+#include <cstdlib>
 
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -24,6 +26,7 @@
 #include "elem.cuh"
 #include "joint.cuh"
 #include "rnnt_b200.h"
+#include "tc.cuh"
 
 namespace rnnt {
 namespace {
@@ -69,21 +72,24 @@ __device__ int utt_offset(const int32_t* T_b, const int32_t* U_b, int b, int Tma
     return off;
 }
 
-// K7, pass 1: block (chunk, b, slice) takes frames [chunk * kTC, +kTC) of utterance b and a 128-column slice
-// of H, and reads each of its rows of dpre (K8's output, tanh' already applied) ONCE.  Warp w owns units u = w (mod 4):
-// its sum over the chunk's frames is the chunk's partial of d pred(b, u) (-> part, registers); its
-// contribution to d enc(b, t) is added to a per-warp shared-memory partial, summed over the four warps in a
-// fixed order at the end (the block owns every unit of its frames: d enc is complete, written directly).
-// Pass 2 sums the chunk partials of d pred in chunk order.  Deterministic; 128 threads x 4 columns.
-// (Round 1 read dh and h here and applied tanh'; K8's epilogue now does that, halving K7's bytes.)
+// K7, pass 1: block (chunk, b, slice) takes frames [chunk * kTC, +kTC) of utterance b and a 256-column slice of
+// H, and streams each of its rows of dh (K8's output) and h ONCE: dpre = dh * (1 - h^2) (kPre: the input already
+// is dpre, K8 applied tanh'; h is not read).  256 threads = 8 warps; lane = 8 columns, so a warp reads a whole
+// 512-byte row segment per 16-byte load; warp w owns units u = w (mod 8) and loads its kTC frames of a unit at
+// once.  Its sum over the chunk's frames is the chunk's partial of d pred(b, u) (-> part); its contribution to
+// d enc(b, t) stays in registers and the 8 warps' partials are added in a fixed tree order through shared
+// memory (the block owns every unit of its frames: d enc is complete, written directly).  Pass 2 sums the
+// chunk partials of d pred in chunk order.  Deterministic.
 constexpr int kTC = 8;
 
-__global__ void __launch_bounds__(128) k7_reduce(const __nv_bfloat16* __restrict__ dpre,
-                                                 const int32_t* __restrict__ T_b, const int32_t* __restrict__ U_b,
-                                                 int B, int Tmax, int Umax, int H, float* __restrict__ d_enc,
-                                                 float* __restrict__ part) {
-    __shared__ int s_part[4];
-    __shared__ float4 s_enc[4][kTC][32];
+template <bool kPre>
+__global__ void __launch_bounds__(256, 1) k7_reduce(const __nv_bfloat16* __restrict__ dx,
+                                                    const __nv_bfloat16* __restrict__ h,
+                                                    const int32_t* __restrict__ T_b, const int32_t* __restrict__ U_b,
+                                                    int B, int Tmax, int Umax, int H, float* __restrict__ d_enc,
+                                                    float* __restrict__ part) {
+    __shared__ int s_part[8];
+    __shared__ float4 s_enc[4][kTC][2][32];  // tree-combine slots: [slot][frame][half of the 8 columns][lane]
     const int chunk = blockIdx.x, b = blockIdx.y;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int off = utt_offset(T_b, U_b, b, Tmax, Umax, s_part);
@@ -91,66 +97,77 @@ __global__ void __launch_bounds__(128) k7_reduce(const __nv_bfloat16* __restrict
     const int T = n ? T_b[b] : 0, U = n ? U_b[b] : -1;
     const int t0 = chunk * kTC;
     const int tn = max(0, min(T - t0, kTC));
-    const int c = blockIdx.z * 128 + lane * 4;
-    float4 enc[kTC];  // this warp's partial of d enc(b, t0 + k) over its units (registers; shared at the end)
+    const int c = blockIdx.z * 256 + lane * 8;
+    const bool col_in = c < H;
+    float enc[kTC][8];
 #pragma unroll
-    for (int k = 0; k < kTC; ++k) enc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int u = warp; u <= U && tn > 0; u += 4) {
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k = 0; k < kTC; ++k)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) enc[k][e] = 0.f;
+    for (int u = warp; u <= U && tn > 0 && col_in; u += 8) {
+        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         const int64_t r0 = off + static_cast<int64_t>(t0) * (U + 1) + u;
-        auto row = [&](int k, uint2 dw) {
-            float4 d;
-            d.x = __uint_as_float(dw.x << 16);
-            d.y = __uint_as_float(dw.x & 0xffff0000u);
-            d.z = __uint_as_float(dw.y << 16);
-            d.w = __uint_as_float(dw.y & 0xffff0000u);
-            acc.x += d.x;
-            acc.y += d.y;
-            acc.z += d.z;
-            acc.w += d.w;
-            float4& e = enc[k];
-            e.x += d.x;
-            e.y += d.y;
-            e.z += d.z;
-            e.w += d.w;
-        };
-        auto ld = [&](int k, uint2& dw) {
-            const int64_t r = r0 + static_cast<int64_t>(k) * (U + 1);
-            dw = __ldcs(reinterpret_cast<const uint2*>(dpre + r * H + c));
-        };
-        if (tn == kTC) {  // whole chunk: all kTC rows' loads issued before any use
-            uint2 dw[kTC];
+        uint4 dv[kTC], hv[kTC];
 #pragma unroll
-            for (int k = 0; k < kTC; ++k) ld(k, dw[k]);
+        for (int k = 0; k < kTC; ++k)  // all the unit's rows in flight before any use
+            if (k < tn) {
+                const int64_t r = r0 + static_cast<int64_t>(k) * (U + 1);
+                dv[k] = __ldcs(reinterpret_cast<const uint4*>(dx + r * H + c));
+                if (!kPre) hv[k] = __ldcs(reinterpret_cast<const uint4*>(h + r * H + c));
+            }
 #pragma unroll
-            for (int k = 0; k < kTC; ++k) row(k, dw[k]);
-        } else {
+        for (int k = 0; k < kTC; ++k)
+            if (k < tn) {
+                const uint32_t dw[4] = {dv[k].x, dv[k].y, dv[k].z, dv[k].w};
+                uint32_t hw[4] = {0u, 0u, 0u, 0u};
+                if (!kPre) hw[0] = hv[k].x, hw[1] = hv[k].y, hw[2] = hv[k].z, hw[3] = hv[k].w;
 #pragma unroll
-            for (int k = 0; k < kTC; ++k)  // unrolled so enc[] stays in registers
-                if (k < tn) {
-                    uint2 dw;
-                    ld(k, dw);
-                    row(k, dw);
+                for (int j = 0; j < 4; ++j) {
+                    float2 d = unpack_bf16x2(dw[j]);
+                    if (!kPre) {
+                        const float2 hh = unpack_bf16x2(hw[j]);
+                        d = upk(fmul2(pk(d.x, d.y), ffma2(pk(-hh.x, -hh.y), pk(hh.x, hh.y), pk(1.f, 1.f))));
+                    }
+                    acc[2 * j] += d.x;
+                    acc[2 * j + 1] += d.y;
+                    enc[k][2 * j] += d.x;
+                    enc[k][2 * j + 1] += d.y;
                 }
-        }
-        *reinterpret_cast<float4*>(part + ((static_cast<int64_t>(chunk) * B + b) * (Umax + 1) + u) * H + c) = acc;
+            }
+        float4* pp = reinterpret_cast<float4*>(part + ((static_cast<int64_t>(chunk) * B + b) * (Umax + 1) + u) * H + c);
+        pp[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        pp[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
     }
+    // tree combine of the 8 warps' d enc partials: (w, w + 4), then (w, w + 2), then (0, 1)
 #pragma unroll
-    for (int k = 0; k < kTC; ++k) s_enc[warp][k][lane] = enc[k];
-    __syncthreads();
-    for (int k = warp; k < kTC && t0 + k < Tmax; k += 4) {
-        float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (k < tn) {
+    for (int step = 4; step >= 1; step >>= 1) {
+        if (warp >= step && warp < 2 * step) {
 #pragma unroll
-            for (int w = 0; w < 4; ++w) {
-                const float4 e = s_enc[w][k][lane];
-                o.x += e.x;
-                o.y += e.y;
-                o.z += e.z;
-                o.w += e.w;
+            for (int k = 0; k < kTC; ++k) {
+                s_enc[warp - step][k][0][lane] = make_float4(enc[k][0], enc[k][1], enc[k][2], enc[k][3]);
+                s_enc[warp - step][k][1][lane] = make_float4(enc[k][4], enc[k][5], enc[k][6], enc[k][7]);
             }
         }
-        *reinterpret_cast<float4*>(d_enc + (static_cast<int64_t>(b) * Tmax + t0 + k) * H + c) = o;
+        __syncthreads();
+        if (warp < step) {
+#pragma unroll
+            for (int k = 0; k < kTC; ++k) {
+                const float4 x = s_enc[warp][k][0][lane], y = s_enc[warp][k][1][lane];
+                enc[k][0] += x.x, enc[k][1] += x.y, enc[k][2] += x.z, enc[k][3] += x.w;
+                enc[k][4] += y.x, enc[k][5] += y.y, enc[k][6] += y.z, enc[k][7] += y.w;
+            }
+        }
+        __syncthreads();
+    }
+    if (warp == 0 && col_in) {
+#pragma unroll
+        for (int k = 0; k < kTC; ++k)
+            if (t0 + k < Tmax) {
+                float4* o = reinterpret_cast<float4*>(d_enc + (static_cast<int64_t>(b) * Tmax + t0 + k) * H + c);
+                const bool v = k < tn;
+                o[0] = v ? make_float4(enc[k][0], enc[k][1], enc[k][2], enc[k][3]) : make_float4(0.f, 0.f, 0.f, 0.f);
+                o[1] = v ? make_float4(enc[k][4], enc[k][5], enc[k][6], enc[k][7]) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
     }
 }
 
@@ -196,8 +213,8 @@ GradLayout grad_layout(int B, int Tmax, int Umax, int H, int V) {
     off += align256(std::max(sizeof(__nv_bfloat16) * L.R * L.Vp,
                              sizeof(float) * static_cast<size_t>((Tmax + kTC - 1) / kTC) * B * (Umax + 1) * H));
     L.h = off;
-    off += align256(sizeof(__nv_bfloat16) * L.R * (H + kJointHGPad));
-    L.dpre = off;  // K8's output [R][H] bf16
+    off += align256(sizeof(__nv_bfloat16) * L.R * H);
+    L.dpre = off;  // K8's output [R][H] bf16: dh (or dpre)
     off += align256(sizeof(__nv_bfloat16) * L.R * H);
     L.part = off;  // K9's per-row-range partials of dW and dbias
     off += align256(k9_partial_bytes(L.Vp, H));
@@ -255,21 +272,25 @@ extern "C" rnnt_status rnnt_joint_loss_grad(const void* enc, const void* pred, c
     // every padded row with the tail [*nrows, R) zeroed on the device
     const int R = static_cast<int>(valid_rows >= 0 ? valid_rows : L.R);
     if (valid_rows < 0) {
-        k7_zero_tail<<<1184, 256, 0, s>>>(nrows, L.R, L.Vp, H + kJointHGPad, dz, hb);
+        k7_zero_tail<<<1184, 256, 0, s>>>(nrows, L.R, L.Vp, H, dz, hb);
     } else {
         k7_check_rows<<<1, 256, 0, s>>>(nrows, valid_rows, B, losses);
     }
     if (cudaGetLastError() != cudaSuccess) return RNNT_ERR_CUDA;
-    // K8: dpre = (dz W) * (1 - h^2); K9: dW, dbias (tensor cores, k8_joint_bwd.cu)
-    if (launch_k8(dz, static_cast<const __nv_bfloat16*>(weight), hb, dpre, R, H, H + kJointHGPad, V, L.Vp, s) !=
-        cudaSuccess)
+    // K8: dh = dz W (bf16; RNNT_K8_TANH=1: dpre = dh * (1 - h^2) in K8's epilogue, A/B); K9: dW, dbias (tensor
+    // cores, k8_joint_bwd.cu)
+    const bool tanh_k8 = getenv("RNNT_K8_TANH") && atoi(getenv("RNNT_K8_TANH")) != 0;
+    if (launch_k8(dz, static_cast<const __nv_bfloat16*>(weight), hb, dpre, R, H, H, V, L.Vp, tanh_k8, s) != cudaSuccess)
         return RNNT_ERR_CUDA;
-    if (launch_k9(dz, hb, R, H, H + kJointHGPad, V, L.Vp, part, d_weight, d_bias, s) != cudaSuccess)
+    if (launch_k9(dz, hb, R, H, H, V, L.Vp, part, d_weight, d_bias, s) != cudaSuccess)
         return RNNT_ERR_CUDA;
-    // K7: the reductions of dpre into d enc / d pred
+    // K7: tanh' and the reductions into d enc / d pred
     float* ppart = reinterpret_cast<float*>(ws + L.dz);  // dz is dead after K8 / K9
-    k7_reduce<<<dim3((Tmax + kTC - 1) / kTC, B, H / 128), 128, 0, s>>>(dpre, logit_lens, target_lens, B, Tmax, Umax,
-                                                                       H, d_enc, ppart);
+    const dim3 g7((Tmax + kTC - 1) / kTC, B, (H + 255) / 256);
+    if (tanh_k8)
+        k7_reduce<true><<<g7, 256, 0, s>>>(dpre, nullptr, logit_lens, target_lens, B, Tmax, Umax, H, d_enc, ppart);
+    else
+        k7_reduce<false><<<g7, 256, 0, s>>>(dpre, hb, logit_lens, target_lens, B, Tmax, Umax, H, d_enc, ppart);
     k7_pred_sum<<<dim3(Umax + 1, B), 128, 0, s>>>(ppart, logit_lens, target_lens, B, Tmax, Umax, H, d_pred);
     return cudaGetLastError() == cudaSuccess ? RNNT_OK : RNNT_ERR_CUDA;
 }
