@@ -78,9 +78,37 @@ __device__ __forceinline__ void mma_kblock(uint32_t d_tmem, uint32_t a_tmem, uin
         "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// The same K block as one pair MMA (cta_group::2, M = 256: the A rows are this CTA's tile then the peer's, each
+// in its own TMEM at a_tmem; B's N = 128 columns are split 64 / 64 between the two CTAs' stages), issued by
+// the pair's even CTA only.
+__device__ __forceinline__ void mma_kblock_2sm(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                               uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p, q, e;\n"
+        ".reg .b32 a1, a2, a3;\n"
+        ".reg .b64 b1, b2, b3;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "setp.eq.b32 q, %4, %4;\n"
+        "add.u32 a1, %1, 8;\n"
+        "add.u32 a2, %1, 16;\n"
+        "add.u32 a3, %1, 24;\n"
+        "add.u64 b1, %2, 2;\n"
+        "add.u64 b2, %2, 4;\n"
+        "add.u64 b3, %2, 6;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a1], b1, %3, q;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a2], b2, %3, q;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a3], b3, %3, q;\n"
+        "}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
 // Instruction descriptor: fp32 D (bits 4-5 = 1), bf16 A (7-9 = 1) and B (10-12 = 1), both K-major,
 // N >> 3 at bits 17-22, M >> 4 at bits 24-28.
 constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(kNTile >> 3) << 17) | (uint32_t(128 >> 4) << 24);
+constexpr uint32_t kIdescPair = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(kNTile >> 3) << 17) | (uint32_t(256 >> 4) << 24);
 __device__ __forceinline__ float rcp_approx(float x) {
     float y;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -164,14 +192,22 @@ __device__ __forceinline__ float4 bias4(const JointArgs& a, int v) {
 // kSB: the bias (padded to whole N tiles with -inf) is staged once in shared memory -- when it is small
 // (Vp <= kSBiasMaxV); else it is read per chunk from global memory (bias4), issued ahead of the TMEM load.
 // Measured: the shared copy is ~14% faster on the forward at V = 1024 (epilogue latency).
-template <bool kGrad, int kCl, bool kSB>
+// kPair (kCl = 2): the pair's tiles go through ONE pair MMA (cta_group::2, M = 256) per K16 step instead of one
+// MMA per CTA, each CTA holding only its 64-column half of every W stage (no multicast): per CTA and stage 8 KB
+// of W against 256 MMA cycles, half of what the multicast pair receives -- the L2 -> SM delivery (~47 B per
+// cycle per SM measured on K9) is then no longer the limit.  Only the even CTA issues MMAs; the odd CTA's
+// builders tell it that their A tile is in TMEM (one remote arrive per tile) and its epilogue warps release the
+// accumulators on the leader's acc_empty (one remote arrive per warp per N tile).
+template <bool kGrad, int kCl, bool kSB, bool kPair>
 __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
     k6_joint_lse(const __grid_constant__ CUtensorMap w_map, const JointArgs a) {
+    static_assert(!kPair || kCl == 2, "pair MMAs need clusters of 2");
+    constexpr int kSlot = kPair ? kStageBytes / 2 : kStageBytes;  // a W stage slot in this CTA
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // carve: [W stages (1024-aligned)] [A staging 128 x H bf16] [epilogue exchange] [barriers] [tmem slot]
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* wst = base;
-    uint8_t* stage_a = wst + static_cast<size_t>(a.stages) * kStageBytes;
+    uint8_t* stage_a = wst + static_cast<size_t>(a.stages) * kSlot;
     const int Vp = (a.V + kNTile - 1) / kNTile * kNTile;  // V rounded up to whole N tiles
     // A staging: 128 rows of H + kJointHPad bf16 (the 16-byte pad: conflict-free thread-per-row reads; kGrad: the
     // rows' first H columns are h's global rows)
@@ -207,25 +243,31 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
         return true;
     };
 
+    const uint32_t crank = kCl > 1 ? cluster_rank() : 0;
+    const bool leader = crank == 0;
     if (threadIdx.x == 0) {
         for (int s = 0; s < a.stages; ++s) {
             mbar_init(&b_full[s], 1);
-            mbar_init(&b_empty[s], kCl);  // released by the MMAs of every CTA of the cluster
+            mbar_init(&b_empty[s], kPair ? 1 : kCl);  // released by the MMAs of every CTA of the cluster
         }
-        mbar_init(a_full, 256);
+        mbar_init(a_full, kPair ? 256 + 1 : 256);  // pair: + the odd CTA's builders (one remote arrive)
         mbar_init(a_empty, 1);
         for (int i = 0; i < kAccBufs; ++i) {
             mbar_init(&acc_full[i], 1);
-            mbar_init(&acc_empty[i], 256);  // both epilogue groups
+            mbar_init(&acc_empty[i], kPair ? 256 + 8 : 256);  // both epilogue groups (pair: + the odd CTA's 8 warps)
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&w_map)) : "memory");
     }
     if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(kTmemCols)
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        if constexpr (kPair) {
+            tmem_alloc_2sm(tmem_slot, kTmemCols);
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                         "r"(kTmemCols)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
     }
     tc_fence_before();
     if constexpr (kCl > 1)
@@ -237,7 +279,6 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
     // Row tiles: blockIdx.x + k * gridDim.x for k < n_iter, n_iter taken from the cluster's first CTA
     const int64_t bx = blockIdx.x, cl0 = bx - bx % kCl;
     const int64_t n_iter = ntiles > cl0 ? (ntiles - cl0 + gridDim.x - 1) / gridDim.x : 0;
-    const uint32_t crank = kCl > 1 ? cluster_rank() : 0;
     const bool pon = (a.dbg & 4) != 0;
     unsigned long long w_tma = 0, w_afull = 0, w_accempty = 0, w_bfull = 0, w_accfull = 0, w_aempty = 0;
     const long long t_start = clock64();
@@ -251,6 +292,11 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
                 for (int n = 0; n < NT; ++n)
                     for (int kb = 0; kb < KB; ++kb) {
                         mbar_wait_t(&b_empty[s], ph ^ 1, pon, w_tma);
+                        if constexpr (kPair) {  // own 64-column half, landing on the leader's barrier
+                            if (leader) mbar_expect_tx(&b_full[s], kStageBytes);  // both halves
+                            tma_load_2d_2sm(wst + static_cast<size_t>(s) * kSlot, &w_map, leader_addr(&b_full[s]),
+                                            kb * kKBlock, n * kNTile + static_cast<int>(crank) * (kNTile / 2));
+                        } else {
                         mbar_expect_tx(&b_full[s], kStageBytes);  // the whole stage lands here (both halves)
                         if constexpr (kCl > 1)
                             tma_load_2d_mc(wst + static_cast<size_t>(s) * kStageBytes + crank * (kStageBytes / kCl),
@@ -259,14 +305,15 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
                         else
                             tma_load_2d(wst + static_cast<size_t>(s) * kStageBytes, &w_map, &b_full[s], kb * kKBlock,
                                         n * kNTile);
+                        }
                         if (++s == a.stages) {
                             s = 0;
                             ph ^= 1;
                         }
                     }
         }
-    } else if (warp == 1) {
-        // ===== MMA issuer =====
+    } else if (warp == 1 && (!kPair || leader)) {
+        // ===== MMA issuer (pair: the even CTA, for both) =====
         int s = 0;
         uint32_t ph = 0;
         uint32_t it = 0;  // accumulator use counter
@@ -282,10 +329,15 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
                 for (int kb = 0; kb < KB; ++kb) {
                     mbar_wait_t(&b_full[s], ph, pon, w_bfull);
                     tc_fence_after();
-                    const uint64_t bdesc = sw128_desc(smem_u32(wst + static_cast<size_t>(s) * kStageBytes));
-                    mma_kblock(d_tmem, tmem + kb * (kKBlock / 2), bdesc, kIdesc, kb ? 1u : 0u);
+                    const uint64_t bdesc = sw128_desc(smem_u32(wst + static_cast<size_t>(s) * kSlot));
+                    if constexpr (kPair)
+                        mma_kblock_2sm(d_tmem, tmem + kb * (kKBlock / 2), bdesc, kIdescPair, kb ? 1u : 0u);
+                    else
+                        mma_kblock(d_tmem, tmem + kb * (kKBlock / 2), bdesc, kIdesc, kb ? 1u : 0u);
                     // frees the W stage (in every CTA of the cluster: its producer refills both) once these MMAs complete
-                    if constexpr (kCl > 1)
+                    if constexpr (kPair)
+                        tc_commit_2sm_mc(&b_empty[s], 3);
+                    else if constexpr (kCl > 1)
                         tc_commit_mc(&b_empty[s], static_cast<uint16_t>((1u << kCl) - 1));
                     else
                         tc_commit(&b_empty[s]);
@@ -294,11 +346,17 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
                         ph ^= 1;
                     }
                 }
-                tc_commit(&acc_full[acc]);
+                if constexpr (kPair)
+                    tc_commit_2sm_mc(&acc_full[acc], 3);
+                else
+                    tc_commit(&acc_full[acc]);
             }
             // the A tile in TMEM may be overwritten.  (Handing it over per K half, so that the copy of half 0
             // overlaps the last N tile's MMAs on half 1, measured slower: 1.60 vs 1.52 ms.)
-            tc_commit(a_empty);
+            if constexpr (kPair)
+                tc_commit_2sm_mc(a_empty, 3);
+            else
+                tc_commit(a_empty);
         }
     } else if (warp >= 4 && warp < 12) {
         // ===== epilogue: thread = row; both groups drain every accumulator buffer, group eg taking columns
@@ -414,7 +472,12 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
                         }
                     }
                     tc_fence_before();
-                    mbar_arrive(&acc_empty[acc]);
+                    if (!kPair || leader) {
+                        mbar_arrive(&acc_empty[acc]);
+                    } else {  // the odd CTA: one arrive per warp on the leader's barrier
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_remote(&acc_empty[acc], 0);
+                    }
                 }
                 continue;
             }
@@ -474,7 +537,12 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
                     if (static_cast<unsigned>(yv - v0) < 32u) zy = select32(z, yv - v0);  // some lane's label is in most chunks
                 }
                 tc_fence_before();
-                mbar_arrive(&acc_empty[acc]);
+                if (!kPair || leader) {
+                    mbar_arrive(&acc_empty[acc]);
+                } else {  // the odd CTA: one arrive per warp on the leader's barrier
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_remote(&acc_empty[acc], 0);
+                }
             }
             float4* xb_ = xchg + (tile_local & 1) * kRowsPerTile + rl;
             if (eg == 1) *xb_ = make_float4(m, ssum, zb, zy);
@@ -654,7 +722,12 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
             }
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             tc_fence_before();
-            mbar_arrive(a_full);
+            if (!kPair || leader) {
+                mbar_arrive(a_full);
+            } else {  // the odd CTA's builders: all 256 done, then one arrive on the leader's barrier
+                asm volatile("bar.sync 5, 256;" ::: "memory");
+                if (warp == 12 && lane == 0) mbar_arrive_remote(a_full, 0);
+            }
             if (k + 1 < n_iter) {
                 const int p = p_next;
                 p_next = map_of(tile + 2 * static_cast<int64_t>(gridDim.x));
@@ -679,8 +752,12 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
     else
         __syncthreads();
     tc_fence_after();
-    if (warp == 1)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
+    if (warp == 1) {
+        if constexpr (kPair)
+            tmem_dealloc_2sm(tmem, kTmemCols);
+        else
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
+    }
 }
 
 // Row map of the valid cells (t < T_b, u <= U_b), utterance by utterance: blocks (x, b) write
@@ -714,9 +791,9 @@ __global__ void __launch_bounds__(256) k6_rowmap(const int32_t* __restrict__ T_b
     if (b == B - 1 && blockIdx.x == 0 && threadIdx.x == 0) *nrows = off + n;
 }
 
-size_t joint_smem_bytes(int H, int V, int stages, bool grad) {  // V = 0: bias not staged (!kSB)
+size_t joint_smem_bytes(int H, int V, int stages, bool grad, bool pair) {  // V = 0: bias not staged (!kSB)
     return (grad ? 8 * 2048 + 128 : 0) +  // kGrad: the epilogue warps' dz staging blocks
-           1024 + static_cast<size_t>(stages) * kStageBytes + static_cast<size_t>(kRowsPerTile) * (H + kJointHPad) * 2 +
+           1024 + static_cast<size_t>(stages) * (pair ? kStageBytes / 2 : kStageBytes) + static_cast<size_t>(kRowsPerTile) * (H + kJointHPad) * 2 +
            static_cast<size_t>((V + kNTile - 1) / kNTile * kNTile) * 4 + 2 * kRowsPerTile * 16 + (2 * kMaxStages + 2 + 2 * kAccBufs) * 8 + 16;
 }
 
@@ -792,13 +869,17 @@ rnnt_status joint_front(const void* enc, const void* pred, const void* weight, c
     int stages = kMaxStages;
     const bool sb = V <= kSBiasMaxV;  // bias staged in shared memory (small vocabularies), else read from global
     const int Vs = sb ? V : 0;
-    while (stages > 2 && joint_smem_bytes(H, Vs, stages, g != nullptr) > static_cast<size_t>(smem_max)) --stages;
-    const size_t smem = joint_smem_bytes(H, Vs, stages, g != nullptr);
+    // CTA pairs run pair MMAs by default (RNNT_K6_PAIR=0: per-CTA MMAs with the W stage multicast, for A/B)
+    const bool pair = cl == 2 && !(getenv("RNNT_K6_PAIR") && atoi(getenv("RNNT_K6_PAIR")) == 0);
+    while (stages > 2 && joint_smem_bytes(H, Vs, stages, g != nullptr, pair) > static_cast<size_t>(smem_max)) --stages;
+    const size_t smem = joint_smem_bytes(H, Vs, stages, g != nullptr, pair);
     if (smem > static_cast<size_t>(smem_max)) return RNNT_ERR_UNSUPPORTED;
-    auto kern = sb ? (g ? (cl > 1 ? k6_joint_lse<true, 2, true> : k6_joint_lse<true, 1, true>)
-                        : (cl > 1 ? k6_joint_lse<false, 2, true> : k6_joint_lse<false, 1, true>))
-                   : (g ? (cl > 1 ? k6_joint_lse<true, 2, false> : k6_joint_lse<true, 1, false>)
-                        : (cl > 1 ? k6_joint_lse<false, 2, false> : k6_joint_lse<false, 1, false>));
+    auto kern = pair ? (sb ? (g ? k6_joint_lse<true, 2, true, true> : k6_joint_lse<false, 2, true, true>)
+                           : (g ? k6_joint_lse<true, 2, false, true> : k6_joint_lse<false, 2, false, true>))
+              : sb ? (g ? (cl > 1 ? k6_joint_lse<true, 2, true, false> : k6_joint_lse<true, 1, true, false>)
+                        : (cl > 1 ? k6_joint_lse<false, 2, true, false> : k6_joint_lse<false, 1, true, false>))
+                   : (g ? (cl > 1 ? k6_joint_lse<true, 2, false, false> : k6_joint_lse<true, 1, false, false>)
+                        : (cl > 1 ? k6_joint_lse<false, 2, false, false> : k6_joint_lse<false, 1, false, false>));
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
         return RNNT_ERR_CUDA;
 
