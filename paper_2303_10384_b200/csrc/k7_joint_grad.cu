@@ -75,15 +75,16 @@ __device__ int utt_offset(const int32_t* T_b, const int32_t* U_b, int b, int Tma
 // K7, pass 1: block (chunk, b, slice) takes frames [chunk * kTC, +kTC) of utterance b and a 256-column slice of
 // H, and streams each of its rows of dh (K8's output) and h ONCE: dpre = dh * (1 - h^2) (kPre: the input already
 // is dpre, K8 applied tanh'; h is not read).  256 threads = 8 warps; lane = 8 columns, so a warp reads a whole
-// 512-byte row segment per 16-byte load; warp w owns units u = w (mod 8).  Its sum over the chunk's frames is the chunk's partial of d pred(b, u) (-> part); its contribution to
+// 512-byte row segment per 16-byte load; warp w owns units u = w (mod 8) and loads its kTC frames of a unit at
+// once.  Its sum over the chunk's frames is the chunk's partial of d pred(b, u) (-> part); its contribution to
 // d enc(b, t) stays in registers and the 8 warps' partials are added in a fixed tree order through shared
-// memory (the block owns every unit of its frames: d enc is complete, written directly).  Two blocks per SM
-// (<= 128 registers: a quarter of a unit's frames in flight at a time, all 8 warps).  Pass 2 sums the
+// memory (the block owns every unit of its frames: d enc is complete, written directly).  (Two blocks per SM
+// at <= 128 registers, with fewer frames in flight per warp, was slower: 0.83 vs 0.63 ms at c3.)  Pass 2 sums the
 // chunk partials of d pred in chunk order.  Deterministic.
 constexpr int kTC = 8;
 
 template <bool kPre>
-__global__ void __launch_bounds__(256, 2) k7_reduce(const __nv_bfloat16* __restrict__ dx,
+__global__ void __launch_bounds__(256, 1) k7_reduce(const __nv_bfloat16* __restrict__ dx,
                                                     const __nv_bfloat16* __restrict__ h,
                                                     const int32_t* __restrict__ T_b, const int32_t* __restrict__ U_b,
                                                     int B, int Tmax, int Umax, int H, float* __restrict__ d_enc,
@@ -107,36 +108,33 @@ __global__ void __launch_bounds__(256, 2) k7_reduce(const __nv_bfloat16* __restr
     for (int u = warp; u <= U && tn > 0 && col_in; u += 8) {
         float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         const int64_t r0 = off + static_cast<int64_t>(t0) * (U + 1) + u;
+        uint4 dv[kTC], hv[kTC];
 #pragma unroll
-        for (int k0 = 0; k0 < kTC; k0 += kTC / 4) {  // a quarter of the unit's frames in flight at once (2 blocks per SM)
-            uint4 dv[kTC / 4], hv[kTC / 4];
+        for (int k = 0; k < kTC; ++k)  // all the unit's rows in flight before any use
+            if (k < tn) {
+                const int64_t r = r0 + static_cast<int64_t>(k) * (U + 1);
+                dv[k] = __ldcs(reinterpret_cast<const uint4*>(dx + r * H + c));
+                if (!kPre) hv[k] = __ldcs(reinterpret_cast<const uint4*>(h + r * H + c));
+            }
 #pragma unroll
-            for (int k = 0; k < kTC / 4; ++k)
-                if (k0 + k < tn) {
-                    const int64_t r = r0 + static_cast<int64_t>(k0 + k) * (U + 1);
-                    dv[k] = __ldcs(reinterpret_cast<const uint4*>(dx + r * H + c));
-                    if (!kPre) hv[k] = __ldcs(reinterpret_cast<const uint4*>(h + r * H + c));
-                }
+        for (int k = 0; k < kTC; ++k)
+            if (k < tn) {
+                const uint32_t dw[4] = {dv[k].x, dv[k].y, dv[k].z, dv[k].w};
+                uint32_t hw[4] = {0u, 0u, 0u, 0u};
+                if (!kPre) hw[0] = hv[k].x, hw[1] = hv[k].y, hw[2] = hv[k].z, hw[3] = hv[k].w;
 #pragma unroll
-            for (int k = 0; k < kTC / 4; ++k)
-                if (k0 + k < tn) {
-                    const uint32_t dw[4] = {dv[k].x, dv[k].y, dv[k].z, dv[k].w};
-                    uint32_t hw[4] = {0u, 0u, 0u, 0u};
-                    if (!kPre) hw[0] = hv[k].x, hw[1] = hv[k].y, hw[2] = hv[k].z, hw[3] = hv[k].w;
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        float2 d = unpack_bf16x2(dw[j]);
-                        if (!kPre) {
-                            const float2 hh = unpack_bf16x2(hw[j]);
-                            d = upk(fmul2(pk(d.x, d.y), ffma2(pk(-hh.x, -hh.y), pk(hh.x, hh.y), pk(1.f, 1.f))));
-                        }
-                        acc[2 * j] += d.x;
-                        acc[2 * j + 1] += d.y;
-                        enc[k0 + k][2 * j] += d.x;
-                        enc[k0 + k][2 * j + 1] += d.y;
+                for (int j = 0; j < 4; ++j) {
+                    float2 d = unpack_bf16x2(dw[j]);
+                    if (!kPre) {
+                        const float2 hh = unpack_bf16x2(hw[j]);
+                        d = upk(fmul2(pk(d.x, d.y), ffma2(pk(-hh.x, -hh.y), pk(hh.x, hh.y), pk(1.f, 1.f))));
                     }
+                    acc[2 * j] += d.x;
+                    acc[2 * j + 1] += d.y;
+                    enc[k][2 * j] += d.x;
+                    enc[k][2 * j + 1] += d.y;
                 }
-        }
+            }
         float4* pp = reinterpret_cast<float4*>(part + ((static_cast<int64_t>(chunk) * B + b) * (Umax + 1) + u) * H + c);
         pp[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
         pp[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
