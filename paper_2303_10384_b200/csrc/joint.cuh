@@ -38,8 +38,9 @@ rnnt_status joint_front(const void* enc, const void* pred, const void* weight, c
 size_t k9_partial_bytes(int Vp, int H);
 cudaError_t launch_k8(const __nv_bfloat16* dz, const __nv_bfloat16* weight, const __nv_bfloat16* h,
                       __nv_bfloat16* out, int R, int H, int Hg, int V, int Vp, bool tanh_in_k8, cudaStream_t s);
+// max_ctas > 0 caps K9's grid (the rest of the SMs run K7 concurrently); 0 = every co-resident pair.
 cudaError_t launch_k9(const __nv_bfloat16* dz, const __nv_bfloat16* h, int R, int H, int Hg, int V, int Vp,
-                      float* part, float* d_weight, float* d_bias, cudaStream_t s);
+                      float* part, float* d_weight, float* d_bias, cudaStream_t s, int max_ctas = 0);
 
 constexpr int kJointVTile = 128;  // K6's N tile: dz rows are padded to a multiple of it
 constexpr int kJointHPad = 8;     // K6's A staging rows: H + 8 bf16 (16 bytes of pad: conflict-free row reads)

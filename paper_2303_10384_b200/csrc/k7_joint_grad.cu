@@ -82,6 +82,11 @@ __device__ int utt_offset(const int32_t* T_b, const int32_t* U_b, int b, int Tma
 // at <= 128 registers, with fewer frames in flight per warp, was slower: 0.83 vs 0.63 ms at c3.)  Pass 2 sums the
 // chunk partials of d pred in chunk order.  Deterministic.
 constexpr int kTC = 8;
+// K9's SM cap when K7 runs beside it (K7 fills the rest).  0 = sequential (the default): A/B on B200, 3
+// alternating reps of 60-step training steps (scripts/gpu_k9ovl2.sh): c3 7.29 ms sequential, 7.19 with K9 on
+// 96 SMs, 7.25 on 112; p124 2.13 sequential, 2.14 / 2.16 -- within the power-capped clock's noise, so the
+// simpler schedule stays.  RNNT_K9_CTAS=n turns the overlap on.
+constexpr int kK9OverlapCtas = 0;
 
 template <bool kPre>
 __global__ void __launch_bounds__(256, 1) k7_reduce(const __nv_bfloat16* __restrict__ dx,
@@ -197,7 +202,7 @@ __global__ void __launch_bounds__(128) k7_pred_sum(const float* __restrict__ par
 struct GradLayout {
     int64_t R;  // padded rows B * Tmax * (Umax + 1)
     int Vp;
-    size_t base, rowmap, nrows, dz, h, dpre, part, total;
+    size_t base, rowmap, nrows, dz, h, dpre, part, kpart, total;
 };
 
 GradLayout grad_layout(int B, int Tmax, int Umax, int H, int V) {
@@ -210,15 +215,16 @@ GradLayout grad_layout(int B, int Tmax, int Umax, int H, int V) {
     off += align256(sizeof(int) * L.R);
     L.nrows = off;
     off += 256;
-    L.dz = off;  // dz; after K8 / K9, K7's d pred partials [ceil(Tmax / kTC)][B][Umax + 1][H] fp32
-    off += align256(std::max(sizeof(__nv_bfloat16) * L.R * L.Vp,
-                             sizeof(float) * static_cast<size_t>((Tmax + kTC - 1) / kTC) * B * (Umax + 1) * H));
+    L.dz = off;
+    off += align256(sizeof(__nv_bfloat16) * L.R * L.Vp);
     L.h = off;
     off += align256(sizeof(__nv_bfloat16) * L.R * H);
     L.dpre = off;  // K8's output [R][H] bf16: dh (or dpre)
     off += align256(sizeof(__nv_bfloat16) * L.R * H);
     L.part = off;  // K9's per-row-range partials of dW and dbias
     off += align256(k9_partial_bytes(L.Vp, H));
+    L.kpart = off;  // K7's per-frame-chunk partials of d pred [ceil(Tmax / kTC)][B][Umax + 1][H] fp32
+    off += align256(sizeof(float) * static_cast<size_t>((Tmax + kTC - 1) / kTC) * B * (Umax + 1) * H);
     L.total = off;
     return L;
 }
@@ -278,20 +284,36 @@ extern "C" rnnt_status rnnt_joint_loss_grad(const void* enc, const void* pred, c
         k7_check_rows<<<1, 256, 0, s>>>(nrows, valid_rows, B, losses);
     }
     if (cudaGetLastError() != cudaSuccess) return RNNT_ERR_CUDA;
-    // K8: dh = dz W (bf16; RNNT_K8_TANH=1: dpre = dh * (1 - h^2) in K8's epilogue, A/B); K9: dW, dbias (tensor
-    // cores, k8_joint_bwd.cu)
+    // K8: dh = dz W (bf16; RNNT_K8_TANH=1: dpre = dh * (1 - h^2) in K8's epilogue, A/B), on every SM.  Then K9
+    // (dW, dbias: tensor-bound) and K7 (tanh' + reductions: HBM-bound) run side by side: K9 on an internal
+    // high-priority stream with its grid capped at kK9OverlapCtas SMs, K7 on the caller's stream filling the
+    // SMs K9 leaves (neither fits on an SM next to the other: K9 holds ~200 KB of shared memory); the caller's
+    // stream then joins K9 back.  RNNT_K9_CTAS=n sets the cap (0: K9 on every SM, then K7: sequential).
     const bool tanh_k8 = getenv("RNNT_K8_TANH") && atoi(getenv("RNNT_K8_TANH")) != 0;
     if (launch_k8(dz, static_cast<const __nv_bfloat16*>(weight), hb, dpre, R, H, H, V, L.Vp, tanh_k8, s) != cudaSuccess)
         return RNNT_ERR_CUDA;
-    if (launch_k9(dz, hb, R, H, H, V, L.Vp, part, d_weight, d_bias, s) != cudaSuccess)
+    int k9_ctas = kK9OverlapCtas;
+    if (const char* e = getenv("RNNT_K9_CTAS")) k9_ctas = atoi(e);
+    AuxPool* pool = k9_ctas > 0 ? aux_pool() : nullptr;
+    cudaStream_t k9s = s;
+    if (pool) {
+        k9s = pool->aux[0];
+        if (cudaEventRecord(pool->k1_done[0], s) != cudaSuccess || cudaStreamWaitEvent(k9s, pool->k1_done[0], 0) != cudaSuccess)
+            return RNNT_ERR_CUDA;
+    }
+    if (launch_k9(dz, hb, R, H, H, V, L.Vp, part, d_weight, d_bias, k9s, pool ? k9_ctas : 0) != cudaSuccess)
         return RNNT_ERR_CUDA;
-    // K7: tanh' and the reductions into d enc / d pred
-    float* ppart = reinterpret_cast<float*>(ws + L.dz);  // dz is dead after K8 / K9
+    if (pool && cudaEventRecord(pool->k2_done[0], k9s) != cudaSuccess) return RNNT_ERR_CUDA;
+    // K7: tanh' and the reductions into d enc / d pred (its d pred partials in their own region: K9 may still
+    // be reading dz)
+    float* ppart = reinterpret_cast<float*>(ws + L.kpart);
     const dim3 g7((Tmax + kTC - 1) / kTC, B, (H + 255) / 256);
     if (tanh_k8)
         k7_reduce<true><<<g7, 256, 0, s>>>(dpre, nullptr, logit_lens, target_lens, B, Tmax, Umax, H, d_enc, ppart);
     else
         k7_reduce<false><<<g7, 256, 0, s>>>(dpre, hb, logit_lens, target_lens, B, Tmax, Umax, H, d_enc, ppart);
     k7_pred_sum<<<dim3(Umax + 1, B), 128, 0, s>>>(ppart, logit_lens, target_lens, B, Tmax, Umax, H, d_pred);
-    return cudaGetLastError() == cudaSuccess ? RNNT_OK : RNNT_ERR_CUDA;
+    if (cudaGetLastError() != cudaSuccess) return RNNT_ERR_CUDA;
+    if (pool && cudaStreamWaitEvent(s, pool->k2_done[0], 0) != cudaSuccess) return RNNT_ERR_CUDA;  // join K9
+    return RNNT_OK;
 }

@@ -1114,7 +1114,7 @@ cudaError_t launch_k8(const __nv_bfloat16* dz, const __nv_bfloat16* weight, cons
 }
 
 cudaError_t launch_k9(const __nv_bfloat16* dz, const __nv_bfloat16* h, int R, int H, int Hg, int V, int Vp,
-                      float* part, float* d_weight, float* d_bias, cudaStream_t s) {
+                      float* part, float* d_weight, float* d_bias, cudaStream_t s, int max_ctas) {
     int smem_max = 0;
     const int nsm = sm_count_and_smem(&smem_max);
     if (!nsm) return cudaErrorUnknown;
@@ -1135,6 +1135,7 @@ cudaError_t launch_k9(const __nv_bfloat16* dz, const __nv_bfloat16* h, int R, in
         return cudaErrorInvalidConfiguration;
     int resident = max_clusters(kern, cl, smem, kK9Threads);  // one wave: every work unit co-resident
     if (resident <= 0) resident = nsm / cl;
+    if (max_ctas > 0) resident = std::max(1, std::min(resident, max_ctas / cl));  // leave SMs to a concurrent K7
     int splits = std::max(1, std::min(resident, kK9MaxCtas / cl) / groups);
     splits = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(splits, nst_total)));
     const int per = static_cast<int>((nst_total + splits - 1) / splits);
