@@ -506,9 +506,9 @@ def main():
 
     # ---- end to end through the host-buffer C-ABI entry point (pinned host in/out, copies in the timed region)
     e2e = None
-    if not args.no_e2e and args.dtype != "f32":
-        e2e = {"value": None, "unit": UNIT, "reason": "the host-buffer entry point takes fp32 only"}
-    elif not args.no_e2e and 2.2 * z.numel() * 4 * int(os.environ.get("LOCAL_WORLD_SIZE", world)) > host_avail_bytes():
+    if not args.no_e2e and args.mode != "loss_grad":
+        e2e = {"value": None, "unit": UNIT, "reason": "the host-buffer entry point computes loss + grad"}
+    elif not args.no_e2e and 2.2 * z.numel() * esize * int(os.environ.get("LOCAL_WORLD_SIZE", world)) > host_avail_bytes():
         e2e = {"value": None, "unit": UNIT, "reason": "pinned host copies of logits + grads exceed host RAM"}
     elif not args.no_e2e:
         zh = z.cpu().pin_memory()
@@ -522,7 +522,7 @@ def main():
         del z
         pb["logits"] = None
         torch.cuda.empty_cache()
-        dbuf = torch.empty(rb.rnnt_host_buffer_bytes(B, Tmax, Umax, V), dtype=torch.uint8, device=dev)
+        dbuf = torch.empty(rb.rnnt_host_buffer_bytes(B, Tmax, Umax, V, zh.dtype), dtype=torch.uint8, device=dev)
         for _ in range(1):
             rb.rnnt_loss_host(zh, th, Th, Uh, gcfg.blank, variant, losses_host=lh, grads_host=gh, device_buffer=dbuf)
         torch.cuda.synchronize()
@@ -535,11 +535,12 @@ def main():
         e_end.record()
         torch.cuda.synchronize()
         e_ms = rdist.max_over_ranks(e_start.elapsed_time(e_end), dev) / args.e2e_steps
-        h2d = zh.numel() * 4 + th.numel() * 4 + Th.numel() * 4 + Uh.numel() * 4
-        d2h = gh.numel() * 4 + lh.numel() * 4
+        h2d = zh.numel() * esize + th.numel() * 4 + Th.numel() * 4 + Uh.numel() * 4
+        d2h = gh.numel() * esize + lh.numel() * 4
         e2e = {"value": units / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": e_ms, "steps": args.e2e_steps,
-               "api": "rnnt_loss_host (pinned host buffers; chunked H2D / compute / D2H overlap)"}
+               "api": f"rnnt_loss_host ({args.dtype} pinned host buffers; chunks of utterances through a 3-slot "
+                      f"device ring, H2D / compute / D2H overlapped)"}
         del dbuf
     if rank == 0:
         line["e2e"] = e2e

@@ -160,16 +160,26 @@ rnnt_status rnnt_loss_sum(const float* losses, int B, double* loss_sum, void* st
 
 /* Host-buffer entry point (the end-to-end path): logits_host / targets_host / lens_host / losses_host /
  * grads_host are HOST pointers (pinned memory recommended; pageable works but serialises the copies).
- * device_buffer must hold rnnt_host_buffer_bytes(...) bytes of device memory: it receives staged logits
- * (and grads, in place) plus the workspace.  variant: -1 = plain RNN-T, else a wrnnt_variant.  Copies and
- * compute are pipelined over chunks of utterances on `stream` and internal events; the call returns after
- * enqueueing -- synchronize `stream` before reading the host outputs.  grads_host may be NULL (loss only). */
+ * device_buffer must hold rnnt_host_buffer_bytes(...) bytes of device memory: a ring of 3 staging slots of
+ * ~B/16 utterances each (logits in, grads out in place) plus their workspaces -- not the whole batch.
+ * variant: -1 = plain RNN-T, else a wrnnt_variant.  Copies and compute are pipelined over chunks of
+ * utterances (H2D of chunk c+1, compute of c and D2H of c-1 at once) on `stream` and two internal copy
+ * streams (cached per host thread and device) joined back into `stream`; the call returns after enqueueing --
+ * synchronize `stream` before reading the host outputs.  grads_host may be NULL (loss only).
+ * The _ex forms take the logits' storage type (rnnt_dtype: fp32 / fp16 / bf16, as rnnt_loss_ex; grads_host
+ * in the same type), so 16-bit storage halves the PCIe bytes. */
 size_t rnnt_host_buffer_bytes(int B, int Tmax, int Umax, int V);
+size_t rnnt_host_buffer_bytes_ex(int B, int Tmax, int Umax, int V, rnnt_dtype dtype);
 rnnt_status rnnt_loss_host(const float* logits_host, const int32_t* targets_host,
                            const int32_t* logit_lens_host, const int32_t* target_lens_host,
                            int B, int Tmax, int Umax, int V, int blank, int variant,
                            float* losses_host, float* grads_host,
                            void* device_buffer, size_t device_buffer_bytes, void* stream);
+rnnt_status rnnt_loss_host_ex(const void* logits_host, rnnt_dtype dtype, const int32_t* targets_host,
+                              const int32_t* logit_lens_host, const int32_t* target_lens_host,
+                              int B, int Tmax, int Umax, int V, int blank, int variant,
+                              float* losses_host, void* grads_host,
+                              void* device_buffer, size_t device_buffer_bytes, void* stream);
 
 /* Fused joint network + loss (§4.1: the benchmark's joint over Encoder
  * and Predictor embeddings of size 512; X comes from the joint network).  The logits

@@ -24,7 +24,8 @@ VARIANTS = {"rnnt": -1, "force_final": 0, "allow_ignore": 1}
 # Every symbol include/rnnt_b200.h declares.
 EXPORTS = ("rnnt_workspace_bytes", "rnnt_loss", "wrnnt_loss", "rnnt_loss_timed", "rnnt_loss_ex", "rnnt_viterbi",
            "rnnt_loss_sum", "rnnt_lattice_workspace_bytes", "rnnt_lattice_loss",
-           "rnnt_host_buffer_bytes", "rnnt_loss_host", "rnnt_joint_loss", "rnnt_joint_loss_ex", "rnnt_joint_viterbi",
+           "rnnt_host_buffer_bytes", "rnnt_loss_host", "rnnt_host_buffer_bytes_ex", "rnnt_loss_host_ex",
+           "rnnt_joint_loss", "rnnt_joint_loss_ex", "rnnt_joint_viterbi",
            "rnnt_joint_grad_workspace_bytes", "rnnt_joint_loss_grad",
            "rnnt_status_string", "rnnt_version")
 DTYPES = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2}
@@ -53,6 +54,8 @@ def _load():
         "rnnt_loss_sum": ([P, I, P, P], I),
         "rnnt_host_buffer_bytes": ([I, I, I, I], S),
         "rnnt_loss_host": ([P, P, P, P, I, I, I, I, I, I, P, P, P, S, P], I),
+        "rnnt_host_buffer_bytes_ex": ([I, I, I, I, I], S),
+        "rnnt_loss_host_ex": ([P, I, P, P, P, I, I, I, I, I, I, P, P, P, S, P], I),
         "rnnt_joint_loss": ([P, P, P, P, P, P, P, I, I, I, I, I, I, I, P, P, S, P], I),
         "rnnt_joint_loss_ex": ([P, P, P, P, P, P, P, I, I, I, I, I, I, I, P, P, S, P, P], I),
         "rnnt_joint_viterbi": ([P, P, P, P, P, P, P, I, I, I, I, I, I, I, P, P, P, P, S, P], I),
@@ -133,8 +136,8 @@ def rnnt_workspace_bytes(B: int, Tmax: int, Umax: int) -> int:
     return int(library.rnnt_workspace_bytes(B, Tmax, Umax))
 
 
-def rnnt_host_buffer_bytes(B: int, Tmax: int, Umax: int, V: int) -> int:
-    return int(library.rnnt_host_buffer_bytes(B, Tmax, Umax, V))
+def rnnt_host_buffer_bytes(B: int, Tmax: int, Umax: int, V: int, dtype=torch.float32) -> int:
+    return int(library.rnnt_host_buffer_bytes_ex(B, Tmax, Umax, V, DTYPES[dtype]))
 
 
 def _as_i32(x, device):
@@ -413,9 +416,10 @@ def rnnt_loss_sum(losses, out=None, stream=None):
 
 def rnnt_loss_host(logits_host, targets_host, logit_lens_host, target_lens_host, blank=0, variant="rnnt",
                    losses_host=None, grads_host=None, device_buffer=None, stream=None):
-    """Host-buffer entry point: host (ideally pinned) CPU tensors in and out; copies overlap compute.
-
-    Returns (losses_host, grads_host).  Synchronize the stream before reading them.
+    """Host-buffer entry point: host (ideally pinned) CPU tensors in and out; H2D copies, compute and D2H copies
+    of utterance chunks overlap through a 3-slot device ring.  logits_host: float32 / float16 / bfloat16
+    [B, Tmax, Umax+1, V] (grads_host, if given, the same type and shape); targets int32 [B, Umax], lengths int32
+    [B].  Returns (losses_host, grads_host).  Synchronize the stream before reading them.
     """
     def host(name, t, dtype, shape):
         if not (isinstance(t, torch.Tensor) and not t.is_cuda and t.dtype == dtype and t.is_contiguous()
@@ -424,11 +428,12 @@ def rnnt_loss_host(logits_host, targets_host, logit_lens_host, target_lens_host,
                             f"(got {getattr(t, 'dtype', type(t))} {tuple(getattr(t, 'shape', ()))})")
         return t
 
-    if not (isinstance(logits_host, torch.Tensor) and logits_host.dim() == 4):
-        raise TypeError("logits_host must be a CPU float32 tensor [B, Tmax, Umax+1, V]")
+    if not (isinstance(logits_host, torch.Tensor) and logits_host.dim() == 4 and logits_host.dtype in DTYPES):
+        raise TypeError("logits_host must be a CPU float32 / float16 / bfloat16 tensor [B, Tmax, Umax+1, V]")
     B, Tmax, Up1, V = logits_host.shape
     Umax = Up1 - 1
-    host("logits_host", logits_host, torch.float32, (B, Tmax, Up1, V))
+    dt = logits_host.dtype
+    host("logits_host", logits_host, dt, (B, Tmax, Up1, V))
     host("logit_lens_host", logit_lens_host, torch.int32, (B,))
     host("target_lens_host", target_lens_host, torch.int32, (B,))
     if Umax > 0:
@@ -437,14 +442,14 @@ def rnnt_loss_host(logits_host, targets_host, logit_lens_host, target_lens_host,
         losses_host = torch.empty(B, dtype=torch.float32, pin_memory=True)
     host("losses_host", losses_host, torch.float32, (B,))
     if grads_host is not None:
-        host("grads_host", grads_host, torch.float32, (B, Tmax, Up1, V))
-    need = rnnt_host_buffer_bytes(B, Tmax, Umax, V)
+        host("grads_host", grads_host, dt, (B, Tmax, Up1, V))
+    need = rnnt_host_buffer_bytes(B, Tmax, Umax, V, dt)
     if device_buffer is None:
         device_buffer = torch.empty(need, dtype=torch.uint8, device="cuda")
     _keep(stream, device_buffer)
     tg = targets_host if Umax > 0 else None
-    _check(library.rnnt_loss_host(_ptr(logits_host), _ptr(tg), _ptr(logit_lens_host), _ptr(target_lens_host),
-                                  B, Tmax, Umax, V, int(blank), VARIANTS[variant], _ptr(losses_host),
-                                  _ptr(grads_host), _ptr(device_buffer), device_buffer.numel(),
-                                  _stream(stream)))
+    _check(library.rnnt_loss_host_ex(_ptr(logits_host), DTYPES[dt], _ptr(tg), _ptr(logit_lens_host),
+                                     _ptr(target_lens_host), B, Tmax, Umax, V, int(blank), VARIANTS[variant],
+                                     _ptr(losses_host), _ptr(grads_host), _ptr(device_buffer),
+                                     device_buffer.numel(), _stream(stream)))
     return losses_host, grads_host

@@ -187,6 +187,35 @@ namespace {
 // Chunk size of the host path: ~16 chunks, so the pipeline fill (first H2D) and drain (last D2H) are short
 // against the overlapped middle where H2D(c+1), compute(c) and D2H(c-1) run together.
 int host_chunk(int B) { return std::max(1, (B + 15) / 16); }
+// Device staging slots of the host path: a ring (chunk c uses slot c % kHostSlots), so the device holds
+// kHostSlots chunks -- one arriving, one computing, one leaving -- not the whole batch.
+constexpr int kHostSlots = 3;
+int dtype_size(int dtype) { return dtype == rnnt::kF32 ? 4 : 2; }
+
+// Per-host-thread, per-device cache of the host path's copy streams and events (created once: creating them
+// per call cost tens of microseconds of host time).
+struct HostPool {
+    bool ready = false;
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t start = nullptr, done = nullptr;
+    cudaEvent_t in[kHostSlots] = {}, computed[kHostSlots] = {}, out[kHostSlots] = {};
+};
+thread_local HostPool t_host_pools[64];
+
+HostPool* host_pool() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    HostPool& hp = t_host_pools[dev];
+    if (hp.ready) return &hp;
+    auto ev = [](cudaEvent_t* e) { return cudaEventCreateWithFlags(e, cudaEventDisableTiming) == cudaSuccess; };
+    if (cudaStreamCreateWithFlags(&hp.h2d, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&hp.d2h, cudaStreamNonBlocking) != cudaSuccess || !ev(&hp.start) || !ev(&hp.done))
+        return nullptr;
+    for (int k = 0; k < kHostSlots; ++k)
+        if (!ev(&hp.in[k]) || !ev(&hp.computed[k]) || !ev(&hp.out[k])) return nullptr;
+    hp.ready = true;
+    return &hp;
+}
 
 }  // namespace
 
@@ -266,41 +295,53 @@ rnnt_status rnnt_loss_sum(const float* losses, int B, double* loss_sum, void* st
     return RNNT_OK;
 }
 
-// Device buffer of the host path: [logits/grads staging B*cells*V fp32][targets][T_b][U_b][losses]
-// [workspace for one chunk per chunk slot].  All 256-byte aligned.
-size_t rnnt_host_buffer_bytes(int B, int Tmax, int Umax, int V) {
+// Device buffer of the host path: [kHostSlots staging slots of C utterances' logits / grads][targets][T_b][U_b]
+// [losses][one chunk workspace per slot].  All 256-byte aligned.
+size_t rnnt_host_buffer_bytes_ex(int B, int Tmax, int Umax, int V, rnnt_dtype dtype) {
     if (check_sizes(B, Tmax, Umax, V, 0) != RNNT_OK) return 0;
+    if (dtype != RNNT_F32 && dtype != RNNT_F16 && dtype != RNNT_BF16) return 0;
     const int64_t cells = static_cast<int64_t>(Tmax) * (Umax + 1);
     const int C = host_chunk(B);
-    const int nchunks = (B + C - 1) / C;
+    const int slots = std::min(kHostSlots, (B + C - 1) / C);
     size_t s = 0;
-    s += rnnt::align256(sizeof(float) * B * cells * V);
+    s += static_cast<size_t>(std::max(slots, 1)) * rnnt::align256(static_cast<size_t>(dtype_size(dtype)) * C * cells * V);
     s += rnnt::align256(sizeof(int32_t) * B * std::max(Umax, 1));
     s += 2 * rnnt::align256(sizeof(int32_t) * B);
     s += rnnt::align256(sizeof(float) * B);
-    s += static_cast<size_t>(nchunks) * rnnt::workspace_bytes(C, Tmax, Umax);
+    s += static_cast<size_t>(std::max(slots, 1)) * rnnt::workspace_bytes(C, Tmax, Umax);
     return s;
 }
 
-rnnt_status rnnt_loss_host(const float* logits_host, const int32_t* targets_host, const int32_t* logit_lens_host,
-                           const int32_t* target_lens_host, int B, int Tmax, int Umax, int V, int blank,
-                           int variant, float* losses_host, float* grads_host, void* device_buffer,
-                           size_t device_buffer_bytes, void* stream) {
+size_t rnnt_host_buffer_bytes(int B, int Tmax, int Umax, int V) {
+    return rnnt_host_buffer_bytes_ex(B, Tmax, Umax, V, RNNT_F32);
+}
+
+rnnt_status rnnt_loss_host_ex(const void* logits_host, rnnt_dtype dtype, const int32_t* targets_host,
+                              const int32_t* logit_lens_host, const int32_t* target_lens_host, int B, int Tmax,
+                              int Umax, int V, int blank, int variant, float* losses_host, void* grads_host,
+                              void* device_buffer, size_t device_buffer_bytes, void* stream) {
     rnnt_status st = check_sizes(B, Tmax, Umax, V, blank);
     if (st != RNNT_OK) return st;
     if (variant < -1 || variant > 1) return RNNT_ERR_INVALID_ARG;
+    if (dtype != RNNT_F32 && dtype != RNNT_F16 && dtype != RNNT_BF16) return RNNT_ERR_INVALID_ARG;
     if (B == 0) return RNNT_OK;
     if (!logits_host || !logit_lens_host || !target_lens_host || !losses_host || !device_buffer)
         return RNNT_ERR_INVALID_ARG;
     if (Umax > 0 && !targets_host) return RNNT_ERR_INVALID_ARG;
-    if (device_buffer_bytes < rnnt_host_buffer_bytes(B, Tmax, Umax, V)) return RNNT_ERR_WORKSPACE_TOO_SMALL;
+    if (device_buffer_bytes < rnnt_host_buffer_bytes_ex(B, Tmax, Umax, V, dtype)) return RNNT_ERR_WORKSPACE_TOO_SMALL;
+    HostPool* hp = host_pool();
+    if (!hp) return RNNT_ERR_CUDA;
     const int kind = (variant < 0) ? rnnt::kRnnt : (variant == 0 ? rnnt::kForceFinal : rnnt::kAllowIgnore);
-
+    const int es = dtype_size(dtype);
     const int64_t cells = static_cast<int64_t>(Tmax) * (Umax + 1);
-    const int64_t utt_elems = cells * V;
+    const int64_t utt_bytes = cells * V * es;
+    const int C = host_chunk(B);
+    const int nchunks = (B + C - 1) / C;
+    const int slots = std::min(kHostSlots, nchunks);
+    const size_t slot_bytes = rnnt::align256(static_cast<size_t>(C) * utt_bytes);
     char* p = static_cast<char*>(device_buffer);
-    float* d_logits = reinterpret_cast<float*>(p);
-    p += rnnt::align256(sizeof(float) * B * utt_elems);
+    char* d_stage = p;
+    p += static_cast<size_t>(slots) * slot_bytes;
     int32_t* d_targets = reinterpret_cast<int32_t*>(p);
     p += rnnt::align256(sizeof(int32_t) * B * std::max(Umax, 1));
     int32_t* d_T = reinterpret_cast<int32_t*>(p);
@@ -309,83 +350,54 @@ rnnt_status rnnt_loss_host(const float* logits_host, const int32_t* targets_host
     p += rnnt::align256(sizeof(int32_t) * B);
     float* d_losses = reinterpret_cast<float*>(p);
     p += rnnt::align256(sizeof(float) * B);
-    const int C = host_chunk(B);
-    const int nchunks = (B + C - 1) / C;
     const size_t ws_chunk = rnnt::workspace_bytes(C, Tmax, Umax);
+    const char* lh = static_cast<const char*>(logits_host);
+    char* gh = static_cast<char*>(grads_host);
 
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    cudaStream_t h2d = nullptr, d2h = nullptr;
-    cudaEvent_t ev_start = nullptr, ev_done = nullptr;
-    cudaEvent_t* ev_in = new cudaEvent_t[nchunks]();
-    cudaEvent_t* ev_out = new cudaEvent_t[nchunks]();
-    rnnt_status ret = RNNT_OK;
-    auto ok = [&](cudaError_t e) {
-        if (e != cudaSuccess && ret == RNNT_OK) ret = RNNT_ERR_CUDA;
-        return e == cudaSuccess;
-    };
-    do {
-        if (!ok(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking))) break;
-        if (!ok(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking))) break;
-        if (!ok(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming))) break;
-        if (!ok(cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming))) break;
-        bool good = true;
-        for (int c = 0; c < nchunks && good; ++c)
-            good = ok(cudaEventCreateWithFlags(&ev_in[c], cudaEventDisableTiming)) &&
-                   ok(cudaEventCreateWithFlags(&ev_out[c], cudaEventDisableTiming));
-        if (!good) break;
-        // Small inputs first, on the caller's stream; the copy streams start after prior work on it.
-        if (!ok(cudaEventRecord(ev_start, s))) break;
-        if (!ok(cudaStreamWaitEvent(h2d, ev_start, 0))) break;
-        if (!ok(cudaStreamWaitEvent(d2h, ev_start, 0))) break;
-        if (Umax > 0 && !ok(cudaMemcpyAsync(d_targets, targets_host, sizeof(int32_t) * B * Umax,
-                                            cudaMemcpyHostToDevice, s)))
-            break;
-        if (!ok(cudaMemcpyAsync(d_T, logit_lens_host, sizeof(int32_t) * B, cudaMemcpyHostToDevice, s))) break;
-        if (!ok(cudaMemcpyAsync(d_U, target_lens_host, sizeof(int32_t) * B, cudaMemcpyHostToDevice, s))) break;
-        // H2D(c) on h2d  ->  K1..K3(c) on s  ->  D2H(c) on d2h; chunks own disjoint staging, so no WAR hazards.
-        for (int c = 0; c < nchunks && good; ++c) {
-            const int b0 = c * C, nb = std::min(C, B - b0);
-            const size_t bytes = sizeof(float) * nb * utt_elems;
-            good = ok(cudaMemcpyAsync(d_logits + b0 * utt_elems, logits_host + b0 * utt_elems, bytes,
-                                      cudaMemcpyHostToDevice, h2d)) &&
-                   ok(cudaEventRecord(ev_in[c], h2d));
-        }
-        for (int c = 0; c < nchunks && good; ++c) {
-            const int b0 = c * C, nb = std::min(C, B - b0);
-            good = ok(cudaStreamWaitEvent(s, ev_in[c], 0));
-            if (!good) break;
-            void* ws = p + static_cast<size_t>(c) * ws_chunk;
-            float* zc = d_logits + b0 * utt_elems;
-            rnnt_status r = run(zc, rnnt::kF32, d_targets + static_cast<int64_t>(b0) * Umax, d_T + b0, d_U + b0,
-                                nb, Tmax, Umax, V, blank, d_losses + b0, grads_host ? zc : nullptr, nullptr, ws,
-                                ws_chunk, s, kind);
-            if (r != RNNT_OK) {
-                ret = r;
-                good = false;
-                break;
-            }
-            good = ok(cudaEventRecord(ev_out[c], s)) && ok(cudaStreamWaitEvent(d2h, ev_out[c], 0));
-            if (good && grads_host)
-                good = ok(cudaMemcpyAsync(grads_host + b0 * utt_elems, zc, sizeof(float) * nb * utt_elems,
-                                          cudaMemcpyDeviceToHost, d2h));
-        }
-        if (!good) break;
-        if (!ok(cudaMemcpyAsync(losses_host, d_losses, sizeof(float) * B, cudaMemcpyDeviceToHost, s))) break;
-        if (!ok(cudaEventRecord(ev_done, d2h))) break;
-        ok(cudaStreamWaitEvent(s, ev_done, 0));
-    } while (false);
-    // Destroying streams/events with pending work is legal: resources are released on completion.
+    auto ok = [](cudaError_t e) { return e == cudaSuccess; };
+    // The copy streams start after prior work on the caller's stream; small inputs go first, on s.
+    if (!ok(cudaEventRecord(hp->start, s)) || !ok(cudaStreamWaitEvent(hp->h2d, hp->start, 0)) ||
+        !ok(cudaStreamWaitEvent(hp->d2h, hp->start, 0)))
+        return RNNT_ERR_CUDA;
+    if (Umax > 0 && !ok(cudaMemcpyAsync(d_targets, targets_host, sizeof(int32_t) * B * Umax, cudaMemcpyHostToDevice, s)))
+        return RNNT_ERR_CUDA;
+    if (!ok(cudaMemcpyAsync(d_T, logit_lens_host, sizeof(int32_t) * B, cudaMemcpyHostToDevice, s)) ||
+        !ok(cudaMemcpyAsync(d_U, target_lens_host, sizeof(int32_t) * B, cudaMemcpyHostToDevice, s)))
+        return RNNT_ERR_CUDA;
+    // Chunk c, slot k = c % slots:  H2D(c) on h2d (after D2H(c - slots) has drained slot k)  ->  K1..K3(c) on
+    // s (in place)  ->  D2H(c) on d2h.  The three streams pipeline H2D(c+1), compute(c) and D2H(c-1).
     for (int c = 0; c < nchunks; ++c) {
-        if (ev_in[c]) cudaEventDestroy(ev_in[c]);
-        if (ev_out[c]) cudaEventDestroy(ev_out[c]);
+        const int k = c % slots, b0 = c * C, nb = std::min(C, B - b0);
+        char* slot = d_stage + static_cast<size_t>(k) * slot_bytes;
+        const size_t bytes = static_cast<size_t>(nb) * utt_bytes;
+        if (c >= slots && !ok(cudaStreamWaitEvent(hp->h2d, hp->out[k], 0))) return RNNT_ERR_CUDA;
+        if (!ok(cudaMemcpyAsync(slot, lh + b0 * utt_bytes, bytes, cudaMemcpyHostToDevice, hp->h2d)) ||
+            !ok(cudaEventRecord(hp->in[k], hp->h2d)) || !ok(cudaStreamWaitEvent(s, hp->in[k], 0)))
+            return RNNT_ERR_CUDA;
+        void* ws = p + static_cast<size_t>(k) * ws_chunk;
+        const rnnt_status r = run(slot, static_cast<int>(dtype), d_targets + static_cast<int64_t>(b0) * Umax, d_T + b0,
+                                  d_U + b0, nb, Tmax, Umax, V, blank, d_losses + b0, grads_host ? slot : nullptr,
+                                  nullptr, ws, ws_chunk, s, kind);
+        if (r != RNNT_OK) return r;
+        if (!ok(cudaEventRecord(hp->computed[k], s)) || !ok(cudaStreamWaitEvent(hp->d2h, hp->computed[k], 0)))
+            return RNNT_ERR_CUDA;
+        if (grads_host && !ok(cudaMemcpyAsync(gh + b0 * utt_bytes, slot, bytes, cudaMemcpyDeviceToHost, hp->d2h)))
+            return RNNT_ERR_CUDA;
+        if (!ok(cudaEventRecord(hp->out[k], hp->d2h))) return RNNT_ERR_CUDA;
     }
-    delete[] ev_in;
-    delete[] ev_out;
-    if (ev_start) cudaEventDestroy(ev_start);
-    if (ev_done) cudaEventDestroy(ev_done);
-    if (h2d) cudaStreamDestroy(h2d);
-    if (d2h) cudaStreamDestroy(d2h);
-    return ret;
+    if (!ok(cudaMemcpyAsync(losses_host, d_losses, sizeof(float) * B, cudaMemcpyDeviceToHost, s)) ||
+        !ok(cudaEventRecord(hp->done, hp->d2h)) || !ok(cudaStreamWaitEvent(s, hp->done, 0)))
+        return RNNT_ERR_CUDA;
+    return RNNT_OK;
+}
+
+rnnt_status rnnt_loss_host(const float* logits_host, const int32_t* targets_host, const int32_t* logit_lens_host,
+                           const int32_t* target_lens_host, int B, int Tmax, int Umax, int V, int blank,
+                           int variant, float* losses_host, float* grads_host, void* device_buffer,
+                           size_t device_buffer_bytes, void* stream) {
+    return rnnt_loss_host_ex(logits_host, RNNT_F32, targets_host, logit_lens_host, target_lens_host, B, Tmax, Umax, V,
+                             blank, variant, losses_host, grads_host, device_buffer, device_buffer_bytes, stream);
 }
 
 const char* rnnt_status_string(rnnt_status status) {

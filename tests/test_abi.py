@@ -28,7 +28,8 @@ def _declared_functions():
 def test_header_declares_expected_entry_points():
     names = _declared_functions()
     for n in ("rnnt_loss", "wrnnt_loss", "rnnt_workspace_bytes", "rnnt_status_string", "rnnt_loss_sum",
-              "rnnt_loss_host", "rnnt_host_buffer_bytes", "rnnt_version"):
+              "rnnt_loss_host", "rnnt_host_buffer_bytes", "rnnt_loss_host_ex", "rnnt_host_buffer_bytes_ex",
+              "rnnt_version"):
         assert n in names
 
 

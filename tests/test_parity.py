@@ -329,3 +329,27 @@ def test_host_path_matches_device_path(rb, variant):
     lh, gh = rb.rnnt_loss_host(zh, th, Th, Uh, pb["blank"], variant, grads_host=gh)
     torch.cuda.synchronize()
     assert np.array_equal(lh.numpy().astype(np.float64), l_dev) and np.array_equal(gh.numpy(), g_dev)
+
+
+@pytest.mark.parametrize("dtype", (torch.bfloat16, torch.float16), ids=("bf16", "f16"))
+def test_host_path_16bit_and_ring_reuse(rb, dtype):
+    """16-bit host buffers (half the PCIe bytes): equal bit for bit to the device path on the same 16-bit
+    logits; 11 utterances = 11 chunks through the 3-slot device ring (every slot reused); a second call on the
+    same buffers gives the same bits (the cached copy streams and events carry no state between calls)."""
+    cfg = workloads.random_config(11, 45, 14, 200, seed=19, variant="force_final")
+    pb = workloads.problem(cfg)
+    z16 = pb["logits"].to(dtype)
+    l_dev, g_dev = rb.wrnnt_loss(z16.cuda(), pb["targets"], pb["logit_lens"], pb["target_lens"], pb["blank"],
+                                 "force_final")
+    torch.cuda.synchronize()
+    zh = z16.pin_memory()
+    th = torch.from_numpy(pb["targets"]).pin_memory()
+    Th = torch.from_numpy(pb["logit_lens"]).pin_memory()
+    Uh = torch.from_numpy(pb["target_lens"]).pin_memory()
+    buf = torch.empty(rb.rnnt_host_buffer_bytes(11, 45, 14, 200, dtype), dtype=torch.uint8, device="cuda")
+    assert buf.numel() < 11 * 45 * 15 * 200 * 2  # the ring holds 3 chunks, not the batch
+    for _ in range(2):
+        gh = torch.empty_like(zh).pin_memory()
+        lh, gh = rb.rnnt_loss_host(zh, th, Th, Uh, pb["blank"], "force_final", grads_host=gh, device_buffer=buf)
+        torch.cuda.synchronize()
+        assert torch.equal(lh, l_dev.cpu()) and torch.equal(gh, g_dev.cpu())
