@@ -125,6 +125,19 @@ __device__ __forceinline__ float2 tanh2_mufu(float x0, float x1) {
     const float2 d = upk(fadd2(pk(ex2(y.x), ex2(y.y)), pk(1.f, 1.f)));
     return upk(ffma2(pk(rcp_approx(d.x), rcp_approx(d.y)), pk(-2.f, -2.f), pk(1.f, 1.f)));
 }
+// Opt-in builders' tanh (RNNT_K6_FAST_TANH=1): one MUFU op per element (tanh.approx.f32, relative error ~2^-11)
+// instead of two (ex2 + rcp, tanh2_mufu).  At the paper's shapes (V = 500: 4 N tiles per row tile) the two MUFU
+// ops per element make K6 MUFU-bound: p124 forward 0.457 -> 0.366 ms, c3 1.391 -> 1.332 ms (A/B, one box).  But
+// h = bf16(tanh) then differs from R22's bf16 of the exact tanh by one bf16 ulp far more often (wherever tanh
+// lies within ~2^-11 of a bf16 rounding boundary, against ~2e-7 for tanh2_mufu): losses moved 1.3e-7 .. 1.8e-7
+// relative at p124 / c3, but 1.2e-5 on 300 short utterances at H = 128 (test_joint_many_short_utterances, bar
+// 1e-5) -- so it is not the default.
+__device__ __forceinline__ float2 tanh2_approx(float x0, float x1) {
+    float y0, y1;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(y0) : "f"(x0));
+    asm("tanh.approx.f32 %0, %1;" : "=f"(y1) : "f"(x1));
+    return make_float2(y0, y1);
+}
 // z[k] for a per-lane k in [0, 32) without local memory: a 5-level select tree (31 FSEL) instead of 32
 // compare-and-move pairs.
 __device__ __forceinline__ float select32(const float (&z)[32], int k) {
@@ -153,7 +166,7 @@ struct JointArgs {
     const int* nrows;   // number of valid cells (compact rows)
     int dbg;  // diagnostics (env RNNT_K6_DEBUG, never set in production): 1 = builders skip tanh,
               // 2 = epilogue skips its math (both give wrong losses: timing ablations only), 4 = per-role
-              // barrier-wait cycle counters printed to stderr
+              // barrier-wait cycle counters printed to stderr, 8 = tanh.approx builders (RNNT_K6_FAST_TANH=1)
     unsigned long long* prof;
     float* lse_out;
     double2* lp_out;
@@ -606,7 +619,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
             }
             // items = 32 nch is a multiple of 4 * 32 (nch in {8, 16, 24, 32}): every batch is full
             // fast: the tile has no rows past the end and no diagnostics -> no per-item / per-word selects
-            const bool fast = (tile + 1) * kRowsPerTile <= rows && a.dbg == 0;
+            const bool fast = (tile + 1) * kRowsPerTile <= rows && (a.dbg & ~8) == 0;
             auto batch = [&](const int (&rows_)[4], const int (&cs)[4], auto fast_c) {
                 constexpr bool kFast = decltype(fast_c)::value;
                 uint4 fa[4], ga[4];
@@ -630,7 +643,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
                     for (int e = 0; e < 4; ++e) {
                         const float2 x = unpack_bf16x2(fw[e]), y = unpack_bf16x2(gw[e]);
                         const float2 xs = upk(fadd2(pk(x.x, x.y), pk(y.x, y.y)));
-                        const float2 h = tanh2_mufu(xs.x, xs.y);
+                        const float2 h = (a.dbg & 8) ? tanh2_approx(xs.x, xs.y) : tanh2_mufu(xs.x, xs.y);
                         ow[e] = kFast ? pack_bf16x2(h.x, h.y)
                                       : !ok[j] ? 0u : (a.dbg & 1) ? (fw[e] ^ gw[e]) : pack_bf16x2(h.x, h.y);
                     }
@@ -904,6 +917,7 @@ rnnt_status joint_front(const void* enc, const void* pred, const void* weight, c
         args.h_out = g->h;
     }
     if (const char* e = getenv("RNNT_K6_DEBUG")) args.dbg = atoi(e);
+    if (const char* e = getenv("RNNT_K6_FAST_TANH")) args.dbg |= atoi(e) ? 8 : 0;
     args.prof = nullptr;
     if (args.dbg & 4) cudaMalloc(&args.prof, sizeof(unsigned long long) * 8 * nsm);
     const int64_t ntiles = (args.rows + kRowsPerTile - 1) / kRowsPerTile;
