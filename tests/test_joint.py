@@ -219,6 +219,38 @@ def test_joint_loss_grad_matches_oracle(rb, shape, variant):
     assert_grads_r23(out, enc, pred, W, b, y, T_b, U_b, 0, variant, tag=f"{shape} {variant}")
 
 
+@pytest.mark.parametrize("shape", [(2, 11, 5, 384, 200), (3, 13, 4, 256, 37), (2, 17, 6, 512, 300),
+                                   (5, 29, 9, 128, 130)],
+                         ids=lambda s: "B{}_T{}_U{}_H{}_V{}".format(*s))
+def test_joint_grad_backward_gemm_shapes(rb, shape):
+    """The backward GEMMs' edge shapes: H = 384 (K8's N chunks 256 + 128, K9's 3 h boxes per CTA), V = 37 and
+    V = 130 (one / three 128-v tiles: K9's pair with an idle odd CTA; K8's last K block partly past V), V = 300
+    (Vp = 384), a row count that is not a multiple of K8's 256-row pair tile or K9's 64-row stage."""
+    B, T, U, H, V = shape
+    cfg = workloads.random_config(B, T, U, V, seed=sum(shape) % 83 + 5, variant="allow_ignore")
+    T_b, U_b = workloads.lengths(cfg)
+    y = workloads.targets(cfg, U_b)
+    enc, pred, W, b = workloads.joint_inputs(B, T, U, H, V, seed=sum(shape) % 83 + 5)
+    out = rb.rnnt_joint_loss_grad(enc.cuda(), pred.cuda(), W.cuda(), b.cuda(), y, T_b, U_b, 0, "allow_ignore")
+    torch.cuda.synchronize()
+    ref_l = oj.joint_loss(*_np(enc, pred, W, b), y, T_b, U_b, 0, "allow_ignore")
+    l = out[0].cpu().numpy().astype(np.float64)
+    assert (np.abs(l - ref_l) / np.maximum(np.abs(ref_l), 1.0)).max() <= 1e-5
+    assert_grads_r23(out, enc, pred, W, b, y, T_b, U_b, 0, "allow_ignore", tag=f"gemm {shape}")
+
+
+def test_joint_grad_no_valid_rows(rb):
+    """Every utterance invalid (T_b > Tmax): no GEMM rows at all -- NaN losses, every gradient exactly zero."""
+    H, V = 128, 130
+    enc, pred, W, b = workloads.joint_inputs(2, 4, 2, H, V, seed=61)
+    out = rb.rnnt_joint_loss_grad(enc.cuda(), pred.cuda(), W.cuda(), b.cuda(), np.array([[1, 2], [3, 4]], np.int32),
+                                  np.array([5, 9], np.int32), np.array([2, 2], np.int32), 0, "rnnt")
+    torch.cuda.synchronize()
+    assert torch.isnan(out[0]).all()
+    for g in out[1:]:
+        assert not g.any()
+
+
 def test_joint_edge_cases(rb):
     """T = 1, U = 0 and an invalid length in one batch; B = 0 is a no-op."""
     H, V = 128, 128
