@@ -177,6 +177,101 @@ __global__ void __launch_bounds__(256, 1) k7_reduce(const __nv_bfloat16* __restr
     }
 }
 
+// K7, pass 1, frame-per-warp form (k7_reduce_f; the default): block (chunk, b, slice) as k7_reduce, but warp w
+// owns FRAME t0 + w and walks every unit: its d enc(b, t0 + w) partial is complete in 8 registers, and the 8
+// warps' dpre rows of each unit are summed into the chunk's d pred partial through shared memory (groups of
+// kG units: one barrier to publish, one to release; a fixed summation order: deterministic).  The next group's
+// rows are loaded while the current one is combined, and ~90 registers allow 2 blocks per SM, so far more of
+// each SM's bytes are in flight than with k7_reduce's 204-register warps.
+constexpr int kG = 4;
+
+template <bool kPre>
+__global__ void __launch_bounds__(256, 2) k7_reduce_f(const __nv_bfloat16* __restrict__ dx,
+                                                      const __nv_bfloat16* __restrict__ h,
+                                                      const int32_t* __restrict__ T_b, const int32_t* __restrict__ U_b,
+                                                      int B, int Tmax, int Umax, int H, float* __restrict__ d_enc,
+                                                      float* __restrict__ part) {
+    __shared__ int s_part[8];
+    __shared__ float4 s_row[kG][8][2][32];  // [unit in group][warp][half of the 8 columns][lane]
+    const int chunk = blockIdx.x, b = blockIdx.y;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int off = utt_offset(T_b, U_b, b, Tmax, Umax, s_part);
+    const int n = utt_count(T_b, U_b, b, Tmax, Umax);
+    const int T = n ? T_b[b] : 0, U = n ? U_b[b] : -1;
+    const int t0 = chunk * kTC, t = t0 + warp;
+    const bool frame_in = t < T;
+    const int c = blockIdx.z * 256 + lane * 8;
+    const bool col_in = c < H;
+    const bool ld = frame_in && col_in;
+    const int64_t rbase = off + static_cast<int64_t>(t) * (U + 1);  // row of (t, u = 0)
+    float enc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    uint4 dv[kG], hv[kG];
+    auto load = [&](int u0) {
+#pragma unroll
+        for (int j = 0; j < kG; ++j) {
+            const int u = u0 + j;
+            if (ld && u <= U) {
+                const int64_t r = rbase + u;
+                dv[j] = __ldcs(reinterpret_cast<const uint4*>(dx + r * H + c));
+                if (!kPre) hv[j] = __ldcs(reinterpret_cast<const uint4*>(h + r * H + c));
+            } else {
+                dv[j] = make_uint4(0u, 0u, 0u, 0u);  // bf16 zeros: contributes 0
+                if (!kPre) hv[j] = make_uint4(0u, 0u, 0u, 0u);
+            }
+        }
+    };
+    const bool any = (T > t0) && U >= 0;  // block-uniform: the chunk has frames
+    if (any) load(0);
+    for (int u0 = 0; any && u0 <= U; u0 += kG) {
+        float d[kG][8];
+#pragma unroll
+        for (int j = 0; j < kG; ++j) {
+            const uint32_t dw[4] = {dv[j].x, dv[j].y, dv[j].z, dv[j].w};
+            uint32_t hw[4] = {0u, 0u, 0u, 0u};
+            if (!kPre) hw[0] = hv[j].x, hw[1] = hv[j].y, hw[2] = hv[j].z, hw[3] = hv[j].w;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                float2 x = unpack_bf16x2(dw[e]);
+                if (!kPre) {
+                    const float2 hh = unpack_bf16x2(hw[e]);
+                    x = upk(fmul2(pk(x.x, x.y), ffma2(pk(-hh.x, -hh.y), pk(hh.x, hh.y), pk(1.f, 1.f))));
+                }
+                d[j][2 * e] = x.x;
+                d[j][2 * e + 1] = x.y;
+                enc[2 * e] += x.x;
+                enc[2 * e + 1] += x.y;
+            }
+        }
+        if (u0 + kG <= U) load(u0 + kG);  // the next group's rows in flight while this one is combined
+#pragma unroll
+        for (int j = 0; j < kG; ++j) {
+            s_row[j][warp][0][lane] = make_float4(d[j][0], d[j][1], d[j][2], d[j][3]);
+            s_row[j][warp][1][lane] = make_float4(d[j][4], d[j][5], d[j][6], d[j][7]);
+        }
+        __syncthreads();
+        // thread -> (unit j = warp / 2, half = warp & 1, lane): sums the 8 frames' rows in warp order
+        {
+            const int j = warp >> 1, hf = warp & 1;
+            const int u = u0 + j;
+            if (u <= U && col_in) {
+                float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int w = 0; w < 8; ++w) {
+                    const float4 x = s_row[j][w][hf][lane];
+                    o.x += x.x, o.y += x.y, o.z += x.z, o.w += x.w;
+                }
+                reinterpret_cast<float4*>(part + ((static_cast<int64_t>(chunk) * B + b) * (Umax + 1) + u) * H + c)[hf] = o;
+            }
+        }
+        __syncthreads();
+    }
+    if (col_in && t < Tmax) {
+        float4* o = reinterpret_cast<float4*>(d_enc + (static_cast<int64_t>(b) * Tmax + t) * H + c);
+        o[0] = frame_in ? make_float4(enc[0], enc[1], enc[2], enc[3]) : make_float4(0.f, 0.f, 0.f, 0.f);
+        o[1] = frame_in ? make_float4(enc[4], enc[5], enc[6], enc[7]) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+}
+
 // K7, pass 2: d pred(b, u, :) = sum over the chunks covering frames < T_b of pass 1's partials (chunk order);
 // padded units (and invalid utterances) get 0.  Block (u, b), 128 threads x 4 columns.
 __global__ void __launch_bounds__(128) k7_pred_sum(const float* __restrict__ part, const int32_t* __restrict__ T_b,
@@ -308,10 +403,18 @@ extern "C" rnnt_status rnnt_joint_loss_grad(const void* enc, const void* pred, c
     // be reading dz)
     float* ppart = reinterpret_cast<float*>(ws + L.kpart);
     const dim3 g7((Tmax + kTC - 1) / kTC, B, (H + 255) / 256);
-    if (tanh_k8)
-        k7_reduce<true><<<g7, 256, 0, s>>>(dpre, nullptr, logit_lens, target_lens, B, Tmax, Umax, H, d_enc, ppart);
-    else
-        k7_reduce<false><<<g7, 256, 0, s>>>(dpre, hb, logit_lens, target_lens, B, Tmax, Umax, H, d_enc, ppart);
+    const bool k7_units = getenv("RNNT_K7_UNITS") && atoi(getenv("RNNT_K7_UNITS")) != 0;  // A/B: unit-per-warp K7
+    if (k7_units) {
+        if (tanh_k8)
+            k7_reduce<true><<<g7, 256, 0, s>>>(dpre, nullptr, logit_lens, target_lens, B, Tmax, Umax, H, d_enc, ppart);
+        else
+            k7_reduce<false><<<g7, 256, 0, s>>>(dpre, hb, logit_lens, target_lens, B, Tmax, Umax, H, d_enc, ppart);
+    } else {
+        if (tanh_k8)
+            k7_reduce_f<true><<<g7, 256, 0, s>>>(dpre, nullptr, logit_lens, target_lens, B, Tmax, Umax, H, d_enc, ppart);
+        else
+            k7_reduce_f<false><<<g7, 256, 0, s>>>(dpre, hb, logit_lens, target_lens, B, Tmax, Umax, H, d_enc, ppart);
+    }
     k7_pred_sum<<<dim3(Umax + 1, B), 128, 0, s>>>(ppart, logit_lens, target_lens, B, Tmax, Umax, H, d_pred);
     if (cudaGetLastError() != cudaSuccess) return RNNT_ERR_CUDA;
     if (pool && cudaStreamWaitEvent(s, pool->k2_done[0], 0) != cudaSuccess) return RNNT_ERR_CUDA;  // join K9
