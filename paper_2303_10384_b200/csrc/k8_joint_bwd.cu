@@ -145,6 +145,57 @@ __device__ __forceinline__ void k8_epilogue(uint32_t lane_base, int64_t row_w, i
     }
 }
 
+#define TMEM_LD16(taddr, r)                                                                                     \
+    asm volatile(                                                                                               \
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];" \
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),       \
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]) \
+        : "r"(taddr))
+
+// The pair K8's epilogue for dh (no tanh'): the accumulator is drained FIRST -- all of this warp's 256 columns
+// (or H / 2) loaded 16 at a time and packed to bf16 in 128 registers -- then released to the leader's MMA, and
+// only then staged and stored (as k8_epilogue: 8 whole 64-byte row segments per instruction).  With the stores
+// before the release, the next tile's MMAs waited for the whole epilogue: the single-buffered 128 x 512 fp32
+// accumulator left the tensor pipe ~69 % busy (ncu); the drain itself is short (tcgen05.ld ~700 B/cycle/SM
+// with 8 warps, scripts/micro/tmem_ld.cu).
+template <typename Wait, typename Release>
+__device__ __forceinline__ void k8_epilogue_drain(uint32_t lane_base, int64_t row_w, int64_t R, __nv_bfloat16* dh,
+                                                  int H, int c_lo, int nch, uint32_t stg, int lane, Wait wait_acc,
+                                                  Release release) {
+    const uint32_t so = stg + 2048;
+    const int sr = lane >> 2, sc = lane & 3;
+    auto soff = [](int row, int chunk) { return static_cast<uint32_t>(row * 64 + ((chunk ^ ((row >> 1) & 3)) << 4)); };
+    uint32_t pk16[128];  // this row's (up to) 256 columns in bf16 pairs
+    wait_acc();
+#pragma unroll
+    for (int c16 = 0; c16 < 16; ++c16) {  // 16 loads of 16 columns (nch * 2 of them are real)
+        if (c16 < 2 * nch) {
+            uint32_t r[16];
+            TMEM_LD16(lane_base + c16 * 16, r);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int j = 0; j < 8; ++j) pk16[c16 * 8 + j] = pack_bf16x2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+        }
+    }
+    release();
+#pragma unroll
+    for (int ci = 0; ci < 8; ++ci) {  // 32-column chunks: stage this row, store 8 rows x 64 B per instruction
+        if (ci >= nch) break;
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            st_shared_v4(so + soff(lane, i), make_uint4(pk16[ci * 16 + 4 * i], pk16[ci * 16 + 4 * i + 1],
+                                                         pk16[ci * 16 + 4 * i + 2], pk16[ci * 16 + 4 * i + 3]));
+        __syncwarp();
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+            const int64_t r = row_w + it * 8 + sr;
+            const uint4 v = ld_shared_v4(so + soff(it * 8 + sr, sc));
+            if (r < R) __stcs(reinterpret_cast<uint4*>(dh + r * H + c_lo + ci * 32 + sc * 8), v);
+        }
+    }
+}
+
 // =============================================================================================== K8 (dh)
 // A cluster of kRT x kNH CTAs: kRT consecutive 128-row tiles x kNH parts of H (<= 256 columns each).  CTA (i, j)
 // (rank i * kNH + j) owns row tile i's part j: D = 128 rows x <= 256 columns, two TMEM buffers, so its epilogue
@@ -474,22 +525,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kK8Threads, 1)
         const uint32_t stg = stg0 + (warp - 4) * kK8StgBytes;
         for (int64_t k = 0; k < n_iter; ++k) {
             const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16) + c_lo;
-            k8_epilogue<kTanh>(lane_base, (pr + k * np) * 256 + rank * 128 + q * 32, a.R, a.h, a.Hg, a.dpre, H, c_lo, nch,
-                        stg, lane,
-                        [&]() {
-                            mbar_wait_t(acc_full, static_cast<uint32_t>(k) & 1, pon, w_accfull);
-                            tc_fence_after();
-                        },
-                        [&]() {  // this warp's last load of the accumulator: release it to the leader
-                            tc_fence_before();
-                            __syncwarp();
-                            if (lane == 0) {
-                                if (leader)
-                                    mbar_arrive(acc_empty);
-                                else
-                                    mbar_arrive_remote(acc_empty, 0);
-                            }
-                        });
+            auto wait = [&]() {
+                mbar_wait_t(acc_full, static_cast<uint32_t>(k) & 1, pon, w_accfull);
+                tc_fence_after();
+            };
+            auto release = [&]() {  // this warp's last load of the accumulator: release it to the leader
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if (leader)
+                        mbar_arrive(acc_empty);
+                    else
+                        mbar_arrive_remote(acc_empty, 0);
+                }
+            };
+            const int64_t row_w = (pr + k * np) * 256 + rank * 128 + q * 32;
+            if constexpr (kTanh)
+                k8_epilogue<true>(lane_base, row_w, a.R, a.h, a.Hg, a.dpre, H, c_lo, nch, stg, lane, wait, release);
+            else
+                k8_epilogue_drain(lane_base, row_w, a.R, a.dpre, H, c_lo, nch, stg, lane, wait, release);
         }
     }
     if (pon) {
