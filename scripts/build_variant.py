@@ -16,6 +16,5 @@ for src in b.sources():
     subprocess.run([b.nvcc(), *b.NVCC_FLAGS, *defs, "-c", src, "-o", obj], check=True, capture_output=True)
     objs.append(obj)
 out = os.path.join(b.LIB_DIR, f"librnnt_b200_{tag}.so")
-subprocess.run([b.nvcc(), *b.ARCH, "-shared", "-cudart", "static", "-o", out, *objs, "-lcublas", "-Xlinker",
-                "-rpath,/usr/local/cuda/lib64"], check=True)
+subprocess.run([b.nvcc(), *b.ARCH, "-shared", "-cudart", "static", "-o", out, *objs], check=True)
 print(out)
