@@ -39,7 +39,8 @@
  *     lattice has no path of non-zero probability (e.g. -inf logits) gets loss = +inf and zero grads.
  *   - Argument errors detectable on the host (sizes, null pointers, workspace size, overlap) are returned
  *     as a status before anything is launched.
- *   - Limits: Umax + 1 <= 1024 (one CTA per utterance and direction in the alpha/beta wavefront);
+ *   - Limits: Umax + 1 <= 4096 (one CTA per utterance and direction in the alpha/beta wavefront, up to 8
+ *     columns per thread); rnnt_viterbi / rnnt_joint_viterbi: Umax + 1 <= 1024 (one thread per column);
  *     element offsets are 64-bit (a single call may exceed 2^31 elements).
  */
 #ifndef RNNT_B200_H
@@ -56,7 +57,7 @@ typedef enum {
     RNNT_OK = 0,
     RNNT_ERR_INVALID_ARG = 1,          /* bad size, null pointer, blank out of range, partial overlap */
     RNNT_ERR_WORKSPACE_TOO_SMALL = 2,  /* workspace_bytes < rnnt_workspace_bytes(B, Tmax, Umax) */
-    RNNT_ERR_UNSUPPORTED = 3,          /* Umax + 1 > 1024 */
+    RNNT_ERR_UNSUPPORTED = 3,          /* Umax + 1 > 4096 (> 1024 for Viterbi); fused joint H % 128 != 0 or > 512 */
     RNNT_ERR_CUDA = 4                  /* a CUDA launch / copy failed (cudaGetLastError) */
 } rnnt_status;
 
@@ -119,7 +120,7 @@ rnnt_status rnnt_loss_ex(const void* logits, rnnt_dtype dtype, const int32_t* ta
  *   span      [B][2]     (first, last) frame covered by scored arcs: > 0 / < T_b-1 when the W skips are taken;
  *                        may be NULL.
  * variant: -1 = plain RNN-T, else a wrnnt_variant.  Same inputs, workspace and stream conventions as
- * rnnt_loss_ex; Umax + 1 <= 1024. */
+ * rnnt_loss_ex; Umax + 1 <= 1024 (else RNNT_ERR_UNSUPPORTED). */
 rnnt_status rnnt_viterbi(const void* logits, rnnt_dtype dtype, const int32_t* targets,
                          const int32_t* logit_lens, const int32_t* target_lens, int B, int Tmax, int Umax,
                          int V, int blank, int variant, float* best_logp, int32_t* frames, int32_t* span,

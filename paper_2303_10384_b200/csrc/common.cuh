@@ -10,7 +10,9 @@ namespace rnnt {
 
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
-constexpr int kMaxUp1 = 1024;         // Umax + 1 limit of the one-CTA-per-utterance wavefront
+constexpr int kMaxUp1 = 4096;         // Umax + 1 limit of the one-CTA-per-utterance wavefront (K2: up to 8
+                                      // columns per lane x 512 lanes)
+constexpr int kMaxUp1Viterbi = 1024;  // K4 (forced alignment): one thread per column
 constexpr int kRowWarpsPerBlock = 8;  // K1 / K3: one warp per (b,t,u) row, 8 rows per 256-thread block
 constexpr int kLpPad = 16;            // diagonals of slack before/after the lp array (>= K2 staging group)
 

@@ -250,7 +250,8 @@ void launch_c(const Problem& p, const Workspace& w, cudaStream_t s) {
 // Measured per step on B200 (T=500): one warp, 1 column per lane: 124 ns; one warp, 2 columns per lane:
 // 160 ns; 2-4 warps, 1 column per lane (a named barrier per step): ~200 ns.  So a single warp while
 // kC <= 2 covers the row, then one column per lane across warps; kPf shrinks as the per-thread register
-// budget does (65536 / threads).  RNNT_K2_CELLS=1|2 forces kC where the table allows it (tuning knob).
+// budget does (65536 / threads).  Beyond 1024 columns (long transcripts, U + 1 <= 4096): 512 lanes with 4 or 8
+// columns each, kPf 2 or 1.  RNNT_K2_CELLS=1|2 forces kC where the table allows it (tuning knob).
 template <int kVariant>
 void launch_variant(const Problem& p, const Workspace& w, cudaStream_t s) {
     const int up1 = p.Umax + 1;
@@ -266,8 +267,12 @@ void launch_variant(const Problem& p, const Workspace& w, cudaStream_t s) {
         launch_c<kVariant, 1, 16, 256>(p, w, s);
     else if (up1 <= 512 && force != 2)
         launch_c<kVariant, 1, 8, 512>(p, w, s);
-    else
+    else if (up1 <= 1024)
         launch_c<kVariant, 2, 4, 512>(p, w, s);
+    else if (up1 <= 2048)  // long transcripts: more columns per lane, shallower operand staging (registers)
+        launch_c<kVariant, 4, 2, 512>(p, w, s);
+    else
+        launch_c<kVariant, 8, 1, 512>(p, w, s);
 }
 
 }  // namespace

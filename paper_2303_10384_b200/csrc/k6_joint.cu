@@ -979,6 +979,7 @@ extern "C" rnnt_status rnnt_joint_viterbi(const void* enc, const void* pred, con
     using namespace rnnt;
     if (variant < -1 || variant > 1) return RNNT_ERR_INVALID_ARG;
     if (B > 0 && (!best_logp || (Umax > 0 && !frames))) return RNNT_ERR_INVALID_ARG;
+    if (Umax + 1 > kMaxUp1Viterbi) return RNNT_ERR_UNSUPPORTED;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const rnnt_status st = joint_front(enc, pred, weight, bias, targets, logit_lens, target_lens, B, Tmax, Umax, H, V,
                                        blank, workspace, workspace_bytes, s, nullptr);

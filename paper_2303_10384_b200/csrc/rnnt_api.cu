@@ -275,6 +275,7 @@ rnnt_status rnnt_viterbi(const void* logits, rnnt_dtype dtype, const int32_t* ta
     if (st != RNNT_OK) return st;
     if (variant < -1 || variant > 1) return RNNT_ERR_INVALID_ARG;
     if (dtype != RNNT_F32 && dtype != RNNT_F16 && dtype != RNNT_BF16) return RNNT_ERR_INVALID_ARG;
+    if (Umax + 1 > rnnt::kMaxUp1Viterbi) return RNNT_ERR_UNSUPPORTED;
     if (B == 0) return RNNT_OK;
     if (!logits || !logit_lens || !target_lens || !best_logp || !workspace) return RNNT_ERR_INVALID_ARG;
     if (Umax > 0 && (!targets || !frames)) return RNNT_ERR_INVALID_ARG;
@@ -405,7 +406,9 @@ const char* rnnt_status_string(rnnt_status status) {
         case RNNT_OK: return "RNNT_OK";
         case RNNT_ERR_INVALID_ARG: return "RNNT_ERR_INVALID_ARG: invalid argument";
         case RNNT_ERR_WORKSPACE_TOO_SMALL: return "RNNT_ERR_WORKSPACE_TOO_SMALL: workspace too small";
-        case RNNT_ERR_UNSUPPORTED: return "RNNT_ERR_UNSUPPORTED: Umax + 1 > 1024";
+        case RNNT_ERR_UNSUPPORTED:
+            return "RNNT_ERR_UNSUPPORTED: Umax + 1 > 4096 (1024 for Viterbi), or a fused-joint H that is not a "
+                   "multiple of 128 up to 512";
         case RNNT_ERR_CUDA: return "RNNT_ERR_CUDA: CUDA launch or copy failed";
     }
     return "unknown rnnt_status";

@@ -271,6 +271,28 @@ def test_max_umax_1023(rb):
         _assert_close(*_gpu(rb, pb, variant), *_oracle(pb, variant), "U1023")
 
 
+@pytest.mark.parametrize("shape", [(2, 30, 1500, 12), (2, 20, 2047, 8), (1, 12, 4095, 6)],
+                         ids=lambda s: "B{}_T{}_U{}_V{}".format(*s))
+def test_long_transcripts(rb, shape):
+    """Umax + 1 up to 4096 (SURVEY §5's long-U case): K2 with 4 / 8 columns per lane across 512 lanes; ragged
+    lengths, all variants, against the oracle element by element."""
+    B, T, U, V = shape
+    cfg = workloads.random_config(B, T, U, V, seed=sum(shape) % 97, variable=True)
+    pb = workloads.problem(cfg)
+    for variant in VARIANTS:
+        _assert_close(*_gpu(rb, pb, variant), *_oracle(pb, variant), f"longU {shape} {variant}")
+
+
+def test_limits_are_loud(rb):
+    """Umax + 1 > 4096 (loss) and > 1024 (Viterbi) are refused with RNNT_ERR_UNSUPPORTED, not computed wrong."""
+    z = torch.zeros((1, 2, 4097, 3), device="cuda")
+    with pytest.raises(rb.RnntError, match="UNSUPPORTED"):
+        rb.rnnt_loss(z, np.ones((1, 4096), np.int32), [2], [4096])
+    z = torch.zeros((1, 2, 1025, 3), device="cuda")
+    with pytest.raises(rb.RnntError, match="UNSUPPORTED"):
+        rb.rnnt_viterbi(z, np.ones((1, 1024), np.int32), [2], [1024])
+
+
 def test_empty_batch(rb):
     z = torch.empty((0, 4, 3, 5), device="cuda")
     l, g = rb.rnnt_loss(z, torch.empty((0, 2), dtype=torch.int32), torch.empty(0), torch.empty(0))
