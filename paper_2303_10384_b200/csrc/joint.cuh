@@ -20,16 +20,20 @@ struct GradIO {
     const float* grad_scale;  // [B] or nullptr (= 1): dz of utterance b is scaled by it (e.g. 1/B for a mean)
     __nv_bfloat16* dz;
     __nv_bfloat16* h;
+    bool h_ready;  // h already holds the rows (the forward stored them, joint_front's h_fwd): K6 loads h
+                   // instead of recomputing tanh(f + g); else K6 computes and stores it
 };
 
 // Argument checks, W's tensor map, (optionally) the compact row map, and K6: the forward (-> lse and the
 // Populate gathers in the workspace) when g == nullptr, the backward's first pass (-> dz, h) otherwise.
 // rowmap / nrows: where the row map lives (nullptr: the workspace's alpha / beta regions, free until K2).
+// h_fwd (forward only): the builders also store h = bf16(tanh(f + g)) there ([rows][H], compact rows), for a
+// later K6<grad> with GradIO::h_ready.
 rnnt_status joint_front(const void* enc, const void* pred, const void* weight, const float* bias,
                         const int32_t* targets, const int32_t* logit_lens, const int32_t* target_lens, int B,
                         int Tmax, int Umax, int H, int V, int blank, void* workspace, size_t workspace_bytes,
                         cudaStream_t s, void* const* events, int* rowmap = nullptr, int* nrows = nullptr,
-                        bool make_map = true, const GradIO* g = nullptr);
+                        bool make_map = true, const GradIO* g = nullptr, __nv_bfloat16* h_fwd = nullptr);
 
 // K8 / K9 (k8_joint_bwd.cu): the backward GEMMs on the tensor cores.  K8: out = bf16(dz W) over R rows, or with
 // tanh_in_k8 bf16((dz W) * (1 - h^2)) (the pair kernel; the 2-D cluster A/B kernel always applies it); K9:

@@ -178,13 +178,17 @@ struct JointArgs {
     const double* logp;
     const float* grad_scale;
     __nv_bfloat16* dz_out;  // [rows][Vp] row-major, Vp = V rounded up to whole N tiles (tail columns 0)
-    __nv_bfloat16* h_out;   // [rows][H]
+    __nv_bfloat16* h_out;   // [rows][H]: h stored by the builders (K6<grad>; the training step's forward), or null
+    const __nv_bfloat16* h_in;  // K6<grad> only: [rows][H] h as the forward stored it -- loaded, not recomputed
 };
 
 // kGrad = false: the forward (lse + gathers).  kGrad = true: the backward's first pass -- the same GEMM
 // recomputes z and the epilogue forms dz = softmax(z) (occ_b + occ_y) - [v = blank] occ_b - [v = y] occ_y
-// (K3's formula, with the forward's lse and K2's alpha / beta), stored in bf16 for the two backward GEMMs;
-// the builders also store h.
+// (K3's formula, with the forward's lse and K2's alpha / beta), stored in bf16 for the two backward GEMMs.
+// h = bf16(tanh(f + g)): the builders store it when h_out is set (the training step's forward; or K6<grad>
+// itself), and K6<grad> with h_in loads the forward's rows instead of recomputing them (K6<grad> 601 -> 457 us
+// at p124, 1791 -> 1651 us at c3; the forward +20 us for the stores: the builders' MUFU work was K6<grad>'s
+// limit at p124).
 // kCl = 2: CTA pairs (clusters of 2) share every W stage -- each CTA fetches half of the stage's rows and
 // multicasts it into both CTAs' shared memory (half the W traffic from L2 per SM); the pair walks the same
 // W sequence in lockstep (a stage is refilled once both MMAs released it) and the same number of row tiles
@@ -222,8 +226,8 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
     uint8_t* wst = base;
     uint8_t* stage_a = wst + static_cast<size_t>(a.stages) * kSlot;
     const int Vp = (a.V + kNTile - 1) / kNTile * kNTile;  // V rounded up to whole N tiles
-    // A staging: 128 rows of H + kJointHPad bf16 (the 16-byte pad: conflict-free thread-per-row reads; kGrad: the
-    // rows' first H columns are h's global rows)
+    // A staging: 128 rows of H + kJointHPad bf16 (the 16-byte pad: conflict-free thread-per-row reads; h_in: the
+    // forward's h rows land in the first H columns by one bulk copy each)
     float* sbias = reinterpret_cast<float*>(stage_a + static_cast<size_t>(kRowsPerTile) * (a.H + kJointHPad) * 2);
     float4* xchg = reinterpret_cast<float4*>(sbias + (kSB ? Vp : 0));  // [2][128] epilogue group 1 -> 0 partials
     uint64_t* bars = reinterpret_cast<uint64_t*>(xchg + 2 * kRowsPerTile);
@@ -233,7 +237,8 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
     uint64_t* a_empty = a_full + 1;
     uint64_t* acc_full = a_full + 2;                 // [kAccBufs]
     uint64_t* acc_empty = a_full + 2 + kAccBufs;     // [kAccBufs]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_full + 2 + 2 * kAccBufs);
+    uint64_t* h_full = a_full + 2 + 2 * kAccBufs;    // h_in: the tile's h rows have landed in the staging buffer
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(h_full + 1);
     // kGrad: per epilogue warp, a 32-row x 32-column bf16 dz staging block (2 KB), 16-byte chunks XOR-swizzled
     uint8_t* dzst = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tmem_slot + 4) + 127) & ~uintptr_t(127));
 
@@ -265,6 +270,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
         }
         mbar_init(a_full, kPair ? 256 + 1 : 256);  // pair: + the odd CTA's builders (one remote arrive)
         mbar_init(a_empty, 1);
+        mbar_init(h_full, 1);
         for (int i = 0; i < kAccBufs; ++i) {
             mbar_init(&acc_full[i], 1);
             mbar_init(&acc_empty[i], kPair ? 256 + 8 : 256);  // both epilogue groups (pair: + the odd CTA's 8 warps)
@@ -597,7 +603,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
         const int row_bytes = (H + kJointHPad) * 2;  // +16 B: conflict-free row reads without a swizzle
         uint8_t* my_row = stage_a + static_cast<size_t>(rl) * row_bytes;
         const uint32_t sa_base = smem_u32(stage_a);  // 32-bit shared addresses for the builders' stores
-        const uint4* f4 = reinterpret_cast<const uint4*>(a.f);
+                const uint4* f4 = reinterpret_cast<const uint4*>(a.f);
         const uint4* g4 = reinterpret_cast<const uint4*>(a.g);
         const int items = 32 * nch;        // (row of the quarter, chunk of the half)
         // Row-map entry of this lane's row (q*32 + lane) in a tile, -1 past the end; fetched one build ahead so
@@ -609,10 +615,27 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
             return identity ? static_cast<int>(row) : __ldg(a.rowmap + row);
         };
         int p_next = -1;
+        const bool hstore = a.h_out != nullptr, hload = kGrad && a.h_in != nullptr;
         auto build = [&](int64_t tile, int p) {
-            if constexpr (kGrad) {  // the previous tile's h store must have read the staging buffer
-                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // each thread its own row copies
-                asm volatile("bar.sync 4, 256;" ::: "memory");  // the 8 builder warps
+            if (hload) {
+                // h as the training step's forward stored it: one bulk async copy per row into the staging
+                // buffer (warps 12-15, one row per thread), completing on h_full; no tanh here.  All 8 builder
+                // warps have copied the previous tile from the staging buffer into TMEM (bar.sync) first.
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("bar.sync 4, 256;" ::: "memory");
+                if (warp < 16) {
+                    const int64_t nv = std::max<int64_t>(0, std::min<int64_t>(kRowsPerTile, rows - tile * kRowsPerTile));
+                    if (warp == 12 && lane == 0) mbar_expect_tx(h_full, static_cast<uint32_t>(nv * H * 2));
+                    const int r = (warp - 12) * 32 + lane;
+                    if (r < nv)
+                        asm volatile(
+                            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                                sa_base + static_cast<uint32_t>(r * row_bytes)),
+                            "l"(a.h_in + (tile * kRowsPerTile + r) * H), "r"(static_cast<uint32_t>(H * 2)),
+                            "r"(smem_u32(h_full))
+                            : "memory");
+                }
+                return;
             }
             // lane r: chunk offsets (16-byte units) of row q*32 + r's f and g rows, -1 past the end
             int fo = -1, go = -1;
@@ -658,6 +681,12 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
                     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sa_base + r2 * row_bytes + (cg << 4)),
                                  "r"(ow[0]), "r"(ow[1]), "r"(ow[2]), "r"(ow[3])
                                  : "memory");
+                    // h for K6<grad> / K8 / K9 / K7, straight from registers: a warp's store writes 512 contiguous
+                    // bytes of one row at H = 512 (a bulk copy per row from the staging buffer made the next build
+                    // wait for the copy to read it: p124 forward 495 -> 582 us)
+                    if (hstore && (kFast || ok[j]))
+                        *reinterpret_cast<uint4*>(a.h_out + (tile * kRowsPerTile + r2) * H + cg * 8) =
+                            make_uint4(ow[0], ow[1], ow[2], ow[3]);
                 }
             };
             if (nch == 32) {  // H = 512: lane = chunk, item j of a batch = row i0 / 32 + j
@@ -692,27 +721,6 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
                 }
             }
             __syncwarp();  // each thread copies its own row, written by the whole warp
-            if constexpr (kGrad) {
-                // h for K9 and K7: the staging rows' first H columns ARE h's rows and the tile's rows are
-                // consecutive compact rows; stored at the global stride H by one bulk async copy (TMA engine) per row,
-                // spread over the builder warps
-                // 12-15 (lane l of warp 12 + j takes row 32 j + l: one copy per thread, the issue cost shared)
-                // once all builders have written the tile; it overlaps the TMEM copy and the next build.
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                asm volatile("bar.sync 4, 256;" ::: "memory");
-                if (warp < 16) {  // builder warps 12-15 only: warps 16-19 would issue no copy
-                    const int64_t nv = std::min<int64_t>(kRowsPerTile, rows - tile * kRowsPerTile);
-                    const int r = (warp - 12) * 32 + lane;
-                    if (r < nv) {
-                        __nv_bfloat16* dst = a.h_out + (tile * kRowsPerTile + r) * H;
-                        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
-                                     "r"(smem_u32(stage_a) + static_cast<uint32_t>(r * row_bytes)),
-                                     "r"(static_cast<uint32_t>(H * 2))
-                                     : "memory");
-                    }
-                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                }
-            }
         };
         const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16);
         uint32_t tl = 0;
@@ -724,6 +732,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
         for (int64_t k = 0; k < n_iter; ++k, ++tl) {
             const int64_t tile = bx + k * gridDim.x;
             if (tl > 0) mbar_wait_t(a_empty, (tl - 1) & 1, pon, w_aempty);
+            if (hload) mbar_wait(h_full, tl & 1);
             tc_fence_after();
             // staging -> TMEM: this thread's row, its K half = nch chunks = nch * 4 columns
             for (int c0 = 0; c0 < nch; c0 += 8) {
@@ -763,8 +772,6 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
         if (warp == 8) o[7] = w_accfull;
         if (warp == 12) o[6] = w_aempty;
     }
-    if (kGrad && warp >= 12 && warp < 16)  // the last h stores complete before the CTA's shared memory is released
-        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     tc_fence_before();
     if constexpr (kCl > 1)
         cluster_sync_all();  // no CTA leaves while its partner may still multicast into it
@@ -813,7 +820,7 @@ __global__ void __launch_bounds__(256) k6_rowmap(const int32_t* __restrict__ T_b
 size_t joint_smem_bytes(int H, int V, int stages, bool grad, bool pair) {  // V = 0: bias not staged (!kSB)
     return (grad ? 8 * 2048 + 128 : 0) +  // kGrad: the epilogue warps' dz staging blocks
            1024 + static_cast<size_t>(stages) * (pair ? kStageBytes / 2 : kStageBytes) + static_cast<size_t>(kRowsPerTile) * (H + kJointHPad) * 2 +
-           static_cast<size_t>((V + kNTile - 1) / kNTile * kNTile) * 4 + 2 * kRowsPerTile * 16 + (2 * kMaxStages + 2 + 2 * kAccBufs) * 8 + 16;
+           static_cast<size_t>((V + kNTile - 1) / kNTile * kNTile) * 4 + 2 * kRowsPerTile * 16 + (2 * kMaxStages + 3 + 2 * kAccBufs) * 8 + 16;
 }
 
 using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -856,7 +863,7 @@ rnnt_status joint_front(const void* enc, const void* pred, const void* weight, c
                         const int32_t* targets, const int32_t* logit_lens, const int32_t* target_lens, int B,
                         int Tmax, int Umax, int H, int V, int blank, void* workspace, size_t workspace_bytes,
                         cudaStream_t s, void* const* events, int* rowmap, int* nrows, bool make_map,
-                        const GradIO* g) {
+                        const GradIO* g, __nv_bfloat16* h_fwd) {
     if (B < 0 || Tmax < 1 || Umax < 0 || V < 2 || blank < 0 || blank >= V || H < 1) return RNNT_ERR_INVALID_ARG;
     if (Umax + 1 > kMaxUp1 || H % 128 != 0 || H > 512) return RNNT_ERR_UNSUPPORTED;
     if (B == 0) return RNNT_OK;
@@ -911,7 +918,7 @@ rnnt_status joint_front(const void* enc, const void* pred, const void* weight, c
     JointArgs args{static_cast<const __nv_bfloat16*>(enc), static_cast<const __nv_bfloat16*>(pred), bias, targets,
                    logit_lens, target_lens, B, Tmax, Umax, H, V, blank,
                    static_cast<int64_t>(B) * Tmax * (Umax + 1), stages, rowmap, nrows, 0, nullptr, w.lse, w.lp,
-                   nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+                   nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, h_fwd, nullptr};
     if (g) {
         args.lse_in = g->lse;
         args.lp_in = g->lp;
@@ -920,7 +927,10 @@ rnnt_status joint_front(const void* enc, const void* pred, const void* weight, c
         args.logp = g->logp;
         args.grad_scale = g->grad_scale;
         args.dz_out = g->dz;
-        args.h_out = g->h;
+        if (g->h_ready)
+            args.h_in = g->h;  // stored by the forward: loaded, not recomputed
+        else
+            args.h_out = g->h;
     }
     if (const char* e = getenv("RNNT_K6_DEBUG")) args.dbg = atoi(e);
     if (const char* e = getenv("RNNT_K6_FAST_TANH")) args.dbg |= atoi(e) ? 8 : 0;

@@ -358,15 +358,19 @@ extern "C" rnnt_status rnnt_joint_loss_grad(const void* enc, const void* pred, c
     cudaStream_t s = static_cast<cudaStream_t>(stream);
 
     // forward: K6 (row map into the gradient workspace, which K2 does not touch) and K2 (alpha, beta, losses)
+    // The forward also stores h (bulk copies beside its MUFU-bound builders) so that K6<grad> loads it instead of
+    // recomputing tanh(f + g) (RNNT_K6_HREUSE=0: K6<grad> recomputes and stores h, for A/B).
+    const bool hreuse = !(getenv("RNNT_K6_HREUSE") && atoi(getenv("RNNT_K6_HREUSE")) == 0);
     rnnt_status st = joint_front(enc, pred, weight, bias, targets, logit_lens, target_lens, B, Tmax, Umax, H, V,
-                                 blank, workspace, workspace_bytes, s, nullptr, rowmap, nrows, true, nullptr);
+                                 blank, workspace, workspace_bytes, s, nullptr, rowmap, nrows, true, nullptr,
+                                 hreuse ? hb : nullptr);
     if (st != RNNT_OK) return st;
     const Workspace w = carve(workspace, B, Tmax, Umax);
     const int vk = (variant < 0) ? kRnnt : (variant == WRNNT_FORCE_FINAL ? kForceFinal : kAllowIgnore);
     Problem p{nullptr, targets, logit_lens, target_lens, B, Tmax, Umax, V, blank, vk, losses, nullptr, nullptr, kF32};
     if (launch_k2_alpha_beta(p, w, s) != cudaSuccess) return RNNT_ERR_CUDA;
     // backward pass 1: z again on the tensor cores -> dz (bf16), h
-    const GradIO g{w.lse, w.lp, w.alpha, w.beta, w.logp, grad_scale, dz, hb};
+    const GradIO g{w.lse, w.lp, w.alpha, w.beta, w.logp, grad_scale, dz, hb, hreuse};
     st = joint_front(enc, pred, weight, bias, targets, logit_lens, target_lens, B, Tmax, Umax, H, V, blank,
                      workspace, workspace_bytes, s, nullptr, rowmap, nrows, false, &g);
     if (st != RNNT_OK) return st;
