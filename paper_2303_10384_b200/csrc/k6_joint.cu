@@ -105,6 +105,30 @@ __device__ __forceinline__ void mma_kblock_2sm(uint32_t d_tmem, uint32_t a_tmem,
         "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// The pair K block with A from shared memory too (k6_dz_2sm): both descriptors advance 32 bytes (>> 4 = 2) per K16.
+__device__ __forceinline__ void mma_kblock_ss_2sm(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                                  uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p, q, e;\n"
+        ".reg .b64 a1, a2, a3, b1, b2, b3;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "setp.eq.b32 q, %4, %4;\n"
+        "add.u64 a1, %1, 2;\n"
+        "add.u64 a2, %1, 4;\n"
+        "add.u64 a3, %1, 6;\n"
+        "add.u64 b1, %2, 2;\n"
+        "add.u64 b2, %2, 4;\n"
+        "add.u64 b3, %2, 6;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a1, b1, %3, q;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a2, b2, %3, q;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a3, b3, %3, q;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
 // Instruction descriptor: fp32 D (bits 4-5 = 1), bf16 A (7-9 = 1) and B (10-12 = 1), both K-major,
 // N >> 3 at bits 17-22, M >> 4 at bits 24-28.
 constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(kNTile >> 3) << 17) | (uint32_t(128 >> 4) << 24);
@@ -181,6 +205,101 @@ struct JointArgs {
     __nv_bfloat16* h_out;   // [rows][H]: h stored by the builders (K6<grad>; the training step's forward), or null
     const __nv_bfloat16* h_in;  // K6<grad> only: [rows][H] h as the forward stored it -- loaded, not recomputed
 };
+
+// Per-row scalars of dz for cell (t,u) of utterance b: the occupancies of the two scored arcs leaving it, as K3
+// (k3_grad.cu), times grad_scale[b]; padded rows and invalid / no-path utterances (logP not finite) get gl = false
+// (dz = 0).  lsel = lse log2 e (+inf for an all -inf row: p = 0).
+struct DzRow {
+    bool gl;
+    float sb, sy, lsel;
+    int gy;  // the label column, -1 if none
+};
+__device__ __forceinline__ DzRow dz_row(const JointArgs& a, bool in, int b, int t, int u, int T, int U, bool live,
+                                        int yv, int64_t cells) {
+    DzRow d{false, 0.f, 0.f, INFINITY, -1};
+    const double lP = in ? a.logp[b] : 0.0;
+    d.gl = live && isfinite(lP);
+    if (!d.gl) return d;
+    const int Up1 = a.Umax + 1;
+    const int64_t dcell = (static_cast<int64_t>(b) * (a.Tmax + a.Umax) + (t + u)) * Up1 + u;
+    const float lse = a.lse_in[static_cast<int64_t>(b) * cells + t * Up1 + u];
+    const double2 l = a.lp_in[dcell];
+    const double al = a.alpha[dcell];
+    if (t < T - 1)
+        d.sb = __expf(static_cast<float>(al + l.x + a.beta[dcell + Up1] - lP));
+    else if (u == U)
+        d.sb = __expf(static_cast<float>(al + l.x - lP));
+    if (u < U) {
+        d.sy = __expf(static_cast<float>(al + l.y + a.beta[dcell + Up1 + 1] - lP));
+        d.gy = yv;
+    }
+    if (a.grad_scale) {
+        const float sc = a.grad_scale[b];
+        d.sb *= sc;
+        d.sy *= sc;
+    }
+    d.lsel = (lse == -INFINITY) ? INFINITY : lse * kLog2e;
+    return d;
+}
+
+// One 32-column chunk v0 .. v0 + 31 of this thread's dz row (K3's formula on z = acc + bias, k3_grad.cu):
+// dz = bf16(2^(z log2 e - lse log2 e) gam - [v = blank] sb - [v = y] sy), zeros where the row carries no
+// gradient (!gl).  Through the warp's 2 KB staging block at `st`: each lane writes its row's 4 chunks, then reads
+// back (row = lane / 4 + 8 s, chunk = lane % 4) so that every global store instruction writes 8 whole 64-byte row
+// segments (8 L1 wavefronts instead of 32 for thread-per-row stores).  row0: the compact row of lane 0; rows:
+// the valid rows; ldz: dz's row pitch in elements.
+template <bool kSB>
+__device__ __forceinline__ void dz_chunk(const JointArgs& a, const uint32_t (&r)[32], const float* sbias,
+                                         const float4 (&bq)[8], int v0, bool gl, f32x2 l2, f32x2 nl, f32x2 g2,
+                                         float sb, float sy, int gy, uint32_t st, int lane, int64_t row0,
+                                         int64_t rows, int64_t ldz) {
+    float g[32];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const float4 bb = kSB ? reinterpret_cast<const float4*>(sbias + v0)[j] : bq[j];
+        const f32x2 z0 = fadd2(pk(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1])), pk(bb.x, bb.y));
+        const f32x2 z1 = fadd2(pk(__uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3])), pk(bb.z, bb.w));
+        const float2 p0 = upk(fmul2(ex2x2(ffma2(z0, l2, nl)), g2));
+        const float2 p1 = upk(fmul2(ex2x2(ffma2(z1, l2, nl)), g2));
+        g[4 * j] = p0.x;
+        g[4 * j + 1] = p0.y;
+        g[4 * j + 2] = p1.x;
+        g[4 * j + 3] = p1.y;
+    }
+    if (static_cast<unsigned>(a.blank - v0) < 32u) {  // the arcs' own logits
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            if (v0 + j == a.blank) g[j] -= sb;
+    }
+    if (static_cast<unsigned>(gy - v0) < 32u) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            if (v0 + j == gy) g[j] -= sy;
+    }
+    __syncwarp();  // the previous chunk's reads are done
+#pragma unroll
+    for (int q4 = 0; q4 < 4; ++q4) {
+        const uint32_t w0 = gl ? pack_bf16x2(g[8 * q4 + 0], g[8 * q4 + 1]) : 0u;
+        const uint32_t w1 = gl ? pack_bf16x2(g[8 * q4 + 2], g[8 * q4 + 3]) : 0u;
+        const uint32_t w2 = gl ? pack_bf16x2(g[8 * q4 + 4], g[8 * q4 + 5]) : 0u;
+        const uint32_t w3 = gl ? pack_bf16x2(g[8 * q4 + 6], g[8 * q4 + 7]) : 0u;
+        const uint32_t ad = st + lane * 64u + ((q4 ^ ((lane >> 1) & 3)) << 4);
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(ad), "r"(w0), "r"(w1), "r"(w2), "r"(w3)
+                     : "memory");
+    }
+    __syncwarp();
+#pragma unroll
+    for (int s4 = 0; s4 < 4; ++s4) {
+        const int rr = (lane >> 2) + 8 * s4, kk = lane & 3;
+        uint4 o;
+        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(o.x), "=r"(o.y), "=r"(o.z), "=r"(o.w)
+                     : "r"(st + rr * 64u + ((kk ^ ((rr >> 1) & 3)) << 4))
+                     : "memory");
+        const int64_t orow = row0 + rr;
+        if (orow < rows) *reinterpret_cast<uint4*>(a.dz_out + orow * ldz + v0 + kk * 8) = o;
+    }
+}
 
 // kGrad = false: the forward (lse + gathers).  kGrad = true: the backward's first pass -- the same GEMM
 // recomputes z and the epilogue forms dz = softmax(z) (occ_b + occ_y) - [v = blank] occ_b - [v = y] occ_y
@@ -395,34 +514,10 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
             const bool live = in && t < T && u <= U;
             const int yv = (live && u < U) ? a.targets[static_cast<int64_t>(b) * a.Umax + u] : -1;
             if constexpr (kGrad) {
-                // Per-row occupancies of the two scored arcs leaving (t,u), as K3 (k3_grad.cu): padded rows,
-                // invalid or no-path utterances (logP not finite) get dz = 0.
-                const double lP = in ? a.logp[b] : 0.0;
-                const bool gl = live && isfinite(lP);
-                float gam = 0.f, sb = 0.f, sy = 0.f, lsel = INFINITY;
-                int gy = -1;
-                if (gl) {
-                    const int Up1 = a.Umax + 1;
-                    const int64_t dcell = (static_cast<int64_t>(b) * (a.Tmax + a.Umax) + (t + u)) * Up1 + u;
-                    const float lse = a.lse_in[static_cast<int64_t>(b) * cells + t * Up1 + u];
-                    const double2 l = a.lp_in[dcell];
-                    const double al = a.alpha[dcell];
-                    if (t < T - 1)
-                        sb = __expf(static_cast<float>(al + l.x + a.beta[dcell + Up1] - lP));
-                    else if (u == U)
-                        sb = __expf(static_cast<float>(al + l.x - lP));
-                    if (u < U) {
-                        sy = __expf(static_cast<float>(al + l.y + a.beta[dcell + Up1 + 1] - lP));
-                        gy = yv;
-                    }
-                    if (a.grad_scale) {
-                        const float sc = a.grad_scale[b];
-                        sb *= sc;
-                        sy *= sc;
-                    }
-                    gam = sb + sy;
-                    lsel = (lse == -INFINITY) ? INFINITY : lse * kLog2e;  // an all -inf row: p = 0
-                }
+                const DzRow d = dz_row(a, in, b, t, u, T, U, live, yv, cells);
+                const bool gl = d.gl;
+                const float sb = d.sb, sy = d.sy, gam = d.sb + d.sy, lsel = d.lsel;
+                const int gy = d.gy;
                 const f32x2 l2 = pk(kLog2e, kLog2e), nl = pk(-lsel, -lsel), g2 = pk(gam, gam);
                 for (int n = 0; n < NT; ++n, ++it) {
                     const uint32_t acc = it % kAccBufs;
@@ -448,58 +543,9 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
                                 if (lane == 0) mbar_arrive_remote(&acc_empty[acc], 0);
                             }
                         }
-                        float g[32];
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            const float4 bb = kSB ? reinterpret_cast<const float4*>(sbias + v0)[j] : bq[j];
-                            const f32x2 z0 = fadd2(pk(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1])), pk(bb.x, bb.y));
-                            const f32x2 z1 = fadd2(pk(__uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3])), pk(bb.z, bb.w));
-                            const float2 p0 = upk(fmul2(ex2x2(ffma2(z0, l2, nl)), g2));
-                            const float2 p1 = upk(fmul2(ex2x2(ffma2(z1, l2, nl)), g2));
-                            g[4 * j] = p0.x;
-                            g[4 * j + 1] = p0.y;
-                            g[4 * j + 2] = p1.x;
-                            g[4 * j + 3] = p1.y;
-                        }
-                        if (static_cast<unsigned>(a.blank - v0) < 32u) {  // the arcs' own logits
-#pragma unroll
-                            for (int j = 0; j < 32; ++j)
-                                if (v0 + j == a.blank) g[j] -= sb;
-                        }
-                        if (static_cast<unsigned>(gy - v0) < 32u) {
-#pragma unroll
-                            for (int j = 0; j < 32; ++j)
-                                if (v0 + j == gy) g[j] -= sy;
-                        }
-                        // dz through the warp's staging block: each lane writes its row's 4 chunks, then reads back
-                        // (row = lane / 4 + 8 s, chunk = lane % 4) so that every global store instruction writes
-                        // 8 whole 64-byte row segments (8 L1 wavefronts instead of 32 for thread-per-row stores)
-                        const uint32_t st = smem_u32(dzst) + static_cast<uint32_t>(warp - 4) * 2048u;
-                        __syncwarp();  // the previous chunk's reads are done
-#pragma unroll
-                        for (int q4 = 0; q4 < 4; ++q4) {
-                            const uint32_t w0 = gl ? pack_bf16x2(g[8 * q4 + 0], g[8 * q4 + 1]) : 0u;
-                            const uint32_t w1 = gl ? pack_bf16x2(g[8 * q4 + 2], g[8 * q4 + 3]) : 0u;
-                            const uint32_t w2 = gl ? pack_bf16x2(g[8 * q4 + 4], g[8 * q4 + 5]) : 0u;
-                            const uint32_t w3 = gl ? pack_bf16x2(g[8 * q4 + 6], g[8 * q4 + 7]) : 0u;
-                            const uint32_t ad = st + lane * 64u + ((q4 ^ ((lane >> 1) & 3)) << 4);
-                            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(ad), "r"(w0), "r"(w1), "r"(w2),
-                                         "r"(w3)
-                                         : "memory");
-                        }
-                        __syncwarp();
-#pragma unroll
-                        for (int s4 = 0; s4 < 4; ++s4) {
-                            const int rr = (lane >> 2) + 8 * s4, kk = lane & 3;
-                            uint4 o;
-                            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                                         : "=r"(o.x), "=r"(o.y), "=r"(o.z), "=r"(o.w)
-                                         : "r"(st + rr * 64u + ((kk ^ ((rr >> 1) & 3)) << 4))
-                                         : "memory");
-                            const int64_t orow = tile * kRowsPerTile + q * 32 + rr;
-                            if (orow < rows)
-                                *reinterpret_cast<uint4*>(a.dz_out + orow * NT * kNTile + v0 + kk * 8) = o;
-                        }
+                        dz_chunk<kSB>(a, r, sbias, bq, v0, gl, l2, nl, g2, sb, sy, gy,
+                                      smem_u32(dzst) + static_cast<uint32_t>(warp - 4) * 2048u, lane,
+                                      tile * kRowsPerTile + q * 32, rows, static_cast<int64_t>(NT) * kNTile);
                     }
                 }
                 continue;
@@ -786,6 +832,200 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
     }
 }
 
+// K6<grad> with h given (the training step, whose forward stored h): the backward's first pass as a plain pair
+// GEMM with both operands in shared memory.  A = the tile's 128 h rows as KB = H / 64 blocks of [128 x 64] bf16
+// (SW128, one 2-SM TMA each onto the leader's barrier, freed block by block by the tile's last N tile so the next
+// tile's rows stream in under it), B = the W stages as k6_joint_lse's pair path.  No warp builds A and A takes no
+// TMEM, so the 512 TMEM columns hold four 128-column accumulators and 16 epilogue warps drain them in four column
+// groups (group e: columns [32 e, 32 e + 32) of every N tile) -- twice k6_joint_lse's dz throughput, which set
+// K6<grad>'s pace once the builders stopped recomputing tanh.
+//   warp 0: W TMA producer; warp 1: MMA issuer (the pair's even CTA, for both); warp 2: A TMA producer;
+//   warps 4-19: dz epilogue (dz_row / dz_chunk)
+constexpr int kDzAcc = 4;
+constexpr int kDzMaxKB = 8;  // H <= 512
+constexpr int kDzABlock = kRowsPerTile * kKBlock * 2;  // 16 KB
+
+template <bool kSB>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    k6_dz_2sm(const __grid_constant__ CUtensorMap w_map, const __grid_constant__ CUtensorMap h_map, const JointArgs a) {
+    constexpr int kSlot = kStageBytes / 2;  // this CTA's 64-column half of a W stage
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    const int H = a.H, V = a.V;
+    const int Vp = (V + kNTile - 1) / kNTile * kNTile;
+    const int KB = H / kKBlock, NT = Vp / kNTile;
+    // carve: [A blocks][W stages] (1024-aligned) [bias] [dz staging 16 x 2 KB] [barriers] [tmem slot]
+    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* ablk = base;
+    uint8_t* wst = ablk + static_cast<size_t>(KB) * kDzABlock;
+    float* sbias = reinterpret_cast<float*>(wst + static_cast<size_t>(a.stages) * kSlot);
+    uint8_t* dzst = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sbias + (kSB ? Vp : 0)) + 127) & ~uintptr_t(127));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(dzst + 16 * 2048);
+    uint64_t* b_full = bars;                       // [stages]
+    uint64_t* b_empty = bars + kMaxStages;         // [stages]
+    uint64_t* a_full = bars + 2 * kMaxStages;      // [KB]
+    uint64_t* a_empty = a_full + kDzMaxKB;         // [KB]
+    uint64_t* acc_full = a_empty + kDzMaxKB;       // [kDzAcc]
+    uint64_t* acc_empty = acc_full + kDzAcc;       // [kDzAcc]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + kDzAcc);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (kSB)
+        for (int i = threadIdx.x; i < Vp; i += blockDim.x) sbias[i] = i < V ? (a.bias ? a.bias[i] : 0.f) : -INFINITY;
+    const int64_t rows = *a.nrows;
+    const int64_t ntiles = (rows + kRowsPerTile - 1) / kRowsPerTile;
+    const int64_t cells = static_cast<int64_t>(a.Tmax) * (a.Umax + 1);
+    const uint32_t crank = cluster_rank();
+    const bool leader = crank == 0;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < a.stages; ++s) {
+            mbar_init(&b_full[s], 1);
+            mbar_init(&b_empty[s], 1);
+        }
+        for (int kb = 0; kb < KB; ++kb) {
+            mbar_init(&a_full[kb], 1);
+            mbar_init(&a_empty[kb], 1);
+        }
+        for (int i = 0; i < kDzAcc; ++i) {
+            mbar_init(&acc_full[i], 1);
+            mbar_init(&acc_empty[i], 16 * 32 + 16);  // the leader's 16 epilogue warps + one arrive per odd-CTA warp
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&w_map)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&h_map)) : "memory");
+    }
+    if (warp == 1) tmem_alloc_2sm(tmem_slot, kTmemCols);
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const int64_t bx = blockIdx.x, cl0 = bx - bx % 2;
+    const int64_t n_iter = ntiles > cl0 ? (ntiles - cl0 + gridDim.x - 1) / gridDim.x : 0;
+    const bool pon = (a.dbg & 4) != 0;  // per-role barrier-wait cycles (RNNT_K6_DEBUG=4)
+    unsigned long long w0 = 0, w1 = 0, w2 = 0, w3 = 0;
+    const long long t_start = clock64();
+
+    if (warp == 0) {
+        // ===== W producer: this CTA's 64-column half of every stage, onto the leader's barrier =====
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            for (int64_t k = 0; k < n_iter; ++k)
+                for (int n = 0; n < NT; ++n)
+                    for (int kb = 0; kb < KB; ++kb) {
+                        mbar_wait_t(&b_empty[s], ph ^ 1, pon, w0);
+                        if (leader) mbar_expect_tx(&b_full[s], kStageBytes);
+                        tma_load_2d_2sm(wst + static_cast<size_t>(s) * kSlot, &w_map, leader_addr(&b_full[s]),
+                                        kb * kKBlock, n * kNTile + static_cast<int>(crank) * (kNTile / 2));
+                        if (++s == a.stages) {
+                            s = 0;
+                            ph ^= 1;
+                        }
+                    }
+        }
+    } else if (warp == 2) {
+        // ===== A producer: the tile's h rows, K block by K block, as the previous tile's last N tile frees them =====
+        if (lane == 0)
+            for (int64_t k = 0; k < n_iter; ++k) {
+                const int row0 = static_cast<int>((bx + k * gridDim.x) * kRowsPerTile);
+                for (int kb = 0; kb < KB; ++kb) {
+                    mbar_wait_t(&a_empty[kb], (static_cast<uint32_t>(k) & 1) ^ 1, pon, w0);
+                    if (leader) mbar_expect_tx(&a_full[kb], 2 * kDzABlock);  // both CTAs' rows
+                    tma_load_2d_2sm(ablk + static_cast<size_t>(kb) * kDzABlock, &h_map, leader_addr(&a_full[kb]),
+                                    kb * kKBlock, row0);
+                }
+            }
+    } else if (warp == 1 && leader) {
+        // ===== MMA issuer: M = 256 (the pair's two row tiles), N = 128, K = H =====
+        int s = 0;
+        uint32_t ph = 0, it = 0;
+        for (int64_t k = 0; k < n_iter; ++k) {
+            for (int n = 0; n < NT; ++n, ++it) {
+                const uint32_t acc = it % kDzAcc;
+                mbar_wait_t(&acc_empty[acc], ((it / kDzAcc) & 1) ^ 1, pon, w1);
+                tc_fence_after();
+                for (int kb = 0; kb < KB; ++kb) {
+                    if (n == 0) mbar_wait_t(&a_full[kb], static_cast<uint32_t>(k) & 1, pon, w0);
+                    mbar_wait_t(&b_full[s], ph, pon, w2);
+                    tc_fence_after();
+                    mma_kblock_ss_2sm(tmem + acc * kNTile, sw128_desc(smem_u32(ablk + static_cast<size_t>(kb) * kDzABlock)),
+                                      sw128_desc(smem_u32(wst + static_cast<size_t>(s) * kSlot)), kIdescPair, kb ? 1u : 0u);
+                    tc_commit_2sm_mc(&b_empty[s], 3);
+                    if (n == NT - 1) tc_commit_2sm_mc(&a_empty[kb], 3);  // the tile's last use of this A block
+                    if (++s == a.stages) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+                tc_commit_2sm_mc(&acc_full[acc], 3);
+            }
+        }
+    } else if (warp >= 4) {
+        // ===== dz epilogue: thread = row, group eg = columns [32 eg, 32 eg + 32) of every N tile =====
+        const int q = warp & 3, eg = (warp - 4) >> 2;
+        const int rl = q * 32 + lane;
+        const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16);
+        const uint32_t st = smem_u32(dzst) + static_cast<uint32_t>(warp - 4) * 2048u;
+        uint32_t it = 0;
+        for (int64_t k = 0; k < n_iter; ++k) {
+            const int64_t tile = bx + k * gridDim.x;
+            const int64_t row = tile * kRowsPerTile + rl;
+            int b = 0, t = 0, u = 0;
+            const bool in = row < rows;
+            if (in) {
+                const int p = __ldg(a.rowmap + row);
+                b = static_cast<int>(p / cells);
+                const int rem = static_cast<int>(p - static_cast<int64_t>(b) * cells);
+                t = rem / (a.Umax + 1);
+                u = rem - t * (a.Umax + 1);
+            }
+            const int T = in ? min(a.T_b[b], a.Tmax) : 0, U = in ? min(a.U_b[b], a.Umax) : 0;
+            const bool live = in && t < T && u <= U;
+            const int yv = (live && u < U) ? a.targets[static_cast<int64_t>(b) * a.Umax + u] : -1;
+            const DzRow d = dz_row(a, in, b, t, u, T, U, live, yv, cells);
+            const f32x2 l2 = pk(kLog2e, kLog2e), nl = pk(-d.lsel, -d.lsel), g2 = pk(d.sb + d.sy, d.sb + d.sy);
+            for (int n = 0; n < NT; ++n, ++it) {
+                const uint32_t acc = it % kDzAcc;
+                const int v0 = n * kNTile + eg * 32;
+                float4 bq[8];  // !kSB: global bias loads in flight under the TMEM load
+#pragma unroll
+                for (int j = 0; j < 8; ++j) bq[j] = kSB ? make_float4(0.f, 0.f, 0.f, 0.f) : bias4(a, v0 + 4 * j);
+                mbar_wait_t(&acc_full[acc], (it / kDzAcc) & 1, pon, w3);
+                tc_fence_after();
+                uint32_t r[32];
+                TMEM_LD32(lane_base + acc * kNTile + eg * 32, r);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                tc_fence_before();  // the accumulator is free once every group has loaded its columns
+                if (leader) {
+                    mbar_arrive(&acc_empty[acc]);
+                } else {
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_remote(&acc_empty[acc], 0);
+                }
+                dz_chunk<kSB>(a, r, sbias, bq, v0, d.gl, l2, nl, g2, d.sb, d.sy, d.gy, st, lane,
+                              tile * kRowsPerTile + q * 32, rows, static_cast<int64_t>(NT) * kNTile);
+            }
+        }
+    }
+    if (pon && lane == 0) {  // the slots joint_front prints: W producer, MMA (a_full, acc_empty, b_full), epilogue, A producer
+        unsigned long long* o = a.prof + static_cast<size_t>(blockIdx.x) * 8;
+        if (warp == 0) { o[0] = clock64() - t_start; o[1] = w0; }
+        if (warp == 1) { o[2] = w0; o[3] = w1; o[4] = w2; }  // zeros in the odd CTA (no MMAs)
+        if (warp == 4) o[5] = w3;
+        if (warp == 16) o[7] = w3;
+        if (warp == 2) o[6] = w0;
+    }
+    tc_fence_before();
+    cluster_sync_all();  // no CTA leaves while its partner may still write into it
+    tc_fence_after();
+    if (warp == 1) tmem_dealloc_2sm(tmem, kTmemCols);
+}
+
+size_t dz_smem_bytes(int H, int V, int stages) {  // V = 0: bias not staged
+    return 1024 + static_cast<size_t>(H / kKBlock) * kDzABlock + static_cast<size_t>(stages) * (kStageBytes / 2) +
+           static_cast<size_t>((V + kNTile - 1) / kNTile * kNTile) * 4 + 128 + 16 * 2048 +
+           (2 * kMaxStages + 2 * kDzMaxKB + 2 * kDzAcc) * 8 + 16;
+}
+
 // Row map of the valid cells (t < T_b, u <= U_b), utterance by utterance: blocks (x, b) write
 // map[off_b + i] = b*Tmax*(Umax+1) + t*(Umax+1) + u for cells i in [x * 4096, (x+1) * 4096) of utterance b's
 // T_b (U_b + 1), off_b = sum of the earlier utterances' counts (invalid lengths count 0); block (0, B-1)
@@ -897,9 +1137,28 @@ rnnt_status joint_front(const void* enc, const void* pred, const void* weight, c
     const int Vs = sb ? V : 0;
     // CTA pairs run pair MMAs by default (RNNT_K6_PAIR=0: per-CTA MMAs with the W stage multicast, for A/B)
     const bool pair = cl == 2 && !(getenv("RNNT_K6_PAIR") && atoi(getenv("RNNT_K6_PAIR")) == 0);
-    while (stages > 2 && joint_smem_bytes(H, Vs, stages, g != nullptr, pair) > static_cast<size_t>(smem_max)) --stages;
-    const size_t smem = joint_smem_bytes(H, Vs, stages, g != nullptr, pair);
+    // K6<grad> on the forward's h (the training step): the two-operand-TMA dz kernel (pair MMAs only)
+    // (RNNT_K6_DZTMA=0: k6_joint_lse<true> with its builders loading h into TMEM, for A/B)
+    const bool dz_tma = g && g->h_ready && pair && !(getenv("RNNT_K6_DZTMA") && atoi(getenv("RNNT_K6_DZTMA")) == 0);
+    auto smem_of = [&](int st) {
+        return dz_tma ? dz_smem_bytes(H, Vs, st) : joint_smem_bytes(H, Vs, st, g != nullptr, pair);
+    };
+    while (stages > 2 && smem_of(stages) > static_cast<size_t>(smem_max)) --stages;
+    const size_t smem = smem_of(stages);
     if (smem > static_cast<size_t>(smem_max)) return RNNT_ERR_UNSUPPORTED;
+    CUtensorMap hmap;  // dz_tma: h [R][H] bf16 (compact rows), [128 rows x 64] boxes, SW128 as MMA operand A
+    if (dz_tma) {
+        const cuuint64_t hdims[2] = {static_cast<cuuint64_t>(H),
+                                     static_cast<cuuint64_t>(static_cast<int64_t>(B) * Tmax * (Umax + 1))};
+        const cuuint32_t hbox[2] = {static_cast<cuuint32_t>(kKBlock), static_cast<cuuint32_t>(kRowsPerTile)};
+        if (enc_fn(&hmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<__nv_bfloat16*>(g->h), hdims, strides, hbox,
+                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return RNNT_ERR_CUDA;
+        if (cudaFuncSetAttribute(sb ? k6_dz_2sm<true> : k6_dz_2sm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)) != cudaSuccess)
+            return RNNT_ERR_CUDA;
+    }
     auto kern = pair ? (sb ? (g ? k6_joint_lse<true, 2, true, true> : k6_joint_lse<false, 2, true, true>)
                            : (g ? k6_joint_lse<true, 2, false, true> : k6_joint_lse<false, 2, false, true>))
               : sb ? (g ? (cl > 1 ? k6_joint_lse<true, 2, true, false> : k6_joint_lse<true, 1, true, false>)
@@ -943,7 +1202,14 @@ rnnt_status joint_front(const void* enc, const void* pred, const void* weight, c
     if (make_map)
         k6_rowmap<<<dim3(static_cast<unsigned>((static_cast<int64_t>(Tmax) * (Umax + 1) + 4095) / 4096), B), 256, 0,
                     s>>>(logit_lens, target_lens, B, Tmax, Umax, rowmap, nrows);
-    kern<<<grid, kThreads, smem, s>>>(map, args);
+    if (dz_tma) {
+        if (sb)
+            k6_dz_2sm<true><<<grid, kThreads, smem, s>>>(map, hmap, args);
+        else
+            k6_dz_2sm<false><<<grid, kThreads, smem, s>>>(map, hmap, args);
+    } else {
+        kern<<<grid, kThreads, smem, s>>>(map, args);
+    }
     if (cudaGetLastError() != cudaSuccess || record_ev(events, 1, s) != cudaSuccess) return RNNT_ERR_CUDA;
     if (args.prof) {  // diagnostics: mean per-CTA cycle split (stderr)
         unsigned long long h[8 * 148] = {};
@@ -953,7 +1219,7 @@ rnnt_status joint_front(const void* enc, const void* pred, const void* weight, c
         for (int c = 0; c < grid && c < 148; ++c)
             for (int k = 0; k < 8; ++k) m[k] += static_cast<double>(h[c * 8 + k]) / grid;
         fprintf(stderr, "K6 cycles/CTA total %.0f | tma wait b_empty %.0f | mma wait a_full %.0f acc_empty %.0f b_full %.0f"
-                        " | epi wait acc_full %.0f / %.0f | builder wait a_empty %.0f\n", m[0], m[1], m[2], m[3], m[4], m[5], m[7], m[6]);
+                        " | epi wait acc_full %.0f / %.0f | builder (dz kernel: A TMA) wait a_empty %.0f\n", m[0], m[1], m[2], m[3], m[4], m[5], m[7], m[6]);
         cudaFree(args.prof);
     }
     return RNNT_OK;
