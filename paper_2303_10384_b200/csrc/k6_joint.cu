@@ -694,7 +694,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
             }
             // items = 32 nch is a multiple of 4 * 32 (nch in {8, 16, 24, 32}): every batch is full
             // fast: the tile has no rows past the end and no diagnostics -> no per-item / per-word selects
-            const bool fast = (tile + 1) * kRowsPerTile <= rows && (a.dbg & ~8) == 0;
+            const bool fast = (tile + 1) * kRowsPerTile <= rows && (a.dbg & ~24) == 0;
             auto batch = [&](const int (&rows_)[4], const int (&cs)[4], auto fast_c) {
                 constexpr bool kFast = decltype(fast_c)::value;
                 uint4 fa[4], ga[4];
@@ -706,8 +706,13 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
                     ok[j] = kFast || fro >= 0;
                     // unconditional loads (row 0 stands in past the end; its output is zeroed below): no
                     // per-register zero fill; 32-bit indices: one IMAD.WIDE per load
-                    fa[j] = __ldg(f4 + static_cast<uint32_t>((kFast || ok[j] ? fro : 0) + cs[j]));
-                    ga[j] = __ldg(g4 + static_cast<uint32_t>((kFast || ok[j] ? gro : 0) + cs[j]));
+                    if (a.dbg & 16) {  // ablation: no f / g loads (wrong results)
+                        fa[j] = make_uint4(fro, gro, cs[j], j);
+                        ga[j] = make_uint4(gro, fro, j, cs[j]);
+                    } else {
+                        fa[j] = __ldg(f4 + static_cast<uint32_t>((kFast || ok[j] ? fro : 0) + cs[j]));
+                        ga[j] = __ldg(g4 + static_cast<uint32_t>((kFast || ok[j] ? gro : 0) + cs[j]));
+                    }
                 }
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
@@ -1133,6 +1138,7 @@ rnnt_status joint_front(const void* enc, const void* pred, const void* weight, c
         cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
         return RNNT_ERR_CUDA;
     int stages = kMaxStages;
+    if (const char* e = getenv("RNNT_K6_STAGES")) stages = std::max(2, std::min(kMaxStages, atoi(e)));  // A/B only
     const bool sb = V <= kSBiasMaxV;  // bias staged in shared memory (small vocabularies), else read from global
     const int Vs = sb ? V : 0;
     // CTA pairs run pair MMAs by default (RNNT_K6_PAIR=0: per-CTA MMAs with the W stage multicast, for A/B)
