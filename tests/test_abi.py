@@ -75,7 +75,7 @@ def test_host_argument_errors(rb):
     assert _call_raw(rb, V=1) == INVALID
     assert _call_raw(rb, blank=4) == INVALID
     assert _call_raw(rb, blank=-1) == INVALID
-    assert _call_raw(rb, U=1024) == UNSUP
+    assert _call_raw(rb, U=4096) == UNSUP  # Umax + 1 > kMaxUp1 = 4096 (rnnt_b200.h)
     assert _call_raw(rb, ws_bytes=16) == WS
     # grads partially overlapping logits (but not equal) is rejected
     assert _call_raw(rb, grads=ctypes.c_void_p((1 << 20) + 4)) == INVALID
