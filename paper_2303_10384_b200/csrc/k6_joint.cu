@@ -247,12 +247,14 @@ __device__ __forceinline__ DzRow dz_row(const JointArgs& a, bool in, int b, int 
 // gradient (!gl).  Through the warp's 2 KB staging block at `st`: each lane writes its row's 4 chunks, then reads
 // back (row = lane / 4 + 8 s, chunk = lane % 4) so that every global store instruction writes 8 whole 64-byte row
 // segments (8 L1 wavefronts instead of 32 for thread-per-row stores).  row0: the compact row of lane 0; rows:
-// the valid rows; ldz: dz's row pitch in elements.
+// the valid rows; ldz: dz's row pitch in elements.  dz_map (k6_dz_2sm): the staging block's layout is TMA's
+// SWIZZLE_64B one, so lane 0 stores it with one TMA tile store (box {32 columns, 32 rows}) instead of the warp's
+// 4 x 16-byte loads and stores per lane -- half the L1 traffic; the block is reused once that store has read it.
 template <bool kSB>
 __device__ __forceinline__ void dz_chunk(const JointArgs& a, const uint32_t (&r)[32], const float* sbias,
                                          const float4 (&bq)[8], int v0, bool gl, f32x2 l2, f32x2 nl, f32x2 g2,
                                          float sb, float sy, int gy, uint32_t st, int lane, int64_t row0,
-                                         int64_t rows, int64_t ldz) {
+                                         int64_t rows, int64_t ldz, const CUtensorMap* dz_map = nullptr) {
     float g[32];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
@@ -276,7 +278,8 @@ __device__ __forceinline__ void dz_chunk(const JointArgs& a, const uint32_t (&r)
         for (int j = 0; j < 32; ++j)
             if (v0 + j == gy) g[j] -= sy;
     }
-    __syncwarp();  // the previous chunk's reads are done
+    if (dz_map && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    __syncwarp();  // the previous chunk's reads (or TMA store) are done
 #pragma unroll
     for (int q4 = 0; q4 < 4; ++q4) {
         const uint32_t w0 = gl ? pack_bf16x2(g[8 * q4 + 0], g[8 * q4 + 1]) : 0u;
@@ -286,6 +289,12 @@ __device__ __forceinline__ void dz_chunk(const JointArgs& a, const uint32_t (&r)
         const uint32_t ad = st + lane * 64u + ((q4 ^ ((lane >> 1) & 3)) << 4);
         asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(ad), "r"(w0), "r"(w1), "r"(w2), "r"(w3)
                      : "memory");
+    }
+    if (dz_map) {  // rows past `rows` (< R: dz's allocation) get zeros; TMA clips at R
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0 && row0 < rows) tma_store_2d(dz_map, st, v0, static_cast<int>(row0));
+        return;
     }
     __syncwarp();
 #pragma unroll
@@ -852,7 +861,8 @@ constexpr int kDzABlock = kRowsPerTile * kKBlock * 2;  // 16 KB
 
 template <bool kSB>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    k6_dz_2sm(const __grid_constant__ CUtensorMap w_map, const __grid_constant__ CUtensorMap h_map, const JointArgs a) {
+    k6_dz_2sm(const __grid_constant__ CUtensorMap w_map, const __grid_constant__ CUtensorMap h_map,
+              const __grid_constant__ CUtensorMap dz_map, const JointArgs a) {
     constexpr int kSlot = kStageBytes / 2;  // this CTA's 64-column half of a W stage
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const int H = a.H, V = a.V;
@@ -863,7 +873,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint8_t* ablk = base;
     uint8_t* wst = ablk + static_cast<size_t>(KB) * kDzABlock;
     float* sbias = reinterpret_cast<float*>(wst + static_cast<size_t>(a.stages) * kSlot);
-    uint8_t* dzst = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sbias + (kSB ? Vp : 0)) + 127) & ~uintptr_t(127));
+    // dz staging blocks: 1024-aligned (each 2 KB block holds whole SWIZZLE_64B atoms for its TMA store)
+    uint8_t* dzst = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sbias + (kSB ? Vp : 0)) + 1023) & ~uintptr_t(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(dzst + 16 * 2048);
     uint64_t* b_full = bars;                       // [stages]
     uint64_t* b_empty = bars + kMaxStages;         // [stages]
@@ -1007,9 +1018,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     if (lane == 0) mbar_arrive_remote(&acc_empty[acc], 0);
                 }
                 dz_chunk<kSB>(a, r, sbias, bq, v0, d.gl, l2, nl, g2, d.sb, d.sy, d.gy, st, lane,
-                              tile * kRowsPerTile + q * 32, rows, static_cast<int64_t>(NT) * kNTile);
+                              tile * kRowsPerTile + q * 32, rows, static_cast<int64_t>(NT) * kNTile,
+                              (a.dbg & 32) ? nullptr : &dz_map);
             }
         }
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // the last dz stores are done
     }
     if (pon && lane == 0) {  // the slots joint_front prints: W producer, MMA (a_full, acc_empty, b_full), epilogue, A producer
         unsigned long long* o = a.prof + static_cast<size_t>(blockIdx.x) * 8;
@@ -1027,7 +1040,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
 size_t dz_smem_bytes(int H, int V, int stages) {  // V = 0: bias not staged
     return 1024 + static_cast<size_t>(H / kKBlock) * kDzABlock + static_cast<size_t>(stages) * (kStageBytes / 2) +
-           static_cast<size_t>((V + kNTile - 1) / kNTile * kNTile) * 4 + 128 + 16 * 2048 +
+           static_cast<size_t>((V + kNTile - 1) / kNTile * kNTile) * 4 + 1024 + 16 * 2048 +
            (2 * kMaxStages + 2 * kDzMaxKB + 2 * kDzAcc) * 8 + 16;
 }
 
@@ -1152,8 +1165,18 @@ rnnt_status joint_front(const void* enc, const void* pred, const void* weight, c
     while (stages > 2 && smem_of(stages) > static_cast<size_t>(smem_max)) --stages;
     const size_t smem = smem_of(stages);
     if (smem > static_cast<size_t>(smem_max)) return RNNT_ERR_UNSUPPORTED;
-    CUtensorMap hmap;  // dz_tma: h [R][H] bf16 (compact rows), [128 rows x 64] boxes, SW128 as MMA operand A
+    CUtensorMap hmap;   // dz_tma: h [R][H] bf16 (compact rows), [128 rows x 64] boxes, SW128 as MMA operand A
+    CUtensorMap dzmap;  // dz_tma: dz [R][Vp] bf16, [32 rows x 32] boxes, SWIZZLE_64B (the epilogue's staging layout)
     if (dz_tma) {
+        const int64_t R = static_cast<int64_t>(B) * Tmax * (Umax + 1);
+        const int Vpad = (V + kNTile - 1) / kNTile * kNTile;
+        const cuuint64_t ddims[2] = {static_cast<cuuint64_t>(Vpad), static_cast<cuuint64_t>(R)};
+        const cuuint64_t dstr[1] = {static_cast<cuuint64_t>(Vpad) * 2};
+        const cuuint32_t dbox[2] = {32, 32};
+        if (enc_fn(&dzmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g->dz, ddims, dstr, dbox, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return RNNT_ERR_CUDA;
         const cuuint64_t hdims[2] = {static_cast<cuuint64_t>(H),
                                      static_cast<cuuint64_t>(static_cast<int64_t>(B) * Tmax * (Umax + 1))};
         const cuuint32_t hbox[2] = {static_cast<cuuint32_t>(kKBlock), static_cast<cuuint32_t>(kRowsPerTile)};
@@ -1210,9 +1233,9 @@ rnnt_status joint_front(const void* enc, const void* pred, const void* weight, c
                     s>>>(logit_lens, target_lens, B, Tmax, Umax, rowmap, nrows);
     if (dz_tma) {
         if (sb)
-            k6_dz_2sm<true><<<grid, kThreads, smem, s>>>(map, hmap, args);
+            k6_dz_2sm<true><<<grid, kThreads, smem, s>>>(map, hmap, dzmap, args);
         else
-            k6_dz_2sm<false><<<grid, kThreads, smem, s>>>(map, hmap, args);
+            k6_dz_2sm<false><<<grid, kThreads, smem, s>>>(map, hmap, dzmap, args);
     } else {
         kern<<<grid, kThreads, smem, s>>>(map, args);
     }
