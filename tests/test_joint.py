@@ -239,6 +239,25 @@ def test_joint_grad_backward_gemm_shapes(rb, shape):
     assert_grads_r23(out, enc, pred, W, b, y, T_b, U_b, 0, "allow_ignore", tag=f"gemm {shape}")
 
 
+def test_joint_grad_many_tiles_per_cta(rb):
+    """~61k valid rows (~480 row tiles, > 3 per CTA on 148 SMs): every CTA pair of K6's forward and k6_dz_2sm
+    walks several row tiles, so the per-K-block A ring (h blocks refilled as the previous tile's last N tile
+    frees them), the accumulator ring and the barrier phases wrap many times; Vp = 256 (2 N tiles), H = 256
+    (4 K blocks)."""
+    B, T, U, H, V = 40, 160, 48, 256, 130
+    cfg = workloads.random_config(B, T, U, V, seed=71, variant="rnnt")
+    T_b, U_b = workloads.lengths(cfg)
+    assert rb.joint_valid_rows(T_b, U_b, T, U) >= 3 * 148 * 128
+    y = workloads.targets(cfg, U_b)
+    enc, pred, W, b = workloads.joint_inputs(B, T, U, H, V, seed=71)
+    out = rb.rnnt_joint_loss_grad(enc.cuda(), pred.cuda(), W.cuda(), b.cuda(), y, T_b, U_b, 0, "rnnt")
+    torch.cuda.synchronize()
+    ref_l = oj.joint_loss(*_np(enc, pred, W, b), y, T_b, U_b, 0, "rnnt")
+    l = out[0].cpu().numpy().astype(np.float64)
+    assert (np.abs(l - ref_l) / np.maximum(np.abs(ref_l), 1.0)).max() <= 1e-5
+    assert_grads_r23(out, enc, pred, W, b, y, T_b, U_b, 0, "rnnt", tag="many tiles")
+
+
 def test_joint_grad_no_valid_rows(rb):
     """Every utterance invalid (T_b > Tmax): no GEMM rows at all -- NaN losses, every gradient exactly zero."""
     H, V = 128, 130
