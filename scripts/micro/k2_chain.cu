@@ -77,6 +77,36 @@ __global__ void chain(int steps, const double* x, double* out, long long* cyc) {
                 pub[j] = cur + xy;
                 selff[j] = static_cast<float>(self[j]);
                 pubf[j] = static_cast<float>(pub[j]);
+            } else if (V == 5 || V == 7 || V == 8) {
+                // restructured: the operand adds off the chain, (m + x) + c; V 7 / 8 add the kernel's per-cell
+                // validity select (7: new form, 8: the current form cur + x)
+                const int t = d - static_cast<int>(threadIdx.x) * kC - j;
+                const bool valid = static_cast<unsigned>(t) < static_cast<unsigned>(steps);
+                const double diff = self[j] - nb;
+                const double m = diff > 0.0 ? self[j] : nb;
+                const float xf = fminf(-fabsf(static_cast<float>(diff)) * kLog2e, 0.f);
+                const double c = static_cast<double>(lg2(1.f + ex2(xf)) * kLn2);
+                if (V == 5) {
+                    self[j] = (m + xb) + c;
+                    pub[j] = (m + xy) + c;
+                } else if (V == 7) {
+                    self[j] = valid ? (m + xb) + c : -INFINITY;
+                    pub[j] = valid ? (m + xy) + c : -INFINITY;
+                } else {
+                    const double cur = m + c;
+                    self[j] = valid ? cur + xb : -INFINITY;
+                    pub[j] = valid ? cur + xy : -INFINITY;
+                }
+            } else if (V == 6) {
+                // the current backward step: the neighbour's operand add and the terminal-cell select on the chain
+                const int t = d - static_cast<int>(threadIdx.x) * kC - j;
+                const bool valid = static_cast<unsigned>(t) < static_cast<unsigned>(steps);
+                const bool last = t == steps - 3;
+                const double op2 = nb + xy;
+                double cur = lse_v1(self[j] + xb, op2);
+                cur = last ? xb : cur;
+                self[j] = valid ? cur : -INFINITY;
+                pub[j] = self[j];
             } else if (V == 4) {
                 const double cur = lse_v4(self[j], nb);
                 self[j] = cur + xb;
@@ -118,5 +148,13 @@ int main() {
     run(chain<3, 1>, "all fp32 (rejected by R11), kC=1");
     run(chain<4, 1>, "fp64 adds only (int max / conversions), kC=1");
     run(chain<4, 2>, "fp64 adds only (int max / conversions), kC=2");
+    run(chain<5, 1>, "restructured (m + x) + c, kC=1");
+    run(chain<5, 2>, "restructured (m + x) + c, kC=2");
+    run(chain<8, 1>, "current forward + validity select, kC=1");
+    run(chain<7, 1>, "restructured + validity select, kC=1");
+    run(chain<6, 1>, "current backward (+x on chain, last select), kC=1");
+    run(chain<8, 2>, "current forward + validity select, kC=2");
+    run(chain<7, 2>, "restructured + validity select, kC=2");
+    run(chain<6, 2>, "current backward (+x on chain, last select), kC=2");
     return 0;
 }
