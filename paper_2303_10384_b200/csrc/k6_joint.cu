@@ -21,6 +21,8 @@
 // TMEM: A [0, 256) columns, kAccBufs = 2 accumulators of 128 columns in [256, 512).  (N = 64 with four
 // buffers was measured slower: 2.20 vs 1.77 ms at c3 / H = 512 -- the narrower MMAs lose more than the
 // deeper buffering gains.)  mbarriers link the roles.
+// The training step's backward first pass on the forward's stored h is a separate kernel, k6_dz_2sm (below):
+// A from shared memory by TMA, four accumulators, 16 dz epilogue warps.
 // Constraints: H % 128 == 0, H <= 512 (any V: the last N tile's missing columns are masked).
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -202,8 +204,9 @@ struct JointArgs {
     const double* logp;
     const float* grad_scale;
     __nv_bfloat16* dz_out;  // [rows][Vp] row-major, Vp = V rounded up to whole N tiles (tail columns 0)
-    __nv_bfloat16* h_out;   // [rows][H]: h stored by the builders (K6<grad>; the training step's forward), or null
+    __nv_bfloat16* h_out;   // [rows][H]: h stored by the builders (the training step's forward; K6<grad> A/B), or null
     const __nv_bfloat16* h_in;  // K6<grad> only: [rows][H] h as the forward stored it -- loaded, not recomputed
+                                // (k6_dz_2sm reads it through its own tensor map; k6_joint_lse<true> by bulk copies)
 };
 
 // Per-row scalars of dz for cell (t,u) of utterance b: the occupancies of the two scored arcs leaving it, as K3

@@ -7,8 +7,9 @@
 //   dpre       = dh * (1 - h^2)   (dh accumulated in fp32 in TMEM, stored in bf16; tanh' from the stored bf16 h)
 //   d enc(b,t,:) = sum_{u <= U_b} dpre(t,u,:)           d pred(b,u,:) = sum_{t < T_b} dpre(t,u,:)
 // over the valid cells.  Pipeline (all on the caller's stream, every kernel this library's own):
-//   K6 (forward: lse, gathers) -> K2 (alpha, beta, losses) -> K6<grad> (recomputes z on the tensor cores;
-//   its epilogue writes dz in bf16, its builders write h) -> K8 (dh = dz W, CTA-pair tcgen05 GEMM) and K9
+//   K6 (forward: lse, gathers, and h from its builders' registers) -> K2 (alpha, beta, losses) -> K6<grad>
+//   (k6_dz_2sm: z again on the tensor cores from the stored h, its epilogue writes dz in bf16) -> K8 (dh = dz W,
+//   CTA-pair tcgen05 GEMM) and K9
 //   (dW = dz^T h and dbias, CTA-pair tcgen05 GEMM split over row ranges, k9_reduce) (k8_joint_bwd.cu) -> K7
 //   (tanh' and the two reductions, one streaming pass over dh and h).  The [B,T,U+1,V] logits never exist; dz
 //   does, in
@@ -358,7 +359,7 @@ extern "C" rnnt_status rnnt_joint_loss_grad(const void* enc, const void* pred, c
     cudaStream_t s = static_cast<cudaStream_t>(stream);
 
     // forward: K6 (row map into the gradient workspace, which K2 does not touch) and K2 (alpha, beta, losses)
-    // The forward also stores h (bulk copies beside its MUFU-bound builders) so that K6<grad> loads it instead of
+    // The forward also stores h (from its builders' registers) so that K6<grad> loads it by TMA instead of
     // recomputing tanh(f + g) (RNNT_K6_HREUSE=0: K6<grad> recomputes and stores h, for A/B).
     const bool hreuse = !(getenv("RNNT_K6_HREUSE") && atoi(getenv("RNNT_K6_HREUSE")) == 0);
     rnnt_status st = joint_front(enc, pred, weight, bias, targets, logit_lens, target_lens, B, Tmax, Umax, H, V,
@@ -369,7 +370,7 @@ extern "C" rnnt_status rnnt_joint_loss_grad(const void* enc, const void* pred, c
     const int vk = (variant < 0) ? kRnnt : (variant == WRNNT_FORCE_FINAL ? kForceFinal : kAllowIgnore);
     Problem p{nullptr, targets, logit_lens, target_lens, B, Tmax, Umax, V, blank, vk, losses, nullptr, nullptr, kF32};
     if (launch_k2_alpha_beta(p, w, s) != cudaSuccess) return RNNT_ERR_CUDA;
-    // backward pass 1: z again on the tensor cores -> dz (bf16), h
+    // backward pass 1: z again on the tensor cores -> dz (bf16) (and h when the forward did not store it)
     const GradIO g{w.lse, w.lp, w.alpha, w.beta, w.logp, grad_scale, dz, hb, hreuse};
     st = joint_front(enc, pred, weight, bias, targets, logit_lens, target_lens, B, Tmax, Umax, H, V, blank,
                      workspace, workspace_bytes, s, nullptr, rowmap, nrows, false, &g);

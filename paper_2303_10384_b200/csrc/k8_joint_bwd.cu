@@ -8,7 +8,7 @@
 //        split over row ranges (K) -- the output is only V x H -- with partials reduced in a fixed order
 //        (k9_reduce), so the result is deterministic.  dbias comes from the same dz tiles in shared memory.
 //
-// Operands (bf16, fp32 accumulation in TMEM): dz [R][Vp] and h [R][Hg] as K6<grad> writes them, W [V][H] as the
+// Operands (bf16, fp32 accumulation in TMEM): dz [R][Vp] and h [R][Hg] as K6 / K6<grad> write them, W [V][H] as the
 // caller passes it.  K8: A = dz tile (K-major: v contiguous), B = W (MN-major: h contiguous, K = v); K9: A = dz^T
 // and B = h, both MN-major (v / h contiguous, K = r).  Every operand moves by TMA as SWIZZLE_128B boxes of
 // 64 elements along the contiguous dimension; the MN-major ones are read by the MMA through sw128_mn_desc.
