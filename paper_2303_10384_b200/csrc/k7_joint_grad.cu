@@ -184,22 +184,35 @@ __global__ void __launch_bounds__(256, 1) k7_reduce(const __nv_bfloat16* __restr
 // kG units: one barrier to publish, one to release; a fixed summation order: deterministic).  The next group's
 // rows are loaded while the current one is combined, and ~90 registers allow 2 blocks per SM, so far more of
 // each SM's bytes are in flight than with k7_reduce's 204-register warps.
+// kFW warps = frames per block: 16 (512 threads, one block per SM) halves the d pred partials against 8 (two
+// blocks per SM, the same 16 warps): the partials are [ceil(T / kFW)][B][U + 1][H] fp32, written here and read
+// back by k7_pred_sum -- at p124 0.63 GB of traffic per step with 8-frame chunks, as much as 44 % of the dh and
+// h bytes themselves.  RNNT_K7_FRAMES=8 builds the 8-frame form (A/B).
 constexpr int kG = 4;
+#ifndef RNNT_K7_FRAMES
+#define RNNT_K7_FRAMES 16
+#endif
+constexpr int kFW = RNNT_K7_FRAMES;
+static_assert(kFW == 8 || kFW == 16, "frames per K7 block");
+
+constexpr size_t k7_rows_bytes() { return sizeof(float4) * kG * kFW * 2 * 32; }
 
 template <bool kPre>
-__global__ void __launch_bounds__(256, 2) k7_reduce_f(const __nv_bfloat16* __restrict__ dx,
+__global__ void __launch_bounds__(kFW * 32, 16 / kFW) k7_reduce_f(const __nv_bfloat16* __restrict__ dx,
                                                       const __nv_bfloat16* __restrict__ h,
                                                       const int32_t* __restrict__ T_b, const int32_t* __restrict__ U_b,
                                                       int B, int Tmax, int Umax, int H, float* __restrict__ d_enc,
                                                       float* __restrict__ part) {
-    __shared__ int s_part[8];
-    __shared__ float4 s_row[kG][8][2][32];  // [unit in group][warp][half of the 8 columns][lane]
+    __shared__ int s_part[kFW];
+    // [unit in group][warp][half of the 8 columns][lane]: 32 KB at kFW = 8, 64 KB at 16 (dynamic: > 48 KB static)
+    extern __shared__ float4 k7_rows[];
+    auto s_row = reinterpret_cast<float4 (*)[kFW][2][32]>(k7_rows);
     const int chunk = blockIdx.x, b = blockIdx.y;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int off = utt_offset(T_b, U_b, b, Tmax, Umax, s_part);
     const int n = utt_count(T_b, U_b, b, Tmax, Umax);
     const int T = n ? T_b[b] : 0, U = n ? U_b[b] : -1;
-    const int t0 = chunk * kTC, t = t0 + warp;
+    const int t0 = chunk * kFW, t = t0 + warp;
     const bool frame_in = t < T;
     const int c = blockIdx.z * 256 + lane * 8;
     const bool col_in = c < H;
@@ -250,14 +263,14 @@ __global__ void __launch_bounds__(256, 2) k7_reduce_f(const __nv_bfloat16* __res
             s_row[j][warp][1][lane] = make_float4(d[j][4], d[j][5], d[j][6], d[j][7]);
         }
         __syncthreads();
-        // thread -> (unit j = warp / 2, half = warp & 1, lane): sums the 8 frames' rows in warp order
-        {
+        // thread of warps 0-7 -> (unit j = warp / 2, half = warp & 1, lane): sums the kFW frames' rows in warp order
+        if (warp < 2 * kG) {
             const int j = warp >> 1, hf = warp & 1;
             const int u = u0 + j;
             if (u <= U && col_in) {
                 float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-                for (int w = 0; w < 8; ++w) {
+                for (int w = 0; w < kFW; ++w) {
                     const float4 x = s_row[j][w][hf][lane];
                     o.x += x.x, o.y += x.y, o.z += x.z, o.w += x.w;
                 }
@@ -277,11 +290,11 @@ __global__ void __launch_bounds__(256, 2) k7_reduce_f(const __nv_bfloat16* __res
 // padded units (and invalid utterances) get 0.  Block (u, b), 128 threads x 4 columns.
 __global__ void __launch_bounds__(128) k7_pred_sum(const float* __restrict__ part, const int32_t* __restrict__ T_b,
                                                    const int32_t* __restrict__ U_b, int B, int Tmax, int Umax, int H,
-                                                   float* __restrict__ d_pred) {
+                                                   int tc, float* __restrict__ d_pred) {  // tc: frames per chunk
     const int u = blockIdx.x, b = blockIdx.y;
     const int n = utt_count(T_b, U_b, b, Tmax, Umax);
     const int T = n ? T_b[b] : 0, U = n ? U_b[b] : -1;
-    const int nch = (u <= U) ? (T + kTC - 1) / kTC : 0;
+    const int nch = (u <= U) ? (T + tc - 1) / tc : 0;
     for (int c = threadIdx.x * 4; c < H; c += blockDim.x * 4) {
         float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
         for (int ch = 0; ch < nch; ++ch) {
@@ -319,7 +332,7 @@ GradLayout grad_layout(int B, int Tmax, int Umax, int H, int V) {
     off += align256(sizeof(__nv_bfloat16) * L.R * H);
     L.part = off;  // K9's per-row-range partials of dW and dbias
     off += align256(k9_partial_bytes(L.Vp, H));
-    L.kpart = off;  // K7's per-frame-chunk partials of d pred [ceil(Tmax / kTC)][B][Umax + 1][H] fp32
+    L.kpart = off;  // K7's per-frame-chunk partials of d pred [ceil(Tmax / tc)][B][Umax + 1][H] fp32, tc >= kTC
     off += align256(sizeof(float) * static_cast<size_t>((Tmax + kTC - 1) / kTC) * B * (Umax + 1) * H);
     L.total = off;
     return L;
@@ -407,8 +420,20 @@ extern "C" rnnt_status rnnt_joint_loss_grad(const void* enc, const void* pred, c
     // K7: tanh' and the reductions into d enc / d pred (its d pred partials in their own region: K9 may still
     // be reading dz)
     float* ppart = reinterpret_cast<float*>(ws + L.kpart);
-    const dim3 g7((Tmax + kTC - 1) / kTC, B, (H + 255) / 256);
     const bool k7_units = getenv("RNNT_K7_UNITS") && atoi(getenv("RNNT_K7_UNITS")) != 0;  // A/B: unit-per-warp K7
+    const int tc = k7_units ? kTC : kFW;  // frames per d pred partial
+    if (!k7_units) {
+        static bool attr = false;  // k7_reduce_f's dynamic shared memory above the 48 KB default
+        if (!attr) {
+            if (cudaFuncSetAttribute(k7_reduce_f<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(k7_rows_bytes())) != cudaSuccess ||
+                cudaFuncSetAttribute(k7_reduce_f<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(k7_rows_bytes())) != cudaSuccess)
+                return RNNT_ERR_CUDA;
+            attr = true;
+        }
+    }
+    const dim3 g7((Tmax + tc - 1) / tc, B, (H + 255) / 256);
     if (k7_units) {
         if (tanh_k8)
             k7_reduce<true><<<g7, 256, 0, s>>>(dpre, nullptr, logit_lens, target_lens, B, Tmax, Umax, H, d_enc, ppart);
@@ -416,11 +441,13 @@ extern "C" rnnt_status rnnt_joint_loss_grad(const void* enc, const void* pred, c
             k7_reduce<false><<<g7, 256, 0, s>>>(dpre, hb, logit_lens, target_lens, B, Tmax, Umax, H, d_enc, ppart);
     } else {
         if (tanh_k8)
-            k7_reduce_f<true><<<g7, 256, 0, s>>>(dpre, nullptr, logit_lens, target_lens, B, Tmax, Umax, H, d_enc, ppart);
+            k7_reduce_f<true><<<g7, kFW * 32, k7_rows_bytes(), s>>>(dpre, nullptr, logit_lens, target_lens, B, Tmax, Umax,
+                                                                      H, d_enc, ppart);
         else
-            k7_reduce_f<false><<<g7, 256, 0, s>>>(dpre, hb, logit_lens, target_lens, B, Tmax, Umax, H, d_enc, ppart);
+            k7_reduce_f<false><<<g7, kFW * 32, k7_rows_bytes(), s>>>(dpre, hb, logit_lens, target_lens, B, Tmax, Umax, H,
+                                                                       d_enc, ppart);
     }
-    k7_pred_sum<<<dim3(Umax + 1, B), 128, 0, s>>>(ppart, logit_lens, target_lens, B, Tmax, Umax, H, d_pred);
+    k7_pred_sum<<<dim3(Umax + 1, B), 128, 0, s>>>(ppart, logit_lens, target_lens, B, Tmax, Umax, H, tc, d_pred);
     if (cudaGetLastError() != cudaSuccess) return RNNT_ERR_CUDA;
     if (pool && cudaStreamWaitEvent(s, pool->k2_done[0], 0) != cudaSuccess) return RNNT_ERR_CUDA;  // join K9
     return RNNT_OK;
