@@ -258,6 +258,27 @@ def test_joint_grad_many_tiles_per_cta(rb):
     assert_grads_r23(out, enc, pred, W, b, y, T_b, U_b, 0, "rnnt", tag="many tiles")
 
 
+@pytest.mark.parametrize("env", [{"RNNT_K6_DZTMA": "0"}, {"RNNT_K6_HREUSE": "0"}, {"RNNT_K6_PAIR": "0"}],
+                         ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
+def test_joint_grad_ab_paths(rb, env, monkeypatch):
+    """The A/B switches of the training step's first backward pass (read per call by joint_front) stay correct:
+    k6_joint_lse<true> loading the forward's h into TMEM (DZTMA=0), recomputing h (HREUSE=0), and per-CTA MMAs
+    (PAIR=0), each against the same exact chain rule (R23) as the default k6_dz_2sm path."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    B, T, U, H, V = 3, 30, 10, 256, 500
+    cfg = workloads.random_config(B, T, U, V, seed=73, variant="allow_ignore")
+    T_b, U_b = workloads.lengths(cfg)
+    y = workloads.targets(cfg, U_b)
+    enc, pred, W, b = workloads.joint_inputs(B, T, U, H, V, seed=73)
+    out = rb.rnnt_joint_loss_grad(enc.cuda(), pred.cuda(), W.cuda(), b.cuda(), y, T_b, U_b, 0, "allow_ignore")
+    torch.cuda.synchronize()
+    ref_l = oj.joint_loss(*_np(enc, pred, W, b), y, T_b, U_b, 0, "allow_ignore")
+    l = out[0].cpu().numpy().astype(np.float64)
+    assert (np.abs(l - ref_l) / np.maximum(np.abs(ref_l), 1.0)).max() <= 1e-5
+    assert_grads_r23(out, enc, pred, W, b, y, T_b, U_b, 0, "allow_ignore", tag=f"ab {env}")
+
+
 def test_joint_grad_no_valid_rows(rb):
     """Every utterance invalid (T_b > Tmax): no GEMM rows at all -- NaN losses, every gradient exactly zero."""
     H, V = 128, 130
