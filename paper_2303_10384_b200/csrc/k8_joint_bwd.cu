@@ -213,6 +213,7 @@ struct K8Args {
     const __nv_bfloat16* h;   // [R][Hg]
     __nv_bfloat16* dpre;      // [R][H]
     int R, H, Hg, V, stages;
+    bool split;               // pair kernel: the two 256-column chunks handed over separately (H = 512)
     unsigned long long* prof;  // RNNT_K8_DEBUG=4: per-CTA wait cycles [grid][8] (diagnostics), else nullptr
 };
 
@@ -432,21 +433,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kK8Threads, 1)
     uint64_t* bars = reinterpret_cast<uint64_t*>(base + static_cast<size_t>(a.stages) * slot_bytes);
     uint64_t* full = bars;                    // [stages], the leader's counts
     uint64_t* empty = bars + kBwdMaxStages;   // [stages]
+    // acc_full / acc_empty [2]: with H > 256 the accumulator's two 256-column chunks are handed over separately --
+    // the last stage of a tile finishes chunk 0 first, its epilogue group drains it while chunk 1's MMAs run, and
+    // the next tile's first stage starts chunk 0 once that half is free (RNNT_K8_SPLIT=0: one hand-over, A/B)
     uint64_t* acc_full = bars + 2 * kBwdMaxStages;
-    uint64_t* acc_empty = acc_full + 1;       // the leader's counts both CTAs' epilogue warps
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 2);
-    const uint32_t stg0 = (smem_u32(acc_full + 4) + 127) & ~127u;  // 8 epilogue warps x kK8StgBytes
+    uint64_t* acc_empty = acc_full + 2;       // the leader's counts both CTAs' epilogue warps
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 4);
+    const uint32_t stg0 = (smem_u32(acc_full + 6) + 127) & ~127u;  // 8 epilogue warps x kK8StgBytes
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int rank = static_cast<int>(cluster_rank());
     const bool leader = rank == 0;
+    const bool split = a.split && H == 512;  // the epilogue groups' halves are the two chunks only at H = 512
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < a.stages; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(acc_full, 1);
-        mbar_init(acc_empty, 16);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&acc_full[i], 1);
+            mbar_init(&acc_empty[i], split ? 8 : 16);  // per chunk: its 4 warps in each CTA; else all 8 in each
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&dz_map)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&w_map)) : "memory");
@@ -497,24 +504,42 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kK8Threads, 1)
             const uint32_t id0 = idesc_bf16(256, min(256, H), false, true);
             const uint32_t id1 = H > 256 ? idesc_bf16(256, H - 256, false, true) : 0u;
             for (int64_t k = 0; k < n_iter; ++k) {
-                mbar_wait_t(acc_empty, (static_cast<uint32_t>(k) & 1) ^ 1, pon, w_accempty);
-                tc_fence_after();
+                const uint32_t pe = (static_cast<uint32_t>(k) & 1) ^ 1;
+                if (!split) {
+                    mbar_wait_t(&acc_empty[0], pe, pon, w_accempty);
+                    tc_fence_after();
+                }
                 for (int kb = 0; kb < KB; ++kb) {
                     mbar_wait_t(&full[s], ph, pon, w_full);
                     tc_fence_after();
                     const uint32_t sa = smem_u32(base + static_cast<size_t>(s) * slot_bytes);
                     const uint64_t adesc = sw128_desc(sa), bdesc = sw128_mn_desc(sa + kK8ABytes, kK8BBox);
-                    if (H > 256)
-                        mma_stage_k8_2sm<2>(tmem, adesc, bdesc, id0, id1, kb ? 1u : 0u);
-                    else
+                    if (split && (kb == 0 || kb == KB - 1)) {  // the chunks one after the other, each handed over
+                        // chunk 1 = D + 256 columns, B + 2 boxes of 8 KB (descriptor + 1024)
+                        if (kb == 0) {
+                            mbar_wait_t(&acc_empty[0], pe, pon, w_accempty);
+                            tc_fence_after();
+                        }
                         mma_stage_k8_2sm<1>(tmem, adesc, bdesc, id0, 0u, kb ? 1u : 0u);
+                        if (kb == KB - 1) tc_commit_2sm_mc(&acc_full[0], 3);
+                        if (kb == 0) {
+                            mbar_wait_t(&acc_empty[1], pe, pon, w_accempty);
+                            tc_fence_after();
+                        }
+                        mma_stage_k8_2sm<1>(tmem + 256, adesc, bdesc + 1024, id1, 0u, kb ? 1u : 0u);
+                        if (kb == KB - 1) tc_commit_2sm_mc(&acc_full[1], 3);
+                    } else if (H > 256) {
+                        mma_stage_k8_2sm<2>(tmem, adesc, bdesc, id0, id1, kb ? 1u : 0u);
+                    } else {
+                        mma_stage_k8_2sm<1>(tmem, adesc, bdesc, id0, 0u, kb ? 1u : 0u);
+                    }
                     tc_commit_2sm_mc(&empty[s], 3);
                     if (++s == a.stages) {
                         s = 0;
                         ph ^= 1;
                     }
                 }
-                tc_commit_2sm_mc(acc_full, 3);
+                if (!split) tc_commit_2sm_mc(&acc_full[0], 3);
             }
         }
     } else if (warp >= 4) {
@@ -525,8 +550,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kK8Threads, 1)
         const uint32_t stg = stg0 + (warp - 4) * kK8StgBytes;
         for (int64_t k = 0; k < n_iter; ++k) {
             const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16) + c_lo;
+            const int hc = split ? eh : 0;  // this group's chunk barrier
             auto wait = [&]() {
-                mbar_wait_t(acc_full, static_cast<uint32_t>(k) & 1, pon, w_accfull);
+                mbar_wait_t(&acc_full[hc], static_cast<uint32_t>(k) & 1, pon, w_accfull);
                 tc_fence_after();
             };
             auto release = [&]() {  // this warp's last load of the accumulator: release it to the leader
@@ -534,9 +560,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kK8Threads, 1)
                 __syncwarp();
                 if (lane == 0) {
                     if (leader)
-                        mbar_arrive(acc_empty);
+                        mbar_arrive(&acc_empty[hc]);
                     else
-                        mbar_arrive_remote(acc_empty, 0);
+                        mbar_arrive_remote(&acc_empty[hc], 0);
                 }
             };
             const int64_t row_w = (pr + k * np) * 256 + rank * 128 + q * 32;
@@ -1095,7 +1121,7 @@ cudaError_t launch_k8(const __nv_bfloat16* dz, const __nv_bfloat16* weight, cons
         const int slot = kK8ABytes + (H / 128) * kK8BBox;
         int stages = kBwdMaxStages;
         auto smem_of = [&](int st) {
-            return static_cast<size_t>(1024 + st * slot + (2 * kBwdMaxStages + 4) * 8 + 128 + 8 * kK8StgBytes);
+            return static_cast<size_t>(1024 + st * slot + (2 * kBwdMaxStages + 6) * 8 + 128 + 8 * kK8StgBytes);
         };
         while (stages > 2 && smem_of(stages) > static_cast<size_t>(smem_max)) --stages;
         const size_t smem = smem_of(stages);
@@ -1106,7 +1132,8 @@ cudaError_t launch_k8(const __nv_bfloat16* dz, const __nv_bfloat16* weight, cons
         int resident = max_clusters(kern2, 2, smem, kK8Threads);
         if (resident <= 0) resident = nsm / 2;
         const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ntiles, resident))) * 2;
-        K8Args args{h, dpre, R, H, Hg, V, stages, nullptr};
+        const bool split = !(getenv("RNNT_K8_SPLIT") && atoi(getenv("RNNT_K8_SPLIT")) == 0);
+        K8Args args{h, dpre, R, H, Hg, V, stages, split, nullptr};
         const bool prof = getenv("RNNT_K8_DEBUG") && (atoi(getenv("RNNT_K8_DEBUG")) & 4);
         if (prof) cudaMalloc(&args.prof, sizeof(unsigned long long) * 8 * grid);
         kern2<<<grid, kK8Threads, smem, s>>>(dz_map, w_map, args);
@@ -1148,7 +1175,7 @@ cudaError_t launch_k8(const __nv_bfloat16* dz, const __nv_bfloat16* weight, cons
     int resident = max_clusters(kern, cl, smem, kK8Threads);  // persistent: only co-resident clusters
     if (resident <= 0) resident = nsm / cl;
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ngroups, resident))) * cl;
-    K8Args args{h, dpre, R, H, Hg, V, stages, nullptr};
+    K8Args args{h, dpre, R, H, Hg, V, stages, false, nullptr};
     const bool prof = getenv("RNNT_K8_DEBUG") && (atoi(getenv("RNNT_K8_DEBUG")) & 4);
     if (prof) cudaMalloc(&args.prof, sizeof(unsigned long long) * 8 * grid);
     kern<<<grid, kK8Threads, smem, s>>>(dz_map, w_map, args);
