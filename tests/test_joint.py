@@ -258,15 +258,16 @@ def test_joint_grad_many_tiles_per_cta(rb):
     assert_grads_r23(out, enc, pred, W, b, y, T_b, U_b, 0, "rnnt", tag="many tiles")
 
 
-@pytest.mark.parametrize("env", [{"RNNT_K6_DZTMA": "0"}, {"RNNT_K6_HREUSE": "0"}, {"RNNT_K6_PAIR": "0"}],
+@pytest.mark.parametrize("env", [{"RNNT_K6_DZTMA": "0"}, {"RNNT_K6_HREUSE": "0"}, {"RNNT_K6_PAIR": "0"},
+                                 {"RNNT_K8_SPLIT": "0"}],
                          ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_joint_grad_ab_paths(rb, env, monkeypatch):
-    """The A/B switches of the training step's first backward pass (read per call by joint_front) stay correct:
-    k6_joint_lse<true> loading the forward's h into TMEM (DZTMA=0), recomputing h (HREUSE=0), and per-CTA MMAs
-    (PAIR=0), each against the same exact chain rule (R23) as the default k6_dz_2sm path."""
+    """The training step's A/B switches (read per call) stay correct: k6_joint_lse<true> loading the forward's h into
+    TMEM (DZTMA=0), recomputing h (HREUSE=0), per-CTA MMAs (PAIR=0), K8's single accumulator hand-over (SPLIT=0),
+    each against the same exact chain rule (R23) as the default path."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
-    B, T, U, H, V = 3, 30, 10, 256, 500
+    B, T, U, H, V = 3, 30, 10, 512, 500  # H = 512: K8's split hand-over applies
     cfg = workloads.random_config(B, T, U, V, seed=73, variant="allow_ignore")
     T_b, U_b = workloads.lengths(cfg)
     y = workloads.targets(cfg, U_b)
