@@ -193,8 +193,8 @@ struct JointArgs {
     int dbg;  // diagnostics (env RNNT_K6_DEBUG, never set in production): 1 = builders skip tanh,
               // 2 = epilogue skips its math (both give wrong losses: timing ablations only), 4 = per-role
               // barrier-wait cycle counters printed to stderr, 8 = tanh.approx builders (RNNT_K6_FAST_TANH=1),
-              // 16 = builders skip the f / g loads (timing ablation, wrong results); k6_dz_2sm: 32 = dz by per-lane
-              // 16-byte stores instead of TMA tile stores, 64 = rows' scalars in place, not one tile ahead (A/B)
+              // 16 = builders skip the f / g loads (timing ablation, wrong results), 32 = k6_dz_2sm stores dz by
+              // per-lane 16-byte stores instead of TMA tile stores (A/B, correct results)
     unsigned long long* prof;
     float* lse_out;
     double2* lp_out;
@@ -244,61 +244,6 @@ __device__ __forceinline__ DzRow dz_row(const JointArgs& a, bool in, int b, int 
         d.sy *= sc;
     }
     d.lsel = (lse == -INFINITY) ? INFINITY : lse * kLog2e;
-    return d;
-}
-
-// dz_row in two halves for k6_dz_2sm's one-tile lookahead: dz_loads issues every load of a row's scalars (none
-// of them used yet, so the warp does not wait), dz_row_of does the arithmetic once they have landed.  Loads whose
-// index could leave its array are guarded by index arithmetic only (no dependence on loaded lengths).
-struct DzLoads {
-    bool in;
-    int t, u, T, U, yv;
-    double lP, al, be0, be1;
-    double2 l;
-    float lse, sc;
-};
-__device__ __forceinline__ DzLoads dz_loads(const JointArgs& a, bool in, int p, int64_t cells) {
-    DzLoads x{};
-    x.in = in;
-    x.yv = -1;
-    if (!in) return x;
-    const int Up1 = a.Umax + 1;
-    const int b = static_cast<int>(p / cells);
-    const int rem = static_cast<int>(p - static_cast<int64_t>(b) * cells);
-    x.t = rem / Up1;
-    x.u = rem - x.t * Up1;
-    x.T = a.T_b[b];
-    x.U = a.U_b[b];
-    x.lP = a.logp[b];
-    x.sc = a.grad_scale ? a.grad_scale[b] : 1.f;
-    if (x.u < a.Umax) x.yv = a.targets[static_cast<int64_t>(b) * a.Umax + x.u];
-    const int64_t dcell = (static_cast<int64_t>(b) * (a.Tmax + a.Umax) + (x.t + x.u)) * Up1 + x.u;
-    x.lse = a.lse_in[static_cast<int64_t>(b) * cells + x.t * Up1 + x.u];
-    x.l = a.lp_in[dcell];
-    x.al = a.alpha[dcell];
-    if (x.t + x.u + 1 < a.Tmax + a.Umax) {  // diagonal t + u + 1 of this utterance exists
-        x.be0 = a.beta[dcell + Up1];
-        if (x.u + 1 < Up1) x.be1 = a.beta[dcell + Up1 + 1];
-    }
-    return x;
-}
-__device__ __forceinline__ DzRow dz_row_of(const JointArgs& a, const DzLoads& x) {
-    DzRow d{false, 0.f, 0.f, INFINITY, -1};
-    const int T = min(x.T, a.Tmax), U = min(x.U, a.Umax);
-    const bool live = x.in && x.t < T && x.u <= U;
-    d.gl = live && isfinite(x.lP);
-    if (!d.gl) return d;
-    if (x.t < T - 1)
-        d.sb = __expf(static_cast<float>(x.al + x.l.x + x.be0 - x.lP));
-    else if (x.u == U)
-        d.sb = __expf(static_cast<float>(x.al + x.l.x - x.lP));
-    if (x.u < U) {
-        d.sy = __expf(static_cast<float>(x.al + x.l.y + x.be1 - x.lP));
-        d.gy = x.yv;
-    }
-    d.sb *= x.sc;
-    d.sy *= x.sc;
-    d.lsel = (x.lse == -INFINITY) ? INFINITY : x.lse * kLog2e;
     return d;
 }
 
@@ -763,7 +708,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
             }
             // items = 32 nch is a multiple of 4 * 32 (nch in {8, 16, 24, 32}): every batch is full
             // fast: the tile has no rows past the end and no diagnostics -> no per-item / per-word selects
-            const bool fast = (tile + 1) * kRowsPerTile <= rows && (a.dbg & ~24) == 0;
+            const bool fast = (tile + 1) * kRowsPerTile <= rows && (a.dbg & ~(8 | 16 | 32)) == 0;  // the A/B bits keep the fast path
             auto batch = [&](const int (&rows_)[4], const int (&cs)[4], auto fast_c) {
                 constexpr bool kFast = decltype(fast_c)::value;
                 uint4 fa[4], ga[4];
@@ -1042,25 +987,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16);
         const uint32_t st = smem_u32(dzst) + static_cast<uint32_t>(warp - 4) * 2048u;
         uint32_t it = 0;
-        // the row's scalars one tile ahead (RNNT_K6_DEBUG=64: in place, A/B): tile k + 1's row-map entry is
-        // loaded when tile k starts, its dependent loads after tile k's first chunk and its DzRow formed after
-        // tile k's last chunk, so their latency overlaps tile k's chunks instead of opening tile k + 1
-        const bool look = (a.dbg & 64) == 0;
-        auto row_of = [&](int64_t kk) { return (bx + kk * gridDim.x) * kRowsPerTile + rl; };
-        DzRow dcur{};
-        {
-            const int64_t r0 = row_of(0);
-            const bool in0 = n_iter > 0 && r0 < rows;
-            dcur = dz_row_of(a, dz_loads(a, in0, in0 ? __ldg(a.rowmap + r0) : 0, cells));
-        }
         for (int64_t k = 0; k < n_iter; ++k) {
             const int64_t tile = bx + k * gridDim.x;
-            const int64_t rn = row_of(k + 1);
-            const bool inn = k + 1 < n_iter && rn < rows;
-            int pn = 0;
-            if (look && inn) pn = __ldg(a.rowmap + rn);
-            DzLoads xn{};
-            const DzRow d = dcur;
+            const int64_t row = tile * kRowsPerTile + rl;
+            int b = 0, t = 0, u = 0;
+            const bool in = row < rows;
+            if (in) {
+                const int p = __ldg(a.rowmap + row);
+                b = static_cast<int>(p / cells);
+                const int rem = static_cast<int>(p - static_cast<int64_t>(b) * cells);
+                t = rem / (a.Umax + 1);
+                u = rem - t * (a.Umax + 1);
+            }
+            const int T = in ? min(a.T_b[b], a.Tmax) : 0, U = in ? min(a.U_b[b], a.Umax) : 0;
+            const bool live = in && t < T && u <= U;
+            const int yv = (live && u < U) ? a.targets[static_cast<int64_t>(b) * a.Umax + u] : -1;
+            const DzRow d = dz_row(a, in, b, t, u, T, U, live, yv, cells);
             const f32x2 l2 = pk(kLog2e, kLog2e), nl = pk(-d.lsel, -d.lsel), g2 = pk(d.sb + d.sy, d.sb + d.sy);
             for (int n = 0; n < NT; ++n, ++it) {
                 const uint32_t acc = it % kDzAcc;
@@ -1083,10 +1025,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 dz_chunk<kSB>(a, r, sbias, bq, v0, d.gl, l2, nl, g2, d.sb, d.sy, d.gy, st, lane,
                               tile * kRowsPerTile + q * 32, rows, static_cast<int64_t>(NT) * kNTile,
                               (a.dbg & 32) ? nullptr : &dz_map);
-                if (look && n == 0) xn = dz_loads(a, inn, pn, cells);  // tile k + 1's scalars in flight
             }
-            if (!look) xn = dz_loads(a, inn, inn ? __ldg(a.rowmap + rn) : 0, cells);
-            dcur = dz_row_of(a, xn);
         }
         if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // the last dz stores are done
     }
