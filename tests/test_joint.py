@@ -281,6 +281,39 @@ def test_joint_grad_ab_paths(rb, env, monkeypatch):
     assert_grads_r23(out, enc, pred, W, b, y, T_b, U_b, 0, "allow_ignore", tag=f"ab {env}")
 
 
+def test_joint_grad_full_p124_properties(rb):
+    """The paper's training shapes in full (B = 30, T <= 433, U <= 92, V = 500, H = 512; the launch bench.py
+    times), checked by what holds at any size: (1) a sampled utterance's loss matches the oracle's R22 forward;
+    (2) every row's dz sums to zero over v in real arithmetic (softmax mass gamma minus the two occupancies), so
+    |sum_v d_bias(v)| is bounded by dz's bf16 rounding, u = 2^-8 of sum |dz| <= 2 sum_b (T_b + U_b) (each path
+    scores T_b blanks and U_b labels: the occupancies sum to T_b + U_b); a dropped or mis-signed occupancy term
+    would leave ~sum_b (T_b + U_b); (3) an utterance's d enc / d pred / loss from the whole batch equal bit for bit
+    those of a one-utterance call (row-independent kernels, per-utterance fixed-order reductions)."""
+    cfg = workloads.EXTRA_CONFIGS["p124"]
+    B, T, U, V, H = cfg.B, cfg.Tmax, cfg.Umax, cfg.V, 512
+    T_b, U_b = workloads.lengths(cfg)
+    y = workloads.targets(cfg, U_b)
+    enc, pred, W, b = workloads.joint_inputs(B, T, U, H, V, seed=91)
+    args = (W.cuda(), b.cuda())
+    out = rb.rnnt_joint_loss_grad(enc.cuda(), pred.cuda(), *args, y, T_b, U_b, cfg.blank, "rnnt")
+    torch.cuda.synchronize()
+    cells = T_b.astype(np.int64) * (U_b.astype(np.int64) + 1)
+    i = int(np.argmin(cells))  # the cheapest utterance for the oracle
+    ref = oj.joint_loss(*_np(enc[i:i + 1], pred[i:i + 1], W, b), y[i:i + 1], T_b[i:i + 1], U_b[i:i + 1], cfg.blank,
+                        "rnnt")
+    l = float(out[0][i])
+    assert abs(l - ref[0]) <= 1e-5 * max(abs(ref[0]), 1.0), (l, ref[0])
+    db = out[4].double()
+    bound = 2.0 ** -8 * 2.0 * float(np.sum(T_b.astype(np.float64) + U_b)) + 1e-3
+    assert abs(float(db.sum())) <= bound, (float(db.sum()), bound)
+    for j in (i, B - 1):
+        o1 = rb.rnnt_joint_loss_grad(enc[j:j + 1].cuda(), pred[j:j + 1].cuda(), *args, y[j:j + 1], T_b[j:j + 1],
+                                     U_b[j:j + 1], cfg.blank, "rnnt")
+        torch.cuda.synchronize()
+        assert torch.equal(o1[0][0], out[0][j])
+        assert torch.equal(o1[1][0], out[1][j]) and torch.equal(o1[2][0], out[2][j])
+
+
 def test_joint_grad_no_valid_rows(rb):
     """Every utterance invalid (T_b > Tmax): no GEMM rows at all -- NaN losses, every gradient exactly zero."""
     H, V = 128, 130
