@@ -281,15 +281,16 @@ def test_joint_grad_ab_paths(rb, env, monkeypatch):
     assert_grads_r23(out, enc, pred, W, b, y, T_b, U_b, 0, "allow_ignore", tag=f"ab {env}")
 
 
-def test_joint_grad_full_p124_properties(rb):
-    """The paper's training shapes in full (B = 30, T <= 433, U <= 92, V = 500, H = 512; the launch bench.py
-    times), checked by what holds at any size: (1) a sampled utterance's loss matches the oracle's R22 forward;
+@pytest.mark.parametrize("name", ["p124", "c3"])
+def test_joint_grad_full_size_properties(rb, name):
+    """The training step at full size -- the paper's shapes (B = 30, T <= 433, U <= 92, V = 500) and c3's
+    (B = 32, T = 500, U = 100, V = 1024), H = 512, the launch bench.py times -- checked by what holds at any size: (1) a sampled utterance's loss matches the oracle's R22 forward;
     (2) every row's dz sums to zero over v in real arithmetic (softmax mass gamma minus the two occupancies), so
     |sum_v d_bias(v)| is bounded by dz's bf16 rounding, u = 2^-8 of sum |dz| <= 2 sum_b (T_b + U_b) (each path
     scores T_b blanks and U_b labels: the occupancies sum to T_b + U_b); a dropped or mis-signed occupancy term
     would leave ~sum_b (T_b + U_b); (3) an utterance's d enc / d pred / loss from the whole batch equal bit for bit
     those of a one-utterance call (row-independent kernels, per-utterance fixed-order reductions)."""
-    cfg = workloads.EXTRA_CONFIGS["p124"]
+    cfg = {**workloads.CONFIGS, **workloads.EXTRA_CONFIGS}[name]
     B, T, U, V, H = cfg.B, cfg.Tmax, cfg.Umax, cfg.V, 512
     T_b, U_b = workloads.lengths(cfg)
     y = workloads.targets(cfg, U_b)
