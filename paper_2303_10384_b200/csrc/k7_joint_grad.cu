@@ -422,17 +422,11 @@ extern "C" rnnt_status rnnt_joint_loss_grad(const void* enc, const void* pred, c
     float* ppart = reinterpret_cast<float*>(ws + L.kpart);
     const bool k7_units = getenv("RNNT_K7_UNITS") && atoi(getenv("RNNT_K7_UNITS")) != 0;  // A/B: unit-per-warp K7
     const int tc = k7_units ? kTC : kFW;  // frames per d pred partial
-    if (!k7_units) {
-        static bool attr = false;  // k7_reduce_f's dynamic shared memory above the 48 KB default
-        if (!attr) {
-            if (cudaFuncSetAttribute(k7_reduce_f<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(k7_rows_bytes())) != cudaSuccess ||
-                cudaFuncSetAttribute(k7_reduce_f<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(k7_rows_bytes())) != cudaSuccess)
-                return RNNT_ERR_CUDA;
-            attr = true;
-        }
-    }
+    // k7_reduce_f's dynamic shared memory above the 48 KB default (set per call: the attribute is per device)
+    if (!k7_units && cudaFuncSetAttribute(tanh_k8 ? k7_reduce_f<true> : k7_reduce_f<false>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(k7_rows_bytes())) != cudaSuccess)
+        return RNNT_ERR_CUDA;
     const dim3 g7((Tmax + tc - 1) / tc, B, (H + 255) / 256);
     if (k7_units) {
         if (tanh_k8)
