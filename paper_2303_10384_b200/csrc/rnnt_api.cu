@@ -4,6 +4,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "elem.cuh"
@@ -97,7 +98,7 @@ using rnnt::kMaxChunks;
 // K1 -> K2 -> K3 for one call.  With chunks c = 0..n-1 the order is
 //   stream s:       K1(0) K1(1) .. K1(n-1)  [wait K2(0)] K3(0)  [wait K2(1)] K3(1) ..
 //   stream aux[c]:  [wait K1(c)] K2(c)                              (high priority, one stream per chunk)
-// so every K2 hides under the remaining K1 / K3 traffic.  events[0..5] (optional): K1 start / end and K3
+// so every K2 hides under the remaining K1 / K3 traffic; small calls put K3(c) on aux[c] after K2(c) instead.  events[0..5] (optional): K1 start / end and K3
 // start (after the first K2 wait) / end on s; K2 start / end on aux[0] (the first chunk's wavefront).
 rnnt_status launch_path(const Problem& p, const Workspace& w, cudaStream_t s, void* const* events) {
     auto ev = [&](int i) { return static_cast<cudaEvent_t>(events[i]); };
@@ -124,6 +125,31 @@ rnnt_status launch_path(const Problem& p, const Workspace& w, cudaStream_t s, vo
     }
     auto ok = [](cudaError_t e) { return e == cudaSuccess; };
     if (events && !ok(record_timing(ev(0), s))) return RNNT_ERR_CUDA;
+    // Small calls (< 2^28 joint elements, e.g. c2): K3(c) follows K2(c) on aux[c] instead of queueing on s behind
+    // every K1 chunk, so the first chunks' gradient passes overlap the later chunks' K1 and the K2 latency of the
+    // last chunk hides under them (c2 0.101 -> 0.094 ms); on large calls the overlapping K1 / K3 streams compete
+    // for HBM and lose (c3 2.91 -> 3.01 ms, p124 0.93 -> 0.95 ms).  RNNT_K3_ON_AUX=0 / 1 forces either (A/B).
+    const int64_t elems = static_cast<int64_t>(p.B) * p.Tmax * (p.Umax + 1) * p.V;
+    bool k3_aux = elems < (int64_t(1) << 28);
+    if (const char* e = getenv("RNNT_K3_ON_AUX")) k3_aux = atoi(e) != 0;
+    if (k3_aux) {
+        for (int c = 0; c < nch; ++c) {
+            cudaStream_t a = pool->aux[c];
+            if (!ok(rnnt::launch_k1_lse_gather(pc[c], wc[c], s)) || !ok(cudaEventRecord(pool->k1_done[c], s)) ||
+                !ok(cudaStreamWaitEvent(a, pool->k1_done[c], 0)))
+                return RNNT_ERR_CUDA;
+            if (c == 0 && events && !ok(record_timing(ev(4), a))) return RNNT_ERR_CUDA;
+            if (!ok(rnnt::launch_k2_alpha_beta(pc[c], wc[c], a))) return RNNT_ERR_CUDA;
+            if (c == 0 && events && (!ok(record_timing(ev(5), a)) || !ok(record_timing(ev(2), a)))) return RNNT_ERR_CUDA;
+            if (p.grads && !ok(rnnt::launch_k3_grad(pc[c], wc[c], a))) return RNNT_ERR_CUDA;
+            if (!ok(cudaEventRecord(pool->k2_done[c], a))) return RNNT_ERR_CUDA;
+        }
+        if (events && !ok(record_timing(ev(1), s))) return RNNT_ERR_CUDA;
+        for (int c = 0; c < nch; ++c)
+            if (!ok(cudaStreamWaitEvent(s, pool->k2_done[c], 0))) return RNNT_ERR_CUDA;
+        if (events && !ok(record_timing(ev(3), s))) return RNNT_ERR_CUDA;
+        return RNNT_OK;
+    }
     for (int c = 0; c < nch; ++c) {
         cudaStream_t a = pool->aux[c];
         if (!ok(rnnt::launch_k1_lse_gather(pc[c], wc[c], s)) || !ok(cudaEventRecord(pool->k1_done[c], s)) ||
