@@ -460,6 +460,15 @@ def main():
                 "frac": k3_gbs / peak, "traffic": traffic,
                 "algorithmic_bytes_per_launch": k3_bytes / nch, "launches_per_step": nch,
                 "algorithmic_bytes_per_step": k3_bytes, "peak_source": peak_src}
+        if nch > 1 and B * Tmax * Up1 * V < (1 << 28):
+            # small call (rnnt_api.cu): each chunk's K3 runs behind its K2 on the chunk's stream, overlapping the
+            # later chunks' K1, so K3 has no span of its own -- report K1 + K3 bytes over K1-start -> K3-end
+            both_ms = span(0, 3)
+            gbs = (k1_bytes + k3_bytes) / (both_ms / 1e3) / 1e9
+            roof = {"bound": "hbm", "kernel": "k1_lse_gather + k3_grad (overlapped, small call)", "achieved": gbs,
+                    "peak": peak, "unit": "GB/s", "frac": gbs / peak, "traffic": None,
+                    "algorithmic_bytes_per_launch": (k1_bytes + k3_bytes) / nch, "launches_per_step": nch,
+                    "algorithmic_bytes_per_step": k1_bytes + k3_bytes, "peak_source": peak_src}
     else:
         nbytes = k1_bytes + (k3_bytes if args.mode == "lattice" else 0)  # lattice: the whole loss+grad step
         gbs = nbytes / ((k1_ms if args.mode == "loss" else ms_step) / 1e3) / 1e9
