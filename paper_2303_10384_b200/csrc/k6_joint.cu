@@ -151,19 +151,6 @@ __device__ __forceinline__ float2 tanh2_mufu(float x0, float x1) {
     const float2 d = upk(fadd2(pk(ex2(y.x), ex2(y.y)), pk(1.f, 1.f)));
     return upk(ffma2(pk(rcp_approx(d.x), rcp_approx(d.y)), pk(-2.f, -2.f), pk(1.f, 1.f)));
 }
-// Opt-in builders' tanh (RNNT_K6_FAST_TANH=1): one MUFU op per element (tanh.approx.f32, relative error ~2^-11)
-// instead of two (ex2 + rcp, tanh2_mufu).  At the paper's shapes (V = 500: 4 N tiles per row tile) the two MUFU
-// ops per element make K6 MUFU-bound: p124 forward 0.457 -> 0.366 ms, c3 1.391 -> 1.332 ms (A/B, one box).  But
-// h = bf16(tanh) then differs from R22's bf16 of the exact tanh by one bf16 ulp far more often (wherever tanh
-// lies within ~2^-11 of a bf16 rounding boundary, against ~2e-7 for tanh2_mufu): losses moved 1.3e-7 .. 1.8e-7
-// relative at p124 / c3, but 1.2e-5 on 300 short utterances at H = 128 (test_joint_many_short_utterances, bar
-// 1e-5) -- so it is not the default.
-__device__ __forceinline__ float2 tanh2_approx(float x0, float x1) {
-    float y0, y1;
-    asm("tanh.approx.f32 %0, %1;" : "=f"(y0) : "f"(x0));
-    asm("tanh.approx.f32 %0, %1;" : "=f"(y1) : "f"(x1));
-    return make_float2(y0, y1);
-}
 // z[k] for a per-lane k in [0, 32) without local memory: a 5-level select tree (31 FSEL) instead of 32
 // compare-and-move pairs.
 __device__ __forceinline__ float select32(const float (&z)[32], int k) {
@@ -192,9 +179,10 @@ struct JointArgs {
     const int* nrows;   // number of valid cells (compact rows)
     int dbg;  // diagnostics (env RNNT_K6_DEBUG, never set in production): 1 = builders skip tanh,
               // 2 = epilogue skips its math (both give wrong losses: timing ablations only), 4 = per-role
-              // barrier-wait cycle counters printed to stderr, 8 = tanh.approx builders (RNNT_K6_FAST_TANH=1),
-              // 16 = builders skip the f / g loads (timing ablation, wrong results), 32 = k6_dz_2sm stores dz by
-              // per-lane 16-byte stores instead of TMA tile stores (A/B, correct results)
+              // barrier-wait cycle counters printed to stderr, 32 = k6_dz_2sm stores dz by per-lane 16-byte
+              // stores instead of TMA tile stores (A/B, correct results).  (No switch inside the builders' loop:
+              // runtime selects there cost ~10 % at p124 -- the tanh.approx opt-in and a load ablation that were
+              // measured this way are recorded in DESIGN.md and removed.)
     unsigned long long* prof;
     float* lse_out;
     double2* lp_out;
@@ -348,7 +336,9 @@ __device__ __forceinline__ float4 bias4(const JointArgs& a, int v) {
 // cycle per SM measured on K9) is then no longer the limit.  Only the even CTA issues MMAs; the odd CTA's
 // builders tell it that their A tile is in TMEM (one remote arrive per tile) and its epilogue warps release the
 // accumulators on the leader's acc_empty (one remote arrive per warp per N tile).
-template <bool kGrad, int kCl, bool kSB, bool kPair>
+// kStore (forward only): the builders also store h for the training step's K6<grad> (a compile-time choice: the
+// store and its predicate stay out of the loss-only forward's builder loop).
+template <bool kGrad, int kCl, bool kSB, bool kPair, bool kStore = false>
 __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
     k6_joint_lse(const __grid_constant__ CUtensorMap w_map, const JointArgs a) {
     static_assert(!kPair || kCl == 2, "pair MMAs need clusters of 2");
@@ -675,7 +665,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
             return identity ? static_cast<int>(row) : __ldg(a.rowmap + row);
         };
         int p_next = -1;
-        const bool hstore = a.h_out != nullptr, hload = kGrad && a.h_in != nullptr;
+        const bool hstore = kGrad ? a.h_out != nullptr : kStore, hload = kGrad && a.h_in != nullptr;
         auto build = [&](int64_t tile, int p) {
             if (hload) {
                 // h as the training step's forward stored it: one bulk async copy per row into the staging
@@ -708,7 +698,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
             }
             // items = 32 nch is a multiple of 4 * 32 (nch in {8, 16, 24, 32}): every batch is full
             // fast: the tile has no rows past the end and no diagnostics -> no per-item / per-word selects
-            const bool fast = (tile + 1) * kRowsPerTile <= rows && (a.dbg & ~(8 | 16 | 32)) == 0;  // the A/B bits keep the fast path
+            const bool fast = (tile + 1) * kRowsPerTile <= rows && (a.dbg & 1) == 0;  // no-tanh ablation: slow path
             auto batch = [&](const int (&rows_)[4], const int (&cs)[4], auto fast_c) {
                 constexpr bool kFast = decltype(fast_c)::value;
                 uint4 fa[4], ga[4];
@@ -720,13 +710,8 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
                     ok[j] = kFast || fro >= 0;
                     // unconditional loads (row 0 stands in past the end; its output is zeroed below): no
                     // per-register zero fill; 32-bit indices: one IMAD.WIDE per load
-                    if (a.dbg & 16) {  // ablation: no f / g loads (wrong results)
-                        fa[j] = make_uint4(fro, gro, cs[j], j);
-                        ga[j] = make_uint4(gro, fro, j, cs[j]);
-                    } else {
-                        fa[j] = __ldg(f4 + static_cast<uint32_t>((kFast || ok[j] ? fro : 0) + cs[j]));
-                        ga[j] = __ldg(g4 + static_cast<uint32_t>((kFast || ok[j] ? gro : 0) + cs[j]));
-                    }
+                    fa[j] = __ldg(f4 + static_cast<uint32_t>((kFast || ok[j] ? fro : 0) + cs[j]));
+                    ga[j] = __ldg(g4 + static_cast<uint32_t>((kFast || ok[j] ? gro : 0) + cs[j]));
                 }
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
@@ -737,7 +722,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
                     for (int e = 0; e < 4; ++e) {
                         const float2 x = unpack_bf16x2(fw[e]), y = unpack_bf16x2(gw[e]);
                         const float2 xs = upk(fadd2(pk(x.x, x.y), pk(y.x, y.y)));
-                        const float2 h = (a.dbg & 8) ? tanh2_approx(xs.x, xs.y) : tanh2_mufu(xs.x, xs.y);
+                        const float2 h = tanh2_mufu(xs.x, xs.y);
                         ow[e] = kFast ? pack_bf16x2(h.x, h.y)
                                       : !ok[j] ? 0u : (a.dbg & 1) ? (fw[e] ^ gw[e]) : pack_bf16x2(h.x, h.y);
                     }
@@ -1193,12 +1178,17 @@ rnnt_status joint_front(const void* enc, const void* pred, const void* weight, c
                                  static_cast<int>(smem)) != cudaSuccess)
             return RNNT_ERR_CUDA;
     }
-    auto kern = pair ? (sb ? (g ? k6_joint_lse<true, 2, true, true> : k6_joint_lse<false, 2, true, true>)
-                           : (g ? k6_joint_lse<true, 2, false, true> : k6_joint_lse<false, 2, false, true>))
+    const bool st = h_fwd != nullptr;  // the training step's forward: builders store h (kStore instances)
+    auto kern = pair ? (sb ? (g ? k6_joint_lse<true, 2, true, true>
+                                : (st ? k6_joint_lse<false, 2, true, true, true> : k6_joint_lse<false, 2, true, true>))
+                           : (g ? k6_joint_lse<true, 2, false, true>
+                                : (st ? k6_joint_lse<false, 2, false, true, true> : k6_joint_lse<false, 2, false, true>)))
               : sb ? (g ? (cl > 1 ? k6_joint_lse<true, 2, true, false> : k6_joint_lse<true, 1, true, false>)
-                        : (cl > 1 ? k6_joint_lse<false, 2, true, false> : k6_joint_lse<false, 1, true, false>))
+                        : st ? (cl > 1 ? k6_joint_lse<false, 2, true, false, true> : k6_joint_lse<false, 1, true, false, true>)
+                             : (cl > 1 ? k6_joint_lse<false, 2, true, false> : k6_joint_lse<false, 1, true, false>))
                    : (g ? (cl > 1 ? k6_joint_lse<true, 2, false, false> : k6_joint_lse<true, 1, false, false>)
-                        : (cl > 1 ? k6_joint_lse<false, 2, false, false> : k6_joint_lse<false, 1, false, false>));
+                        : st ? (cl > 1 ? k6_joint_lse<false, 2, false, false, true> : k6_joint_lse<false, 1, false, false, true>)
+                             : (cl > 1 ? k6_joint_lse<false, 2, false, false> : k6_joint_lse<false, 1, false, false>));
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
         return RNNT_ERR_CUDA;
 
@@ -1226,7 +1216,6 @@ rnnt_status joint_front(const void* enc, const void* pred, const void* weight, c
             args.h_out = g->h;
     }
     if (const char* e = getenv("RNNT_K6_DEBUG")) args.dbg = atoi(e);
-    if (const char* e = getenv("RNNT_K6_FAST_TANH")) args.dbg |= atoi(e) ? 8 : 0;
     args.prof = nullptr;
     if (args.dbg & 4) cudaMalloc(&args.prof, sizeof(unsigned long long) * 8 * nsm);
     const int64_t ntiles = (args.rows + kRowsPerTile - 1) / kRowsPerTile;
