@@ -177,12 +177,11 @@ struct JointArgs {
     int stages;
     const int* rowmap;  // [rows] compact row -> padded row index b*Tmax*(Umax+1) + t*(Umax+1) + u (k6_rowmap)
     const int* nrows;   // number of valid cells (compact rows)
-    int dbg;  // diagnostics (env RNNT_K6_DEBUG, never set in production): 1 = builders skip tanh,
-              // 2 = epilogue skips its math (both give wrong losses: timing ablations only), 4 = per-role
-              // barrier-wait cycle counters printed to stderr, 32 = k6_dz_2sm stores dz by per-lane 16-byte
-              // stores instead of TMA tile stores (A/B, correct results).  (No switch inside the builders' loop:
-              // runtime selects there cost ~10 % at p124 -- the tanh.approx opt-in and a load ablation that were
-              // measured this way are recorded in DESIGN.md and removed.)
+    int dbg;  // diagnostics (env RNNT_K6_DEBUG, never set in production): 1 = builders skip tanh (a timing
+              // ablation on the builders' slow path: wrong losses), 4 = per-role barrier-wait cycle counters
+              // printed to stderr.  (No switch inside the hot loops: runtime selects in the builders' loop cost
+              // ~10 % at p124; the tanh.approx opt-in, the load / epilogue-math ablations and k6_dz_2sm's
+              // per-lane dz-store A/B measured that way are recorded in DESIGN.md and removed.)
     unsigned long long* prof;
     float* lse_out;
     double2* lp_out;
@@ -576,10 +575,6 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
                             __syncwarp();
                             if (lane == 0) mbar_arrive_remote(&acc_empty[acc], 0);
                         }
-                    }
-                    if (a.dbg & 2) {
-                        m = fmaxf(m, __uint_as_float(r[0]) + __uint_as_float(r[31]));
-                        continue;
                     }
                     f32x2 zz[16];
 #pragma unroll
@@ -1008,8 +1003,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     if (lane == 0) mbar_arrive_remote(&acc_empty[acc], 0);
                 }
                 dz_chunk<kSB>(a, r, sbias, bq, v0, d.gl, l2, nl, g2, d.sb, d.sy, d.gy, st, lane,
-                              tile * kRowsPerTile + q * 32, rows, static_cast<int64_t>(NT) * kNTile,
-                              (a.dbg & 32) ? nullptr : &dz_map);
+                              tile * kRowsPerTile + q * 32, rows, static_cast<int64_t>(NT) * kNTile, &dz_map);
             }
         }
         if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // the last dz stores are done

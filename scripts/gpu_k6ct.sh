@@ -4,7 +4,7 @@ out=gpurun_out/k6ct.txt; rm -f $out; mkdir -p gpurun_out
 python -c 'import __graft_entry__ as g; g.build()' > gpurun_out/build.log 2>&1 || exit 1
 timeout -s KILL 500 python -m pytest tests/test_joint.py tests/test_canaries.py -q -x -m gpu -p no:cacheprovider > gpurun_out/k6ct_pytest.log 2>&1
 echo "pytest exit $? $(tail -1 gpurun_out/k6ct_pytest.log)" >> $out
-for rep in 1 2 3; do for v in base head 99eae89; do for c in "--mode joint --config p124" "--mode joint --config c3" "--mode joint_grad --config p124" "--mode joint_grad --config c3"; do
+for rep in 1 2 3; do for v in base head; do for c in "--mode joint --config p124" "--mode joint --config c3" "--mode joint_grad --config p124" "--mode joint_grad --config c3"; do
   if [ $v = base ]; then L=""; else L=$PWD/paper_2303_10384_b200/lib/librnnt_b200_$v.so; fi
   if [ $v = 99eae89 ] && [[ "$c" == *joint_grad* ]]; then continue; fi
   RNNT_B200_LIB=$L timeout -s KILL 200 python bench.py $c --no-e2e --no-cpu-baseline 2>/dev/null | python -c "
