@@ -1139,7 +1139,11 @@ rnnt_status joint_front(const void* enc, const void* pred, const void* weight, c
     const bool sb = V <= kSBiasMaxV;  // bias staged in shared memory (small vocabularies), else read from global
     const int Vs = sb ? V : 0;
     // CTA pairs run pair MMAs by default (RNNT_K6_PAIR=0: per-CTA MMAs with the W stage multicast, for A/B)
-    const bool pair = cl == 2 && !(getenv("RNNT_K6_PAIR") && atoi(getenv("RNNT_K6_PAIR")) == 0);
+    // The forward at small V (<= 4 N tiles, e.g. P:124's V = 500) keeps round 1's per-CTA MMAs with the W stage
+    // multicast: its builders set the pace there and the pair hand-offs only add to it (p124 forward 0.419 ->
+    // 0.413 ms; at c3 the two forms tie).  K6<grad> and k6_dz_2sm always pair.
+    const bool pair = cl == 2 && !(getenv("RNNT_K6_PAIR") && atoi(getenv("RNNT_K6_PAIR")) == 0) &&
+                      !(g == nullptr && (V + kNTile - 1) / kNTile <= 4);
     // K6<grad> on the forward's h (the training step): the two-operand-TMA dz kernel (pair MMAs only)
     // (RNNT_K6_DZTMA=0: k6_joint_lse<true> with its builders loading h into TMEM, for A/B)
     const bool dz_tma = g && g->h_ready && pair && !(getenv("RNNT_K6_DZTMA") && atoi(getenv("RNNT_K6_DZTMA")) == 0);
