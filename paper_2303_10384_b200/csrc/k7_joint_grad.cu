@@ -296,9 +296,27 @@ __global__ void __launch_bounds__(128) k7_pred_sum(const float* __restrict__ par
     const int T = n ? T_b[b] : 0, U = n ? U_b[b] : -1;
     const int nch = (u <= U) ? (T + tc - 1) / tc : 0;
     for (int c = threadIdx.x * 4; c < H; c += blockDim.x * 4) {
+        // chunk order kept (deterministic); eight loads in flight before their adds (a chain of dependent global
+        // loads otherwise)
+        auto at = [&](int ch) {
+            return __ldcs(reinterpret_cast<const float4*>(part + ((static_cast<int64_t>(ch) * B + b) * (Umax + 1) + u) * H + c));
+        };
         float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int ch = 0; ch < nch; ++ch) {
-            const float4 p = __ldcs(reinterpret_cast<const float4*>(part + ((static_cast<int64_t>(ch) * B + b) * (Umax + 1) + u) * H + c));
+        int ch = 0;
+        for (; ch + 8 <= nch; ch += 8) {
+            float4 p[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) p[k] = at(ch + k);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                o.x += p[k].x;
+                o.y += p[k].y;
+                o.z += p[k].z;
+                o.w += p[k].w;
+            }
+        }
+        for (; ch < nch; ++ch) {
+            const float4 p = at(ch);
             o.x += p.x;
             o.y += p.y;
             o.z += p.z;
