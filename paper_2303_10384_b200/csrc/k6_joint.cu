@@ -151,6 +151,32 @@ __device__ __forceinline__ float2 tanh2_mufu(float x0, float x1) {
     const float2 d = upk(fadd2(pk(ex2(y.x), ex2(y.y)), pk(1.f, 1.f)));
     return upk(ffma2(pk(rcp_approx(d.x), rcp_approx(d.y)), pk(-2.f, -2.f), pk(1.f, 1.f)));
 }
+// The same tanh with the reciprocal on the FMA pipe instead of MUFU: the builders' two MUFU ops per element
+// and the epilogue's ex2 per logit share one MUFU pipe (16 results / clk / SM), which sets K6's pace at small V
+// (one MUFU op less per element, tanh.approx, was 20 % faster at p124).  r0 = 0x7EF311C3 - bits(d) is within 5 %
+// of 1 / d on d in [1, 2^64 + 1] (y clamped at 64 so d stays finite and r0 positive), three Newton steps
+// r += r (1 - d r) bring it to 9e-8 relative: |tanh error| 2.3e-7, as the MUFU form's.
+__device__ __forceinline__ float2 tanh2_newton(float x0, float x1) {
+    const float2 y = upk(fmul2(pk(x0, x1), pk(2.8853900817779268f, 2.8853900817779268f)));
+    const float2 d = upk(fadd2(pk(ex2(fminf(y.x, 64.f)), ex2(fminf(y.y, 64.f))), pk(1.f, 1.f)));
+    const float2 nd = make_float2(-d.x, -d.y);
+    float2 r = make_float2(__int_as_float(0x7EF311C3 - __float_as_int(d.x)),
+                           __int_as_float(0x7EF311C3 - __float_as_int(d.y)));
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const float2 e = upk(ffma2(pk(nd.x, nd.y), pk(r.x, r.y), pk(1.f, 1.f)));
+        r = upk(ffma2(pk(r.x, r.y), pk(e.x, e.y), pk(r.x, r.y)));
+    }
+    return upk(ffma2(pk(r.x, r.y), pk(-2.f, -2.f), pk(1.f, 1.f)));
+}
+// words (of the 4 per 16-byte item) whose tanh takes the Newton reciprocal in the loss-only forward; the rest
+// use MUFU rcp.  A/B (scripts/gpu_k6nr.sh, profiles/r02_g/k6nr.txt), K6 at p124: 0 words 0.414 ms, 1 word
+// 0.4015, 2 words 0.411, 4 words 0.437 -- past one word the FMA-pipe work costs more than the MUFU time it
+// frees.  The training step's forward (h stored from the builders) was 1 % slower with 1 word: it keeps MUFU.
+#ifndef RNNT_K6_NR
+#define RNNT_K6_NR 1
+#endif
+static_assert(RNNT_K6_NR >= 0 && RNNT_K6_NR <= 4, "Newton words per item");
 // z[k] for a per-lane k in [0, 32) without local memory: a 5-level select tree (31 FSEL) instead of 32
 // compare-and-move pairs.
 __device__ __forceinline__ float select32(const float (&z)[32], int k) {
@@ -717,7 +743,8 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
                     for (int e = 0; e < 4; ++e) {
                         const float2 x = unpack_bf16x2(fw[e]), y = unpack_bf16x2(gw[e]);
                         const float2 xs = upk(fadd2(pk(x.x, x.y), pk(y.x, y.y)));
-                        const float2 h = tanh2_mufu(xs.x, xs.y);
+                        constexpr int kNR = (kGrad || kStore) ? 0 : RNNT_K6_NR;
+                        const float2 h = e < 4 - kNR ? tanh2_mufu(xs.x, xs.y) : tanh2_newton(xs.x, xs.y);
                         ow[e] = kFast ? pack_bf16x2(h.x, h.y)
                                       : !ok[j] ? 0u : (a.dbg & 1) ? (fw[e] ^ gw[e]) : pack_bf16x2(h.x, h.y);
                     }

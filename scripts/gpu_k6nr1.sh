@@ -1,0 +1,13 @@
+#!/bin/bash
+# confirmation: Newton reciprocal in 1 of 4 words in the loss-only K6 forward only (working tree) vs HEAD
+out=gpurun_out/k6nr1.txt; rm -f $out; mkdir -p gpurun_out
+python -c 'import __graft_entry__ as g; g.build()' > gpurun_out/build.log 2>&1 || exit 1
+timeout -s KILL 500 python -m pytest tests/test_joint.py tests/test_canaries.py -q -x -m gpu -p no:cacheprovider > gpurun_out/k6nr1_pytest.log 2>&1
+echo "pytest exit $? $(tail -1 gpurun_out/k6nr1_pytest.log)" >> $out
+for rep in 1 2 3; do for v in head base; do for c in "--mode joint --config p124" "--mode joint --config c3" "--mode joint_grad --config p124"; do
+  if [ $v = base ]; then L=""; else L=$PWD/paper_2303_10384_b200/lib/librnnt_b200_$v.so; fi
+  RNNT_B200_LIB=$L timeout -s KILL 200 python bench.py $c --no-e2e --no-cpu-baseline 2>/dev/null | python -c "
+import json,sys
+d=json.loads(sys.stdin.read().strip().splitlines()[-1])
+print('$v', '$c', round(d['value']), round(d['ms_per_step'],4), {k: round(x,4) for k,x in d.get('kernels_ms',{}).items()}, d['clocks']['sm_mhz'])" >> $out
+done; done; done
