@@ -103,3 +103,31 @@ def test_half_loss_equals_fp32_loss_on_widened_input(rb):
     l32, _ = rb.loss(z16.float(), pb["targets"], pb["logit_lens"], pb["target_lens"], 0, "rnnt", grads=False)
     torch.cuda.synchronize()
     assert torch.equal(l16, l32)
+
+
+@pytest.mark.parametrize("dtype", (torch.bfloat16, torch.float16), ids=("bf16", "fp16"))
+@pytest.mark.parametrize("blank", (0, 3, 496, 499))
+def test_half_v8_4_piece_and_alignment(rb, dtype, blank):
+    """V % 8 == 4 rows (P:124's V = 500, 64-bit vectors): rows alternate between 16-byte aligned starts and
+    starts 8 bytes past one; blank and labels at both row ends; logits based 16-byte aligned and 8 bytes past it;
+    grads new, in place, and preallocated at the other alignment mod 16."""
+    B, T, U, V = 3, 21, 9, 500
+    cfg = workloads.random_config(B, T, U, V, seed=blank + 31, blank=blank)
+    pb = workloads.problem(cfg)
+    # labels on the piece positions too (a label never equals the blank)
+    tg = pb["targets"].copy()
+    for k, y in enumerate((0, 1, 2, 3, 496, 497, 498, 499)):
+        if y != blank:
+            tg[:, k % U] = y
+    pb["targets"] = tg
+    for off in (0, 4):  # elements: 0 -> 16-byte aligned base, 4 -> 8 bytes past
+        flat = torch.empty(pb["logits"].numel() + 8, dtype=dtype, device="cuda")
+        z = flat[off:off + pb["logits"].numel()].view(pb["logits"].shape)
+        z.copy_(pb["logits"].to(dtype).cuda())
+        _check(rb, pb, "rnnt", dtype, z16=z)
+        zi = z.clone() if off == 0 else flat.clone()[off:off + z.numel()].view(z.shape)
+        _check(rb, pb, "rnnt", dtype, z16=zi, grads="inplace")
+        gflat = torch.empty(z.numel() + 8, dtype=dtype, device="cuda")
+        gout = gflat[4 - off:4 - off + z.numel()].view(z.shape)  # the other alignment mod 16
+        _, g = _check(rb, pb, "rnnt", dtype, z16=z, grads=gout)
+        assert g.data_ptr() == gout.data_ptr()
