@@ -86,7 +86,9 @@ constexpr int kTC = 8;
 // K9's SM cap when K7 runs beside it (K7 fills the rest).  0 = sequential (the default): A/B on B200, 3
 // alternating reps of 60-step training steps (scripts/gpu_k9ovl2.sh): c3 7.29 ms sequential, 7.19 with K9 on
 // 96 SMs, 7.25 on 112; p124 2.13 sequential, 2.14 / 2.16 -- within the power-capped clock's noise, so the
-// simpler schedule stays.  RNNT_K9_CTAS=n turns the overlap on.
+// simpler schedule stays.  Re-measured on the round-2 kernels (scripts/gpu_k9ovl3.sh, profiles/r02_g/k9ovl3.txt,
+// 3 reps): c3 6.98-7.05 ms sequential, 7.02-7.05 on 96 SMs, 7.06 on 112, 7.09-7.12 on 128; p124 1.94-1.95,
+// 1.95-1.98, 1.98-1.99, 1.99-2.03 -- sequential stays.  RNNT_K9_CTAS=n turns the overlap on.
 constexpr int kK9OverlapCtas = 0;
 
 template <bool kPre>
