@@ -154,11 +154,12 @@ __device__ __forceinline__ float2 tanh2_mufu(float x0, float x1) {
 // The same tanh with the reciprocal on the FMA pipe instead of MUFU: the builders' two MUFU ops per element
 // and the epilogue's ex2 per logit share one MUFU pipe (16 results / clk / SM), which sets K6's pace at small V
 // (one MUFU op less per element, tanh.approx, was 20 % faster at p124).  r0 = 0x7EF311C3 - bits(d) is within 5 %
-// of 1 / d on d in [1, 2^64 + 1] (y clamped at 64 so d stays finite and r0 positive), three Newton steps
-// r += r (1 - d r) bring it to 9e-8 relative: |tanh error| 2.3e-7, as the MUFU form's.
+// of 1 / d on d in [1, 2^64 + 1] (y clamped at 64 so d stays finite and r0 positive; the clamp is a compare and
+// select, not fminf, so that a NaN input stays NaN as in the MUFU form), three Newton steps r += r (1 - d r)
+// bring it to 9e-8 relative: |tanh error| 2.3e-7, as the MUFU form's.
 __device__ __forceinline__ float2 tanh2_newton(float x0, float x1) {
     const float2 y = upk(fmul2(pk(x0, x1), pk(2.8853900817779268f, 2.8853900817779268f)));
-    const float2 d = upk(fadd2(pk(ex2(fminf(y.x, 64.f)), ex2(fminf(y.y, 64.f))), pk(1.f, 1.f)));
+    const float2 d = upk(fadd2(pk(ex2(y.x > 64.f ? 64.f : y.x), ex2(y.y > 64.f ? 64.f : y.y)), pk(1.f, 1.f)));
     const float2 nd = make_float2(-d.x, -d.y);
     float2 r = make_float2(__int_as_float(0x7EF311C3 - __float_as_int(d.x)),
                            __int_as_float(0x7EF311C3 - __float_as_int(d.y)));

@@ -90,6 +90,25 @@ def test_joint_loss_matches_oracle(rb, shape, variant):
     _case(rb, B, T, U, H, V, seed=sum(shape) % 97 + 3, variant=variant)
 
 
+def test_joint_nan_input_propagates(rb):
+    """A NaN in one encoder element makes the loss of exactly the utterance it belongs to non-finite (the
+    path reports -inf there; a loss is otherwise >= 0), whichever of the 8 columns of a 16-byte item it sits in
+    (the builders take tanh's reciprocal from MUFU for some of an item's words and from Newton steps for others:
+    a clamp that dropped the NaN would give a finite, wrong loss); the other utterances' losses do not change."""
+    B, T, U, H, V = 3, 12, 5, 256, 200
+    cfg = workloads.random_config(B, T, U, V, seed=41, variant="rnnt", variable=False)
+    T_b, U_b = workloads.lengths(cfg)
+    y = workloads.targets(cfg, U_b)
+    enc, pred, W, b = workloads.joint_inputs(B, T, U, H, V, seed=41)
+    ref = rb.rnnt_joint_loss(enc.cuda(), pred.cuda(), W.cuda(), b.cuda(), y, T_b, U_b, 0, "rnnt").cpu()
+    for col in range(8):
+        e = enc.clone()
+        e[1, 3, 64 + col] = float("nan")
+        l = rb.rnnt_joint_loss(e.cuda(), pred.cuda(), W.cuda(), b.cuda(), y, T_b, U_b, 0, "rnnt").cpu()
+        assert not torch.isfinite(l[1]), (col, l)
+        assert torch.equal(l[[0, 2]], ref[[0, 2]]), col
+
+
 def test_joint_blank_last_no_bias_many_tiles(rb):
     # > 148 row tiles (every CTA loops), ragged last tile, blank = V-1, no bias
     _case(rb, 4, 120, 40, 384, 256, seed=17, variant="rnnt", blank=255, variable=False, bias=False)
