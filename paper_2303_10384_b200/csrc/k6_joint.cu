@@ -659,8 +659,9 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
                 const int64_t urow = static_cast<int64_t>(b) * cells + t * (a.Umax + 1) + u;
                 a.lse_out[urow] = lse;
                 const bool ybad = (u < U) && (yv < 0 || yv >= a.V || yv == a.blank);
-                const float xb = zb - lse;
-                const float xy = (u < U) ? (ybad ? __int_as_float(0x7fc00000) : zy - lse) : -INFINITY;
+                float xb = zb - lse;
+                float xy = (u < U) ? (ybad ? __int_as_float(0x7fc00000) : zy - lse) : -INFINITY;
+                nan_to_inf(xb, xy, ybad);
                 const int64_t diag = static_cast<int64_t>(b) * (a.Tmax + a.Umax) + (t + u);
                 a.lp_out[diag * (a.Umax + 1) + u] = make_double2(xb, xy);
             }

@@ -91,8 +91,8 @@ def test_joint_loss_matches_oracle(rb, shape, variant):
 
 
 def test_joint_nan_input_propagates(rb):
-    """A NaN in one encoder element makes the loss of exactly the utterance it belongs to non-finite (the
-    path reports -inf there; a loss is otherwise >= 0), whichever of the 8 columns of a 16-byte item it sits in
+    """A NaN in one encoder element makes the loss of exactly the utterance it belongs to NaN (R12),
+    whichever of the 8 columns of a 16-byte item it sits in
     (the builders take tanh's reciprocal from MUFU for some of an item's words and from Newton steps for others:
     a clamp that dropped the NaN would give a finite, wrong loss); the other utterances' losses do not change."""
     B, T, U, H, V = 3, 12, 5, 256, 200
@@ -105,7 +105,24 @@ def test_joint_nan_input_propagates(rb):
         e = enc.clone()
         e[1, 3, 64 + col] = float("nan")
         l = rb.rnnt_joint_loss(e.cuda(), pred.cuda(), W.cuda(), b.cuda(), y, T_b, U_b, 0, "rnnt").cpu()
-        assert not torch.isfinite(l[1]), (col, l)
+        assert torch.isnan(l[1]), (col, l)
+        assert torch.equal(l[[0, 2]], ref[[0, 2]]), col
+
+
+def test_joint_grad_nan_input(rb):
+    """The training step with a NaN in one encoder element: that utterance's loss is NaN, the other utterances'
+    losses are bit-identical to the run without it."""
+    B, T, U, H, V = 3, 12, 5, 256, 200
+    cfg = workloads.random_config(B, T, U, V, seed=42, variant="rnnt", variable=False)
+    T_b, U_b = workloads.lengths(cfg)
+    y = workloads.targets(cfg, U_b)
+    enc, pred, W, b = workloads.joint_inputs(B, T, U, H, V, seed=42)
+    ref = rb.rnnt_joint_loss_grad(enc.cuda(), pred.cuda(), W.cuda(), b.cuda(), y, T_b, U_b, 0, "rnnt")[0].cpu()
+    for col in (0, 7):
+        e = enc.clone()
+        e[1, 3, 64 + col] = float("nan")
+        l = rb.rnnt_joint_loss_grad(e.cuda(), pred.cuda(), W.cuda(), b.cuda(), y, T_b, U_b, 0, "rnnt")[0].cpu()
+        assert torch.isnan(l[1]), (col, l)
         assert torch.equal(l[[0, 2]], ref[[0, 2]]), col
 
 

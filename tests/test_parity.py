@@ -175,6 +175,27 @@ def test_degenerate_lengths(rb, variant):
     _assert_close(*_gpu(rb, pb, variant), *_oracle(pb, variant), "degenerate")
 
 
+@pytest.mark.parametrize("dtype", (torch.float32, torch.bfloat16), ids=("fp32", "bf16"))
+@pytest.mark.parametrize("where", ("blank", "label", "other"))
+def test_nan_logit_in_valid_cell(rb, dtype, where):
+    """A NaN logit in a valid cell of utterance 1 -- at the blank, at the cell's label or elsewhere in the row --
+    gives that utterance a NaN loss and zero gradients (R12, as for invalid targets); the other
+    utterances' losses and gradients are bit-identical to the run without it (rows never share data)."""
+    cfg = workloads.random_config(3, 20, 8, 136, seed=5, variable=False)
+    pb = workloads.problem(cfg)
+    z = pb["logits"].to(dtype)
+    t, u = 4, 2
+    v = {"blank": pb["blank"], "label": int(pb["targets"][1, u]), "other": 77}[where]
+    zn = z.clone()
+    zn[1, t, u, v] = float("nan")
+    l0, g0 = rb.loss(z.cuda(), pb["targets"], pb["logit_lens"], pb["target_lens"], pb["blank"], "rnnt")
+    l1, g1 = rb.loss(zn.cuda(), pb["targets"], pb["logit_lens"], pb["target_lens"], pb["blank"], "rnnt")
+    l0, l1, g0, g1 = l0.cpu(), l1.cpu(), g0.cpu(), g1.cpu()
+    assert torch.isnan(l1[1]), l1
+    assert not g1[1].float().any()
+    assert torch.equal(l1[[0, 2]], l0[[0, 2]]) and torch.equal(g1[[0, 2]], g0[[0, 2]])
+
+
 @pytest.mark.parametrize("variant", VARIANTS)
 def test_nan_padding_never_read(rb, variant):
     """NaN in every padded cell: losses match and padded grads are exactly zero (K1 never reads them)."""
