@@ -36,7 +36,8 @@
  *             reduction) inside the gradient pass, at no extra memory traffic.
  *   - Data-dependent errors are NOT reported synchronously (that would need a device sync): an utterance
  *     whose lengths or targets are out of range gets loss = NaN and all-zero grads.  An utterance whose
- *     lattice has no path of non-zero probability (e.g. -inf logits) gets loss = +inf and zero grads.
+ *     lattice has no path of non-zero probability (e.g. -inf logits) gets loss = +inf and zero grads.  An
+ *     utterance with a NaN (or +inf) logit in a valid cell gets loss = NaN and zero grads (R12).
  *   - Argument errors detectable on the host (sizes, null pointers, workspace size, overlap) are returned
  *     as a status before anything is launched.
  *   - Limits: Umax + 1 <= 4096 (one CTA per utterance and direction in the alpha/beta wavefront, up to 8
