@@ -122,15 +122,11 @@ __device__ __forceinline__ float max3(float a, float b, float c) {
 // log(e^a + e^b).  fp64 difference and max, fp32 MUFU correction.  -inf operands need no branch: if one
 // side is -inf the correction is exactly 0; if both are, diff is NaN, fminf(NaN, 0) = 0 and the result is
 // -inf + ln 2 = -inf.
-// A NaN in a row's logits (R12) makes its lse NaN, but K2's LSE below can drop a NaN operand (its
-// max is a compare and select), which would leave that utterance's loss finite.  The Populate step therefore
-// hands K2 +inf instead: every LSE carries +inf through to log P = +inf, which K2 reports as a NaN loss and the
-// gradient passes treat as a non-finite log P (zero gradients), as for invalid targets.  (The NaN written for an
-// invalid label stays: K2 checks the labels itself.)
-__device__ __forceinline__ void nan_to_inf(float& xb, float& xy, bool ybad) {
-    if (xb != xb) xb = INFINITY;
-    if (xy != xy && !ybad) xy = INFINITY;
-}
+// kNanArc: a NaN in a row's logits (R12) makes its lse NaN, but K2's LSE below can drop a NaN operand
+// (its max is a compare and select), which would leave that utterance's loss finite.  The Populate step (K1 / K6)
+// therefore hands K2 +inf arc scores for such a row: every LSE carries +inf through to log P = +inf, which K2
+// reports as a NaN loss and the gradient passes treat as a non-finite log P (zero gradients), as for invalid
+// targets.  (A NaN label score for an invalid label stays: K2 checks the labels itself.)
 
 __device__ __forceinline__ double lse2f(double a, double b) {
     const double diff = a - b;

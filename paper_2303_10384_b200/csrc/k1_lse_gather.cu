@@ -138,10 +138,12 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32, 4)
         if (lse == -INFINITY) {  // an all -inf row forbids its arcs (reading R12)
             xb = -INFINITY;
             xy = -INFINITY;
+        } else if (lse != lse) {  // a NaN in the row: +inf arc scores (common.cuh kNanArc)
+            xb = INFINITY;
+            xy = (u < U) ? INFINITY : -INFINITY;
         } else {
             xb = zb - lse;
             xy = (u < U) ? (ybad ? __int_as_float(0x7fc00000) : zy - lse) : -INFINITY;
-            nan_to_inf(xb, xy, ybad);
         }
         const int64_t diag = static_cast<int64_t>(b) * (Tmax + Umax) + (t + u);
         if (lp_out) lp_out[diag * Up1 + u] = make_double2(xb, xy);
@@ -278,11 +280,13 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32, 3)
         if (lse == -INFINITY) {  // an all -inf row forbids its arcs (reading R12)
             xb = -INFINITY;
             xy = -INFINITY;
+        } else if (lse != lse) {  // a NaN in the row: +inf arc scores (common.cuh kNanArc)
+            xb = INFINITY;
+            xy = (u < U) ? INFINITY : -INFINITY;
         } else {
             xb = (k ? zb[1] : zb[0]) - lse;
             xy = (u < U) ? ((k ? ybad[1] : ybad[0]) ? __int_as_float(0x7fc00000) : (k ? zy[1] : zy[0]) - lse)
                          : -INFINITY;
-            nan_to_inf(xb, xy, k ? ybad[1] : ybad[0]);
         }
         const int64_t diag = static_cast<int64_t>(b) * (Tmax + Umax) + (t + u);
         if (lp_out) lp_out[diag * Up1 + u] = make_double2(xb, xy);
@@ -395,10 +399,12 @@ __global__ void __launch_bounds__(kRowWarpsPerBlock * 32)
         if (lse == -INFINITY) {  // an all -inf row forbids its arcs (reading R12)
             xb = -INFINITY;
             xy = -INFINITY;
+        } else if (lse != lse) {  // a NaN in the row: +inf arc scores (common.cuh kNanArc)
+            xb = INFINITY;
+            xy = (u < U) ? INFINITY : -INFINITY;
         } else {
             xb = zb - lse;
             xy = (u < U) ? (ybad ? __int_as_float(0x7fc00000) : zy - lse) : -INFINITY;
-            nan_to_inf(xb, xy, ybad);
         }
         const int64_t diag = static_cast<int64_t>(b) * (Tmax + Umax) + (t + u);
         if (lp_out) lp_out[diag * Up1 + u] = make_double2(xb, xy);

@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(kMaxThreads)
                 double total = a + xb;  // terminating blank (T-1,U) -> F
                 if (kVariant == kAllowIgnore) total = lse2f(total, skip);
                 logp[b] = total;
-                // log P = +inf only from +inf arc scores: a NaN in the utterance's logits (common.cuh nan_to_inf)
+                // log P = +inf only from +inf arc scores: a NaN in the utterance's logits (common.cuh kNanArc)
                 losses[b] = total == INFINITY ? __int_as_float(0x7fc00000) : static_cast<float>(-total);
             }
         }

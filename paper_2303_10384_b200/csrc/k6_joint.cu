@@ -661,7 +661,10 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
                 const bool ybad = (u < U) && (yv < 0 || yv >= a.V || yv == a.blank);
                 float xb = zb - lse;
                 float xy = (u < U) ? (ybad ? __int_as_float(0x7fc00000) : zy - lse) : -INFINITY;
-                nan_to_inf(xb, xy, ybad);
+                if (lse != lse) {  // a NaN in the row: +inf arc scores (common.cuh kNanArc)
+                    xb = INFINITY;
+                    xy = (u < U) ? INFINITY : -INFINITY;
+                }
                 const int64_t diag = static_cast<int64_t>(b) * (a.Tmax + a.Umax) + (t + u);
                 a.lp_out[diag * (a.Umax + 1) + u] = make_double2(xb, xy);
             }
