@@ -46,7 +46,9 @@ __global__ void __launch_bounds__(256) l2_arc_weights(const float* __restrict__ 
         if (v >= 0) {
             const int64_t row = (static_cast<int64_t>(b) * Tmax + L.t[a]) * Up1 + L.u[a];
             const float l = lse[row];
-            x = (l == -INFINITY) ? -INFINITY : logits[row * V + v] - l;
+            // a NaN in the row (lse NaN): +inf, as the grid path's Populate (common.cuh kNanArc), so that log P
+            // becomes +inf and the loss NaN instead of a NaN operand being dropped by an LSE
+            x = (l == -INFINITY) ? -INFINITY : (l != l) ? INFINITY : logits[row * V + v] - l;
         }
         w[a] = x;
     }
@@ -233,7 +235,7 @@ __global__ void __launch_bounds__(kL3Threads) l3_forward_backward(Lat L, const S
     if (!fwd && tid == 0) {
         const double lP = __ldcg(beta + s_start);
         logp[b] = lP;
-        losses[b] = static_cast<float>(-lP);
+        losses[b] = lP == INFINITY ? __int_as_float(0x7fc00000) : static_cast<float>(-lP);  // +inf: a NaN input
     }
 }
 

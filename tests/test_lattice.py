@@ -117,3 +117,20 @@ def test_row_index_path_is_deterministic_and_matches_atomic_path(rb, lat):
     assert torch.equal(g1, g2) and torch.equal(l1, l2)
     assert torch.equal(l1, l3)
     assert (g1 - g3).abs().max().item() <= 1e-6
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_nan_logit_gives_nan_loss(rb, lat, variant):
+    """A NaN logit in a valid cell of utterance 1 gives it a NaN loss and zero gradients (R12), as on
+    the grid path; the other utterances are bit-identical to the run without it."""
+    cfg = workloads.random_config(3, 20, 8, 64, seed=7, variant=variant, variable=False)
+    pb = workloads.problem(cfg)
+    L = lat.grid_lattices(pb["logit_lens"], pb["target_lens"], pb["targets"], 0, variant)
+    z = pb["logits"].clone()
+    z[1, 5, 3, 9] = float("nan")
+    l0, g0 = rb.rnnt_lattice_loss(pb["logits"].cuda(), L, pb["logit_lens"], pb["target_lens"])
+    l1, g1 = rb.rnnt_lattice_loss(z.cuda(), L, pb["logit_lens"], pb["target_lens"])
+    l0, l1, g0, g1 = l0.cpu(), l1.cpu(), g0.cpu(), g1.cpu()
+    assert torch.isnan(l1[1]), l1
+    assert not g1[1].any()
+    assert torch.equal(l1[[0, 2]], l0[[0, 2]]) and torch.equal(g1[[0, 2]], g0[[0, 2]])
