@@ -176,8 +176,10 @@ __global__ void __launch_bounds__(kMaxThreads)
     __syncthreads();
     if (u != 0) return;
     const double total = s_best;
-    best_out[b] = static_cast<float>(total);
-    if (total == -INFINITY) {
+    // +inf only from +inf arc scores, i.e. a NaN in the utterance's logits (common.cuh kNanArc): reported as an
+    // invalid utterance (NaN, frames and span -1)
+    best_out[b] = total == INFINITY ? __int_as_float(0x7fc00000) : static_cast<float>(total);
+    if (total == -INFINITY || total == INFINITY) {
         if (span) span[2 * b] = span[2 * b + 1] = -1;
         return;
     }

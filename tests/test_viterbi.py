@@ -110,3 +110,18 @@ def test_viterbi_invalid_targets(rb):
     torch.cuda.synchronize()
     assert math.isfinite(best[0].item()) and math.isnan(best[1].item())
     assert (frames[1] == -1).all() and (span[1] == -1).all()
+
+
+def test_viterbi_nan_logit(rb):
+    """A NaN logit in a valid cell of utterance 1: NaN best score, frames and span -1 (as an invalid utterance,
+    DESIGN.md R12); the other utterances' results are unchanged."""
+    cfg = workloads.random_config(3, 16, 6, 40, seed=9, variable=False)
+    pb = workloads.problem(cfg)
+    z = pb["logits"].clone()
+    z[1, 4, 2, 7] = float("nan")
+    r0 = rb.rnnt_viterbi(pb["logits"].cuda(), pb["targets"], pb["logit_lens"], pb["target_lens"], 0, "rnnt")
+    r1 = rb.rnnt_viterbi(z.cuda(), pb["targets"], pb["logit_lens"], pb["target_lens"], 0, "rnnt")
+    (b0, f0, s0), (b1, f1, s1) = [[t.cpu() for t in r] for r in (r0, r1)]
+    assert math.isnan(b1[1].item()) and (f1[1] == -1).all() and (s1[1] == -1).all()
+    assert torch.equal(b1[[0, 2]], b0[[0, 2]]) and torch.equal(f1[[0, 2]], f0[[0, 2]])
+    assert torch.equal(s1[[0, 2]], s0[[0, 2]])
