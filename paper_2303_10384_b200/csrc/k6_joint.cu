@@ -152,8 +152,8 @@ __device__ __forceinline__ float2 tanh2_mufu(float x0, float x1) {
     return upk(ffma2(pk(rcp_approx(d.x), rcp_approx(d.y)), pk(-2.f, -2.f), pk(1.f, 1.f)));
 }
 // The same tanh with the reciprocal on the FMA pipe instead of MUFU: the builders' two MUFU ops per element
-// and the epilogue's ex2 per logit share one MUFU pipe (16 results / clk / SM), which sets K6's pace at small V
-// (one MUFU op less per element, tanh.approx, was 20 % faster at p124).  r0 = 0x7EF311C3 - bits(d) is within 5 %
+// and the epilogue's ex2 per logit share one MUFU pipe (16 results / clk / SM; ncu at p124: 64 % busy), which
+// weighs on K6's pace at small V (one MUFU op less per element, tanh.approx, was 20 % faster at p124).  r0 = 0x7EF311C3 - bits(d) is within 5 %
 // of 1 / d on d in [1, 2^64 + 1] (y clamped at 64 so d stays finite and r0 positive; the clamp is a compare and
 // select, not fminf, so that a NaN input stays NaN as in the MUFU form), three Newton steps r += r (1 - d r)
 // bring it to 9e-8 relative: |tanh error| 2.3e-7, as the MUFU form's.
